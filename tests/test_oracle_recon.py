@@ -1,0 +1,170 @@
+"""Pins of the oracle's reconstructions against exactly integrated
+polynomials (independent 1-D antiderivatives), rank checks and limiter limits."""
+import numpy as np
+import pytest
+
+import oracle
+
+
+def _avg1(k, a, b):
+    """average of x^k over [a, b]"""
+    return (b ** (k + 1) - a ** (k + 1)) / ((k + 1) * (b - a))
+
+
+def poly_case(dim, deg, seed, n=5, h=(0.3, 0.25, 0.2)):
+    """Random polynomial of total degree <= deg over the active axes; exact cell averages and exact
+    cell-averaged gradients on an n^dim grid.  Returns (prob, Q, G, f, grad f)."""
+    rng = np.random.default_rng(seed)
+    terms = []
+    for i in range(deg + 1):
+        for j in range(deg + 1 - i):
+            for k in range(deg + 1 - i - j):
+                if (dim < 2 and j) or (dim < 3 and k):
+                    continue
+                terms.append(((i, j, k), rng.normal()))
+    nn = [n if a < dim else 1 for a in range(3)]
+    hh = [h[a] for a in range(3)]
+    lo = [0.0, 0.0, 0.0]
+    hi = [nn[a] * hh[a] for a in range(3)]
+    edges = [lo[a] + hh[a] * np.arange(nn[a] + 1) for a in range(3)]
+    Q = np.zeros((5, nn[2], nn[1], nn[0]))
+    G = np.zeros((3, 5, nn[2], nn[1], nn[0]))
+    for (e, c) in terms:
+        A = [np.array([_avg1(e[a], edges[a][q], edges[a][q + 1]) for q in range(nn[a])]) for a in range(3)]
+        D = [np.array([(edges[a][q + 1] ** e[a] - edges[a][q] ** e[a]) / hh[a] for q in range(nn[a])])
+             for a in range(3)]
+        Q[:] += c * (A[2][:, None, None] * A[1][None, :, None] * A[0][None, None, :])[None]
+        G[0] += c * (A[2][:, None, None] * A[1][None, :, None] * D[0][None, None, :])[None]
+        G[1] += c * (A[2][:, None, None] * D[1][None, :, None] * A[0][None, None, :])[None]
+        G[2] += c * (D[2][:, None, None] * A[1][None, :, None] * A[0][None, None, :])[None]
+    # make the five components different (scaled copies) and keep density/pressure positive
+    scale = np.array([1.0, -0.5, 0.25, 0.7, 2.0])
+    Q = Q * scale[:, None, None, None]
+    G = G * scale[None, :, None, None, None]
+
+    def f(x):
+        return sum(c * x[0] ** e[0] * x[1] ** e[1] * x[2] ** e[2] for (e, c) in terms) * scale
+
+    def df(x):
+        out = np.zeros((3, 5))
+        for (e, c) in terms:
+            for a in range(3):
+                if e[a] == 0:
+                    continue
+                ee = list(e)
+                ee[a] -= 1
+                out[a] += c * e[a] * x[0] ** ee[0] * x[1] ** ee[1] * x[2] ** ee[2] * scale
+        return out
+
+    prob = oracle.Problem(n=tuple(nn), lo=tuple(lo), hi=tuple(hi), scheme=1)
+    return prob, Q, G, f, df, hh, [nn[a] // 2 for a in range(3)]
+
+
+@pytest.mark.parametrize("dim,nb,nd", [(3, 34, 63), (2, 14, 26), (1, 4, 5)])
+def test_cls_rank_and_sizes(dim, nb, nd):
+    r = oracle.recon5_matrix(dim)
+    assert r["rank_ok"] and r["nb"] == nb and r["nd"] == nd
+    assert r["nc"] == {3: 18, 2: 8, 1: 2}[dim]
+    # constant data (all differences and derivatives zero) -> zero coefficients: R @ 0 = 0 trivially;
+    # the matrix must reproduce the exact constraints: C @ R[:, :nc] = I (checked via quartic exactness below)
+
+
+@pytest.mark.parametrize("dim,seed", [(3, 0), (3, 1), (2, 2), (1, 3)])
+def test_cls_quartic_exactness(dim, seed):
+    # consistent data from any quartic are reproduced exactly (chi == 1, linear mode)
+    prob, Q, G, f, df, h, c = poly_case(dim, 4, seed)
+    rng = np.random.default_rng(seed + 100)
+    x = rng.uniform(-0.5, 0.5, size=(6, 3))
+    x[:, dim:] = 0.0
+    W, dW, _ = oracle.recon_eval(prob, Q, G, c, x)
+    for q in range(x.shape[0]):
+        xp = [(c[a] + 0.5 + x[q, a]) * h[a] if a < dim else 0.5 * h[a] for a in range(3)]
+        ref, dref = f(xp), df(xp)
+        sc = np.abs(Q).max()
+        assert np.allclose(W[q], ref, rtol=0, atol=1e-11 * sc)
+        assert np.allclose(dW[q][:dim], dref[:dim], rtol=0, atol=1e-10 * np.abs(G).max())
+
+
+def test_cls_quintic_is_not_reproduced():
+    # sanity: the reconstruction is exactly quartic (a degree-5 field is not reproduced)
+    prob, Q, G, f, df, h, c = poly_case(2, 5, 9)
+    x = np.array([[0.5, 0.2, 0.0]])
+    W, dW, _ = oracle.recon_eval(prob, Q, G, c, x)
+    xp = [(c[a] + 0.5 + x[0, a]) * h[a] if a < 2 else 0.5 * h[a] for a in range(3)]
+    assert np.abs(W[0] - f(xp)).max() > 1e-8
+
+
+def test_constant_field_exact():
+    prob, Q, G, f, df, h, c = poly_case(3, 0, 4)
+    x = np.array([[0.5, 0.28, -0.28], [-0.5, 0.1, 0.4]])
+    for nl in (0, 1):
+        prob.nonlinear = nl
+        W, dW, chi = oracle.recon_eval(prob, Q, G, c, x)
+        assert np.array_equal(W, np.broadcast_to(Q[:, 2, 2, 2], W.shape))
+        assert np.all(dW == 0.0)
+
+
+def test_geno_linear_field_is_exact_and_chi_one():
+    # equal smoothness indicators on linear data: omega_m = 1/6, chi = 1, reproduction exact
+    prob, Q, G, f, df, h, c = poly_case(3, 1, 5)
+    prob.nonlinear = 1
+    x = np.array([[0.5, 0.288675, -0.288675], [0.1, -0.5, 0.3]])
+    W, dW, chi = oracle.recon_eval(prob, Q, G, c, x)
+    assert np.all(chi > 1 - 1e-12)
+    for q in range(2):
+        xp = [(c[a] + 0.5 + x[q, a]) * h[a] for a in range(3)]
+        assert np.allclose(W[q], f(xp), atol=1e-12 * np.abs(Q).max())
+
+
+def test_geno_step_is_eno():
+    # a jump at the face between cells 1 and 2 along x: cell 2's reconstruction drops to
+    # the ENO sub-stencils (chi -> 0) and its face values stay within the data range
+    n = 5
+    Q = np.zeros((5, n, n, n))
+    Q[0] = 1.0
+    Q[4] = 2.5
+    Q[0][:, :, 2:] = 2.0
+    Q[4][:, :, 2:] = 5.0
+    G = np.zeros((3, 5, n, n, n))
+    prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(1, 1, 1), scheme=1, nonlinear=1)
+    x = np.array([[-0.5, 0.288675, 0.288675], [0.5, -0.288675, 0.288675], [-0.5, 0.0, 0.0]])
+    W, dW, chi = oracle.recon_eval(prob, Q, G, (2, 2, 2), x)
+    assert chi[0] < 1e-6 and chi[4] < 1e-6
+    # chi ~ 1e-8 at an O(1) jump (R8): the overshoot left is chi * (Gibbs overshoot of P^4)
+    assert np.all(W[:, 0] >= 1.0 - 1e-6) and np.all(W[:, 0] <= 2.0 + 1e-6)
+    # the linear quartic overshoots here (Gibbs); GENO must not
+    prob.nonlinear = 0
+    Wl, _, _ = oracle.recon_eval(prob, Q, G, (2, 2, 2), x)
+    assert Wl[:, 0].min() < 1.0 - 1e-3 or Wl[:, 0].max() > 2.0 + 1e-3
+
+
+def test_gks2_linear_exact_and_venkat():
+    prob, Q, G, f, df, h, c = poly_case(3, 1, 6)
+    prob.scheme = 0
+    x = np.array([[0.5, 0.0, 0.0], [0.0, -0.5, 0.0]])
+    for nl in (0, 1):
+        prob.nonlinear = nl
+        W, dW, phi = oracle.recon_eval(prob, Q, G, c, x)
+        # LS on a uniform stencil reproduces linear fields; Venkatakrishnan gives phi = 1 on monotone linear data
+        assert np.all(np.abs(phi - 1.0) < 1e-12)
+        for q in range(2):
+            xp = [(c[a] + 0.5 + x[q, a]) * h[a] for a in range(3)]
+            assert np.allclose(W[q], f(xp), atol=1e-12 * np.abs(Q).max())
+            assert np.allclose(dW[q], df(xp), atol=1e-11 * np.abs(G).max())
+
+
+def test_venkat_extremum_and_constant():
+    n = 5
+    Q = np.ones((5, n, n, n))
+    Q[4] = 2.5
+    G = np.zeros((3, 5, n, n, n))
+    prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(1, 1, 1), scheme=0, nonlinear=1)
+    W, dW, phi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[0.5, 0, 0]]))
+    assert np.all(phi == 1.0)
+    # strict local maximum in x at cell 2 with asymmetric neighbours -> phi0 < 1
+    Q[0][:, :, 1] = 0.9
+    Q[0][:, :, 2] = 1.3
+    Q[0][:, :, 3] = 1.0
+    W, dW, phi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[0.5, 0, 0]]))
+    assert phi[0] < 1.0
+    assert phi[0] >= 0.0

@@ -1,0 +1,155 @@
+"""Whole-scheme pins of the oracle (SURVEY.md 8(c) C3 / BASELINE north_star):
+uniform-flow preservation, conservation, isentropic-vortex convergence order,
+the exact Riemann solution of a Sod tube, the CFL formula and positivity errors."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from cgks_inputs import double_sod, random_smooth, uniform, vortex, vortex_exact
+from riemann_exact import double_sod_density
+
+
+def _prob(case, **kw):
+    d = case.problem_kwargs()
+    d.update(kw)
+    return oracle.Problem(**d)
+
+
+@pytest.mark.parametrize("scheme,nl,ts", [(1, 0, 2), (1, 1, 2), (0, 0, 1), (0, 1, 2)])
+@pytest.mark.parametrize("n", [(6, 5, 4), (7, 6, 1)])
+def test_uniform_flow_bitwise(scheme, nl, ts, n):
+    c = uniform(n, state=(1.3, 0.4, -0.3, 0.2, 0.9))
+    p = _prob(c, scheme=scheme, nonlinear=nl, time_scheme=ts, mu=1e-3, Pr=0.72)
+    Q, G, t, dt, rc = oracle.run(p, c.Q, c.G, 10)
+    assert rc == 0 and t > 0
+    assert np.array_equal(Q, c.Q)
+    assert np.all(G == 0.0)
+
+
+@pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 1)])
+def test_conservation_periodic(scheme, nl):
+    c = random_smooth((10, 8, 6), seed=3, jump=0.5 if nl else 0.0)
+    p = _prob(c, scheme=scheme, nonlinear=nl, mu=2e-3, Pr=0.72, time_scheme=2)
+    Q, G, t, dt, rc = oracle.run(p, c.Q, c.G, 5)
+    assert rc == 0
+    assert np.abs(Q - c.Q).max() > 1e-6  # the state did evolve
+    for v in range(5):
+        s0 = math.fsum(c.Q[v].ravel())
+        s1 = math.fsum(Q[v].ravel())
+        scale = math.fsum(np.abs(c.Q[v]).ravel())
+        assert abs(s1 - s0) <= 1e-13 * scale, (v, s1 - s0)
+
+
+def _vortex_errors(scheme, ns_list=((20, 10), (40, 24), (80, 57)), T=1.0):
+    errs = []
+    for n, ns in ns_list:
+        c = vortex(n)
+        p = _prob(c, scheme=scheme, time_scheme=2, fixed_dt=T / ns)  # dt ~ h^(5/4)
+        Q, G, t, dt, rc = oracle.run(p, c.Q, c.G, ns)
+        assert rc == 0
+        Qe, _ = vortex_exact(n, t)
+        errs.append((np.abs(Q[0] - Qe[0]).mean(), np.abs(Q[0] - Qe[0]).max()))
+    return np.array(errs)
+
+
+@pytest.mark.slow
+def test_vortex_order_cgks5():
+    # BASELINE north_star: "roughly fifth-order L1/Linf convergence for CGKS-5th" (linear, tau = 0, R18)
+    e = _vortex_errors(1)
+    o1 = np.log2(e[:-1, 0] / e[1:, 0])
+    oinf = np.log2(e[:-1, 1] / e[1:, 1])
+    assert o1[-1] > 4.5 and oinf[-1] > 4.2, (e, o1, oinf)
+    assert e[-1, 0] < 2e-6
+
+
+def test_vortex_order_gks2():
+    # second order for GKS-2nd (S2O4 in time, R22)
+    e = _vortex_errors(0, ns_list=((20, 10), (40, 24), (80, 57)))
+    o1 = np.log2(e[:-1, 0] / e[1:, 0])
+    assert np.all(o1 > 1.8), (e, o1)
+
+
+@pytest.mark.parametrize("scheme,bound", [(0, 0.02), (1, 0.015)])
+def test_double_sod_exact_riemann(scheme, bound):
+    # periodic double-Sod, t = 0.2, 100 cells, L1(rho) against the exact Riemann solution
+    c = double_sod(100)
+    p = _prob(c, scheme=scheme, nonlinear=1, time_scheme=2 if scheme else 1)
+    Q, G, t = c.Q.copy(), c.G.copy(), 0.0
+    while t < 0.2 - 1e-14:
+        dt = min(oracle.dt(p, Q), 0.2 - t)
+        p.fixed_dt = dt
+        Q, G, _, _, rc = oracle.run(p, Q, G, 1)
+        assert rc == 0
+        t += dt
+    x = (np.arange(100) + 0.5) * 0.02
+    exact = double_sod_density(x, 0.2)
+    l1 = np.abs(Q[0, 0, 0] - exact).mean()
+    assert l1 < bound, l1
+    assert Q[0].min() > 0.12 and Q[0].max() < 1.01  # essentially non-oscillatory
+
+
+def test_stage_assembly_matches_s2o4():
+    """Plumbing: one oracle step equals P:315-316 (and P:321-322 for gradients, R24) assembled from
+    the oracle's own stage residuals; a consistency check of the step driver, not of the formula."""
+    c = random_smooth((8, 6, 4), seed=9)
+    p = _prob(c, scheme=1, mu=1e-3, Pr=0.72, time_scheme=2)
+    dt = oracle.dt(p, c.Q)
+    L1, Lt1, Gn1, Gt1 = oracle.stage_residual(p, c.Q, c.G, dt)
+    Qs = c.Q + 0.5 * dt * L1 + dt * dt / 8.0 * Lt1
+    Gs = Gn1 + 0.5 * dt * Gt1
+    L2, Lt2, Gn2, Gt2 = oracle.stage_residual(p, Qs, Gs, dt)
+    Qn1 = c.Q + dt * L1 + dt * dt / 6.0 * (Lt1 + 2.0 * Lt2)
+    Gn1p = Gn1 + dt * Gt2
+    Q, G, t, dto, rc = oracle.run(p, c.Q, c.G, 1)
+    assert dto == dt
+    assert np.allclose(Q, Qn1, rtol=1e-15, atol=1e-15 * np.abs(Q).max())
+    assert np.allclose(G, Gn1p, rtol=1e-15, atol=1e-15 * np.abs(G).max())
+
+
+def test_s1o2_is_time_integral_of_flux():
+    # S1O2: dt L + dt^2/2 dL/dt equals the exact time integral of the linearised flux
+    c = random_smooth((8, 6, 1), seed=4)
+    p = _prob(c, scheme=0, time_scheme=1, mu=1e-3)
+    dt = oracle.dt(p, c.Q)
+    L, Lt, _, _ = oracle.stage_residual(p, c.Q, c.G, dt)
+    Q, _, _, _, rc = oracle.run(p, c.Q, c.G, 1)
+    assert np.allclose(Q, c.Q + dt * L + 0.5 * dt * dt * Lt, rtol=1e-15, atol=1e-15 * np.abs(Q).max())
+
+
+def test_dt_examples():
+    # rho=1, p=1/gamma (c=1), U=0, h=0.5, CFL 0.5 -> dt = 0.25
+    c = uniform((4, 4, 4), state=(1.0, 0.0, 0.0, 0.0, 1.0 / 1.4), L=2.0)
+    p = _prob(c, cfl=0.5)
+    assert abs(oracle.dt(p, c.Q) - 0.25) < 1e-15
+    # viscous bound: h = 0.1, nu = 0.01, CFL 0.3, (almost) no sound -> 0.3 * 0.01 / 0.03 = 0.1
+    c = uniform((4, 4, 4), state=(1.0, 0.0, 0.0, 0.0, 1e-14), L=0.4)
+    p = _prob(c, cfl=0.3, mu=0.01)
+    assert abs(oracle.dt(p, c.Q) - 0.1) < 1e-14
+
+
+def test_positivity_error_code():
+    c = uniform((5, 4, 3))
+    Q = c.Q.copy()
+    Q[0, 1, 2, 3] = -1.0
+    p = _prob(c, scheme=1)
+    _, _, _, _, rc = oracle.run(p, Q, c.G, 1)
+    assert rc == 3
+
+
+@pytest.mark.slow
+def test_tgv_initial_energy_decay():
+    # Incompressible limit (Ma = 0.1): dE_k/dt|_0 = -nu <|omega|^2> = -(1/1600)(3/4);
+    # CGKS-5th at 32^3 must be within 8 % (24^3 gives +17 %, 32^3 +4 %: the gap is resolution, not physics)
+    from cgks_inputs import tgv
+    c = tgv(32)
+    p = _prob(c, scheme=1, time_scheme=2)
+
+    def ek(Q):
+        return (0.5 * (Q[1] ** 2 + Q[2] ** 2 + Q[3] ** 2) / Q[0]).mean()
+
+    Q, G, t, dt, rc = oracle.run(p, c.Q, c.G, 2)
+    assert rc == 0
+    rate = (ek(Q) - ek(c.Q)) / t
+    assert abs(rate / (-0.75 / 1600.0) - 1.0) < 0.08, rate
