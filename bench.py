@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the CGKS-5th hot path on B200 (BASELINE.json metric: CGKS-5th FP64
+cell-updates/s and the fraction of the FP64/HBM roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload tgv128|tgv64|hit128|shock_vortex|vortex40] [--scheme cgks5|gks2]
+
+A step is one full S2O4 time step of CGKS-5th (dt min-reduction + two stages of
+reconstruction, fluxes and update) over the whole grid.  Default workload: the
+128^3 Taylor-Green vortex (BASELINE configs[1], the north_star's roofline case),
+linear CGKS-5th as in the paper's subsonic TGV.  Inputs are synthetic (the
+analytic TGV initial condition) and resident in HBM; the state (335 MB) is larger
+than L2 (126 MB), so no flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the host
+cores on a bounded sample of the same workload (the paper's code is not available;
+this tier's reference arm is the oracle).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "CGKS-5th FP64 cell-updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline"
+
+
+def make_case(name):
+    from cgks_inputs import hit, shock_vortex, tgv, vortex
+    if name == "tgv128":
+        return tgv(128)
+    if name == "tgv64":
+        return tgv(64)
+    if name == "hit128":
+        return hit(128)
+    if name == "shock_vortex":
+        return shock_vortex()
+    if name == "vortex40":
+        return vortex(40)
+    raise ValueError(name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(lr)
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    return rank, ws, lr
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(case_name, scheme, budget_s=20.0):
+    """The oracle as it stands, on the host cores, on a bounded sample of the same workload:
+    the same flow at 32^3 (the per-cell work of a step does not depend on the grid size)."""
+    import oracle
+    from cgks_inputs import tgv
+    oracle.build()
+    c = tgv(32) if case_name.startswith("tgv") else make_case(case_name)
+    if case_name in ("hit128",):
+        from cgks_inputs import hit
+        c = hit(32)
+    prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if scheme == "cgks5" else 0,
+                          time_scheme=2 if scheme == "cgks5" else 1)
+    Q, G = c.Q, c.G
+    steps, t_used = 0, 0.0
+    while t_used < budget_s * 0.5 or steps == 0:
+        t0 = time.perf_counter()
+        Q, G, _, _, rc = oracle.run(prob, Q, G, 1)
+        t_used += time.perf_counter() - t0
+        steps += 1
+        if rc or t_used > budget_s:
+            break
+    cores = oracle.max_threads()
+    return {"value": c.ncell * steps / t_used, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"{c.name} {c.n[0]}x{c.n[1]}x{c.n[2]}, {steps} step(s), {t_used:.1f} s, "
+                      f"OpenMP threads={cores}"}
+
+
+def run_reference(args, rank, ws):
+    if rank != 0:
+        return 0
+    cb = cpu_baseline(args.workload, args.scheme, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
+    # the reference arm: W untimed + K timed oracle steps on the bounded sample
+    import oracle
+    from cgks_inputs import tgv
+    c = tgv(24) if args.workload.startswith("tgv") else make_case(args.workload)
+    prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if args.scheme == "cgks5" else 0,
+                          time_scheme=2 if args.scheme == "cgks5" else 1)
+    Q, G = c.Q, c.G
+    for _ in range(args.warmup):
+        Q, G, _, _, _ = oracle.run(prob, Q, G, 1)
+    t0 = time.perf_counter()
+    Q, G, _, _, _ = oracle.run(prob, Q, G, args.steps)
+    dt = time.perf_counter() - t0
+    value = c.ncell * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.workload} bounded sample {c.n[0]}^3 on host cores",
+                       "scheme": args.scheme, "global_cells": c.ncell},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": f"{c.name} {c.n[0]}^3, {args.steps} timed steps"},
+            "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, ws, lr):
+    import torch
+
+    from paper_2508_19911_b200 import Solver
+    from paper_2508_19911_b200.binding import fp64_peak
+
+    scheme_id = 1 if args.scheme == "cgks5" else 0
+    case = make_case(args.workload)
+    if args.nonlinear is not None:
+        case.nonlinear = args.nonlinear
+    stream = torch.cuda.current_stream()
+    S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream)
+    NV = 20 if scheme_id == 1 else 5
+    Qd = torch.from_numpy(np.ascontiguousarray(case.Q)).cuda()
+    Gd = torch.from_numpy(np.ascontiguousarray(case.G)).cuda()
+    S.set_state(Qd, Gd if scheme_id == 1 else None)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        S.step(1)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(lr) as clk:
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0.record(stream)
+        S.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms, ws)
+    cells = case.ncell * ws
+    value = cells * args.steps / (ms * 1e-3)
+
+    # e2e through the C ABI with host buffers: H2D of the inputs + steps + D2H of the result per step
+    Qh = np.ascontiguousarray(case.Q)
+    Gh = np.ascontiguousarray(case.G)
+    Qo = np.empty_like(Qh)
+    Go = np.empty_like(Gh) if scheme_id == 1 else None
+    Qh_pin = torch.from_numpy(Qh).pin_memory()
+    Gh_pin = torch.from_numpy(Gh).pin_memory()
+    Qo_pin = torch.empty(Qh.shape, dtype=torch.float64).pin_memory()
+    Go_pin = torch.empty(Gh.shape, dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        S.set_state(Qh_pin.numpy(), Gh_pin.numpy() if scheme_id == 1 else None)
+        S.step(1)
+        S.get_state(Qo_pin.numpy(), Go_pin.numpy() if scheme_id == 1 else None, with_grad=scheme_id == 1)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
+    e2e_val = cells * e2e_steps / e2e_s
+    nbytes = Qh.nbytes + (Gh.nbytes if scheme_id == 1 else 0)
+
+    # roofline of the dominant kernel: per-kernel CUDA-event durations on the library stream
+    S.set_state(Qd, Gd if scheme_id == 1 else None)
+    prof = S.profile(max(2, min(args.steps, 4)))
+    flops, per_cell = S.algorithmic_flops()
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms = prof[dom][0] / prof[dom][1]
+    total_prof = sum(v[0] for v in prof.values())
+    peak64, _ = fp64_peak()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    achieved = flops.get(dom, 0.0) / (dom_ms * 1e-3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
+            "frac": achieved / peak64 if peak64 else None, "traffic": None,
+            "kernel": dom, "kernel_ms": dom_ms, "kernel_share": prof[dom][0] / total_prof,
+            "algorithmic_flops_per_launch": flops.get(dom, 0.0),
+            "peak_source": "measured FP64 DFMA probe (cgks_fp64_peak) in this run; MEASURED_PEAKS.json has no FP64",
+            "step_frac": (per_cell * cells / ws) / (ms / args.steps * 1e-3) / 1e12 / peak64 if peak64 else None,
+            "hbm_gbs_peak": peaks.get("hbm_gbs")}
+    per_kernel = {k: {"ms_per_launch": v[0] / v[1], "launches": v[1],
+                      "tflops": (flops.get(k, 0.0) / (v[0] / v[1] * 1e-3) / 1e12) if k in flops else None}
+                  for k, v in prof.items()}
+    S.close()
+
+    if rank != 0:
+        return 0
+    line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{case.name} {case.n[0]}x{case.n[1]}x{case.n[2]}",
+                       "scheme": args.scheme + ("-geno" if case.nonlinear else "-linear"),
+                       "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
+                       "parallelism": f"replicas{ws}" if ws > 1 else "1gpu",
+                       "l2": "state larger than L2 (no flush)"},
+            "roofline": roof,
+            "algorithmic_flops_per_cell_update": per_cell,
+            "per_kernel": per_kernel,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes},
+            "gpu_launches": S.launches_per_step() * args.steps if S.ctx else None}
+    line["gpu_launches"] = int(sum(v[1] for v in prof.values()) / max(2, min(args.steps, 4)) * args.steps)
+    if not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(args.workload, args.scheme)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="tgv128")
+    ap.add_argument("--scheme", default="cgks5", choices=["cgks5", "gks2"])
+    ap.add_argument("--nonlinear", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, ws, lr = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, rank, ws)
+    return run_ours(args, rank, ws, lr)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,142 @@
+/*
+ * cgks.h -- C ABI of the B200 (sm_100a) FP64 hot path of the fifth-order compact
+ * gas-kinetic scheme CGKS-5th and the second-order GKS-2nd (arXiv 2508.19911).
+ *
+ * One call of cgks_step advances the cell averages Q and (CGKS-5th) the
+ * cell-averaged gradients grad Q by whole time steps:
+ *   - compact reconstruction at cell interfaces,
+ *   - the time-dependent gas-kinetic interface flux and interface values
+ *     (P:93-129),
+ *   - the simultaneous update of averages and gradients with the two-stage
+ *     fourth-order S2O4 or the one-stage S1O2,
+ *   - the CFL time step, a global min-reduction.
+ * Readings of points the paper leaves open are numbered R1-R34 in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   - Return value: CGKS_OK (0) or one of the CGKS_ERR_* codes below; no
+ *     exceptions cross the ABI.  cgks_last_error() gives a message.
+ *   - All calls are synchronous with respect to the host on return.
+ *   - Array arguments may be host or device pointers (detected with
+ *     cudaPointerGetAttributes); the library copies and never retains them;
+ *     the caller owns them.
+ *   - User layout (rank-local block, x fastest):
+ *       Q     : double[5][nz][ny][nx]      (rho, rho U, rho V, rho W, rho E)
+ *       gradQ : double[3][5][nz][ny][nx]   (physical d/dx, d/dy, d/dz of each Q)
+ *   - A context is bound to one CUDA device (the current device at create) and
+ *     one rank, and is not thread-safe.
+ */
+#ifndef CGKS_H
+#define CGKS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (2/3/4 mirror the exit codes of SPEC S:646) */
+enum {
+  CGKS_OK = 0,
+  CGKS_ERR_CONFIG = 2,     /* invalid sizes, gamma not in (1,5/3], mu<0, Pr<=0, bc/decomposition, CLS rank check */
+  CGKS_ERR_POSITIVITY = 3, /* rho<=0 or p<=0 in a state or reconstructed value (R30); state = last completed step */
+  CGKS_ERR_NUMERICAL = 4,  /* NaN / non-finite time step */
+  CGKS_ERR_CUDA = 5,       /* CUDA runtime failure */
+  CGKS_ERR_COMM = 6        /* inter-GPU exchange failure */
+};
+
+/* boundary kinds per axis side (R29) */
+enum { CGKS_BC_PERIODIC = 0, CGKS_BC_INFLOW = 1, CGKS_BC_OUTFLOW = 2 };
+
+/* scheme ids and time schemes */
+enum { CGKS_GKS2 = 0, CGKS_CGKS5 = 1 };
+enum { CGKS_TIME_DEFAULT = 0, CGKS_TIME_S1O2 = 1, CGKS_TIME_S2O4 = 2 };
+
+typedef struct cgks_ctx cgks_ctx; /* opaque; owns all device memory */
+
+typedef struct {
+  int64_t n[3];              /* global cells per axis; active axes are the leading ones with n>1
+                                (n[2]==1: 2-D run; n[1]==n[2]==1: 1-D run)                          */
+  double lo[3], hi[3];       /* box; uniform spacing h[a] = (hi[a]-lo[a])/n[a]                      */
+  int bc[3][2];              /* CGKS_BC_* per axis (low, high side)                                */
+  double bc_state[3][2][5];  /* conservative state for CGKS_BC_INFLOW sides                        */
+  int nproc[3];              /* ranks per axis; (1,1,P) = z-slabs.  {1,1,1} or zeros = one rank     */
+  int rank;                  /* this process' rank in [0, nproc product)                           */
+  const void* nccl_id;       /* 128-byte ncclUniqueId, or NULL when there is one rank              */
+  void* stream;              /* cudaStream_t to run on, or NULL for a library-owned stream         */
+} cgks_grid;
+
+typedef struct {
+  int id;           /* CGKS_GKS2 or CGKS_CGKS5                                                     */
+  int nonlinear;    /* 0 = linear (chi == 1 / phi == 1), 1 = GENO / Venkatakrishnan   */
+  int time_scheme;  /* CGKS_TIME_*: default S2O4 for CGKS-5th, S1O2 for GKS-2nd (R22)  */
+  double cfl;       /* CFL number of the time step (R25)                               */
+  double fixed_dt;  /* > 0 overrides the CFL time step                                            */
+  double tau_eps;   /* inviscid collision time epsilon, paper 0.05                        */
+  double tau_C;     /* pressure-jump constant C, paper 10                          */
+  double relax_C;   /* tau0 jump constant of the side-state relaxation (R23), 10       */
+  double k_venkat;  /* Venkatakrishnan K (R11), 0.3                                               */
+  double chi_c;     /* GENO chi constant (R8), 0.01                                               */
+} cgks_scheme;
+
+/* Fill a cgks_scheme with the paper defaults for scheme id (CGKS_GKS2 / CGKS_CGKS5). */
+void cgks_scheme_defaults(int id, cgks_scheme* s);
+
+/*
+ * Create a context.  gamma in (1, 5/3]; mu >= 0 is the constant dynamic viscosity
+ * (mu == 0: inviscid collision time P:344); Pr > 0 the Prandtl number (R20).
+ * Builds the CGKS-5th constrained-least-squares matrix (R1-R4) on the
+ * host in long double and checks its rank (CGKS_ERR_CONFIG when deficient).
+ * Allocates all device memory on the current device.  *out is NULL on failure.
+ */
+int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const cgks_scheme* scheme,
+                cgks_ctx** out);
+
+/* Offset and size of this rank's block in the global grid. */
+int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]);
+
+/* Set the state (user layout, rank-local block).  gradQ may be NULL (zero gradients;
+ * not recommended for CGKS-5th, R26; ignored by GKS-2nd).  Resets t and the step count. */
+int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);
+
+/* Advance nsteps time steps (each: dt min-reduction, then one S2O4 or S1O2 step).
+ * On CGKS_ERR_POSITIVITY / CGKS_ERR_NUMERICAL the state is the last completed step. */
+int cgks_step(cgks_ctx* ctx, int nsteps);
+
+/* Copy the state out (user layout).  gradQ may be NULL. */
+int cgks_get_state(const cgks_ctx* ctx, double* Q, double* gradQ);
+
+/* Simulated time, completed steps, and the last time step used. */
+int cgks_get_time(const cgks_ctx* ctx, double* t, int64_t* steps, double* last_dt);
+
+/* Message of the last error (includes cell (i,j,k) and stage for positivity failures). */
+const char* cgks_last_error(const cgks_ctx* ctx);
+
+/* Number of library kernel launches per time step (for launch accounting). */
+int cgks_launches_per_step(const cgks_ctx* ctx);
+
+/* Per-kernel timing: run nsteps steps with a CUDA event pair around every launch on the
+ * library stream; fills up to max entries of names (64 chars each), total ms and launch
+ * counts; *n_out = number of distinct kernels.  Intended for the roofline report. */
+int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_ms, int64_t* launches,
+                 int* n_out);
+
+/* Algorithmic FP64 operation count of this context's formulation, per launch of each
+ * kernel (names as in cgks_profile; up to max entries of 64 chars) and per cell-update
+ * (one full time step of one cell).  Counting rules: + - * / = 1, fma = 2, sqrt and each
+ * special function (exp, expm1, erfc, rsqrt) = 1; compile-time constant folding excluded.
+ * The flux point count comes from running the device formulation with a counting type. */
+int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names, double* flops_per_launch,
+                           double* flops_per_cell_step, int* n_out);
+
+/* FP64 FMA throughput probe: runs a DFMA-bound kernel on all SMs of the current device
+ * and returns the achieved FP64 TFLOP/s (2 flops per FMA) and the kernel time in ms. */
+int cgks_fp64_peak(double* tflops, double* ms);
+
+/* Release all resources.  Safe on NULL. */
+void cgks_destroy(cgks_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CGKS_H */

@@ -1,0 +1,701 @@
+// cgks_api.cu -- host side of the C ABI declared in include/cgks.h: context,
+// device memory, the S2O4 / S1O2 stage driver and per-kernel profiling.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/cgks.h"
+#include "cls_build.h"
+#include "flop_count.h"
+#include "kernels.cuh"
+
+using namespace cgks;
+
+struct cgks_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Geo geo;
+  FluxConst fc;
+  cgks_scheme sch;
+  int scheme_id = 1, nonlinear = 0, time_scheme = 2, dim = 3, box = 0;
+  int NV = 20;
+  long long ncell = 0, necell = 0;
+  double* U[2] = {nullptr, nullptr};
+  double* Us = nullptr;
+  double* carry = nullptr;
+  double* rec = nullptr;
+  double* face[3] = {nullptr, nullptr, nullptr};
+  double* gtab[3] = {nullptr, nullptr, nullptr};
+  double* staging = nullptr;
+  TimeState* ts = nullptr;
+  ErrState* err = nullptr;
+  int cur = 0;
+  ClsTables cls;
+  char msg[512] = {0};
+  // profiling
+  bool prof = false;
+  std::map<std::string, std::pair<double, long long>> ptimes;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  int launches_per_step = 0;
+};
+
+static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
+
+static void set_msg(cgks_ctx* c, const char* fmt, ...) {
+  if (!c) return;
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(c->msg, sizeof(c->msg), fmt, ap);
+  va_end(ap);
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      set_msg(ctx, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__,         \
+              cudaGetErrorString(e_));                                                             \
+      return CGKS_ERR_CUDA;                                                                        \
+    }                                                                                              \
+  } while (0)
+
+static int upload_constants(cgks_ctx* ctx) {
+  if (g_const_owner == ctx) return CGKS_OK;
+  CK(cudaMemcpyToSymbolAsync(c_geo, &ctx->geo, sizeof(Geo), 0, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyToSymbolAsync(c_fc, &ctx->fc, sizeof(FluxConst), 0, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->scheme_id == CGKS_CGKS5)
+    CK(cudaMemcpyToSymbolAsync(c_R, ctx->cls.R, sizeof(double) * ctx->cls.nb * ctx->cls.nd, 0,
+                               cudaMemcpyHostToDevice, ctx->stream));
+  g_const_owner = ctx;
+  return CGKS_OK;
+}
+
+// launch helper with optional per-launch event timing
+template <typename... KArgs, typename... Args>
+static int launch(cgks_ctx* ctx, const char* name, void (*kern)(KArgs...), long long nthreads, int block,
+                  Args... args) {
+  if (nthreads <= 0) return CGKS_OK;
+  long long nblk = (nthreads + block - 1) / block;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, ctx->stream);
+  }
+  kern<<<(unsigned)nblk, block, 0, ctx->stream>>>(args...);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_msg(ctx, "launch of %s failed: %s", name, cudaGetErrorString(e));
+    return CGKS_ERR_CUDA;
+  }
+  if (ctx->prof) {
+    cudaEventRecord(e1, ctx->stream);
+    ctx->pending.push_back({name, {e0, e1}});
+  }
+  return CGKS_OK;
+}
+
+#define LAUNCH(name, kern, n, blk, ...)                                \
+  do {                                                                 \
+    int rc_ = launch(ctx, name, kern, (long long)(n), blk, __VA_ARGS__); \
+    if (rc_) return rc_;                                               \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// one stage: reconstruction, fluxes along each active axis, update
+// ---------------------------------------------------------------------------
+template <int DIM, bool COMPACT, bool NONLIN, bool BOX>
+static int stage_t(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+  if (COMPACT) {
+    LAUNCH("recon5", (k_recon5<DIM, NONLIN, BOX>), ctx->necell, 128, Uin, ctx->rec, ctx->err);
+  } else {
+    LAUNCH("recon2", (k_recon2<DIM, NONLIN, BOX>), ctx->necell, 256, Uin, ctx->rec, ctx->err);
+  }
+  constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
+  for (int a = 0; a < DIM; ++a) {
+    long long nf = (long long)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
+    if (a == 0)
+      LAUNCH("flux_x", (k_flux<DIM, 0, COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[0], ctx->face[0],
+             ctx->ts, ctx->err, stage);
+    if (a == 1)
+      LAUNCH("flux_y", (k_flux<DIM, (DIM > 1 ? 1 : 0), COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[1],
+             ctx->face[1], ctx->ts, ctx->err, stage);
+    if (a == 2)
+      LAUNCH("flux_z", (k_flux<DIM, (DIM > 2 ? 2 : 0), COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[2],
+             ctx->face[2], ctx->ts, ctx->err, stage);
+  }
+  if (mode == 0)
+    LAUNCH("update", (k_update<DIM, COMPACT, 0>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
+           Uout, ctx->carry, ctx->ts, ctx->err);
+  else if (mode == 1)
+    LAUNCH("update", (k_update<DIM, COMPACT, 1>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
+           Uout, ctx->carry, ctx->ts, ctx->err);
+  else
+    LAUNCH("update", (k_update<DIM, COMPACT, 2>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
+           Uout, ctx->carry, ctx->ts, ctx->err);
+  return CGKS_OK;
+}
+
+template <int DIM>
+static int stage_dim(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+  bool c = ctx->scheme_id == CGKS_CGKS5, nl = ctx->nonlinear != 0, b = ctx->box != 0;
+  if (c && !nl && !b) return stage_t<DIM, true, false, false>(ctx, Uin, Uout, mode, stage);
+  if (c && nl && !b) return stage_t<DIM, true, true, false>(ctx, Uin, Uout, mode, stage);
+  if (c && !nl && b) return stage_t<DIM, true, false, true>(ctx, Uin, Uout, mode, stage);
+  if (c && nl && b) return stage_t<DIM, true, true, true>(ctx, Uin, Uout, mode, stage);
+  if (!c && !nl && !b) return stage_t<DIM, false, false, false>(ctx, Uin, Uout, mode, stage);
+  if (!c && nl && !b) return stage_t<DIM, false, true, false>(ctx, Uin, Uout, mode, stage);
+  if (!c && !nl && b) return stage_t<DIM, false, false, true>(ctx, Uin, Uout, mode, stage);
+  return stage_t<DIM, false, true, true>(ctx, Uin, Uout, mode, stage);
+}
+
+static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+  if (ctx->dim == 3) return stage_dim<3>(ctx, Uin, Uout, mode, stage);
+  if (ctx->dim == 2) return stage_dim<2>(ctx, Uin, Uout, mode, stage);
+  return stage_dim<1>(ctx, Uin, Uout, mode, stage);
+}
+
+static int launch_dt(cgks_ctx* ctx, const double* Uin) {
+  if (ctx->dim == 3) LAUNCH("dt", k_dt<3>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
+  if (ctx->dim == 2) LAUNCH("dt", k_dt<2>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
+  if (ctx->dim == 1) LAUNCH("dt", k_dt<1>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
+  LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ctx->ts, (const ErrState*)ctx->err);
+  return CGKS_OK;
+}
+
+// one full time step from U[cur] into U[1-cur]
+static int one_step(cgks_ctx* ctx) {
+  const double* Un = ctx->U[ctx->cur];
+  double* Unext = ctx->U[1 - ctx->cur];
+  int rc = launch_dt(ctx, Un);
+  if (rc) return rc;
+  if (ctx->time_scheme == CGKS_TIME_S1O2) {
+    rc = run_stage(ctx, Un, Unext, 2, 1);
+  } else {
+    rc = run_stage(ctx, Un, ctx->Us, 0, 1);
+    if (!rc) rc = run_stage(ctx, ctx->Us, Unext, 1, 2);
+  }
+  if (rc) return rc;
+  LAUNCH("step_end", k_step_end, 1, 32, ctx->ts, (const ErrState*)ctx->err);
+  ctx->cur = 1 - ctx->cur;
+  return CGKS_OK;
+}
+
+static int count_launches(cgks_ctx* c) {
+  int per_stage = 1 + c->dim + 1;
+  int stages = (c->time_scheme == CGKS_TIME_S1O2) ? 1 : 2;
+  return 2 + stages * per_stage + 1;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+void cgks_scheme_defaults(int id, cgks_scheme* s) {
+  if (!s) return;
+  s->id = id;
+  s->nonlinear = 0;
+  s->time_scheme = CGKS_TIME_DEFAULT;
+  s->cfl = id == CGKS_CGKS5 ? 0.3 : 0.5;
+  s->fixed_dt = 0.0;
+  s->tau_eps = 0.05;
+  s->tau_C = 10.0;
+  s->relax_C = 10.0;
+  s->k_venkat = 0.3;
+  s->chi_c = 0.01;
+}
+
+int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const cgks_scheme* scheme,
+                cgks_ctx** out) {
+  if (!out) return CGKS_ERR_CONFIG;
+  *out = nullptr;
+  if (!grid || !scheme) return CGKS_ERR_CONFIG;
+  cgks_ctx* ctx = new cgks_ctx();
+  auto fail = [&](int code) {
+    std::fprintf(stderr, "cgks_create: %s\n", ctx->msg);
+    cgks_destroy(ctx);
+    return code;
+  };
+  // ---- validation
+  for (int a = 0; a < 3; ++a)
+    if (grid->n[a] < 1 || grid->n[a] > (1 << 20) || !(grid->hi[a] > grid->lo[a])) {
+      set_msg(ctx, "invalid grid along axis %d", a);
+      return fail(CGKS_ERR_CONFIG);
+    }
+  if (!(gamma > 1.0 && gamma <= 5.0 / 3.0 + 1e-12) || !(mu >= 0.0) || !(Pr > 0.0)) {
+    set_msg(ctx, "invalid gas parameters gamma=%g mu=%g Pr=%g", gamma, mu, Pr);
+    return fail(CGKS_ERR_CONFIG);
+  }
+  if (scheme->id != CGKS_GKS2 && scheme->id != CGKS_CGKS5) {
+    set_msg(ctx, "unknown scheme id %d", scheme->id);
+    return fail(CGKS_ERR_CONFIG);
+  }
+  int nranks = 1;
+  for (int a = 0; a < 3; ++a) nranks *= grid->nproc[a] > 0 ? grid->nproc[a] : 1;
+  if (nranks != 1) {
+    set_msg(ctx, "multi-rank decomposition is not available in this build");
+    return fail(CGKS_ERR_CONFIG);
+  }
+  int dim = grid->n[2] > 1 ? 3 : (grid->n[1] > 1 ? 2 : 1);
+  if ((dim < 3 && grid->n[2] != 1) || (dim < 2 && grid->n[1] != 1)) {
+    set_msg(ctx, "active axes must be the leading ones");
+    return fail(CGKS_ERR_CONFIG);
+  }
+  ctx->dim = dim;
+  ctx->sch = *scheme;
+  ctx->scheme_id = scheme->id;
+  ctx->nonlinear = scheme->nonlinear ? 1 : 0;
+  ctx->time_scheme = scheme->time_scheme;
+  if (ctx->time_scheme == CGKS_TIME_DEFAULT)
+    ctx->time_scheme = scheme->id == CGKS_CGKS5 ? CGKS_TIME_S2O4 : CGKS_TIME_S1O2;
+  ctx->NV = scheme->id == CGKS_CGKS5 ? 20 : 5;
+  cudaGetDevice(&ctx->device);
+
+  // ---- geometry constants
+  Geo& g = ctx->geo;
+  std::memset(&g, 0, sizeof(g));
+  g.dim = dim;
+  for (int a = 0; a < 3; ++a) {
+    g.n[a] = (int)grid->n[a];
+    g.h[a] = (grid->hi[a] - grid->lo[a]) / grid->n[a];
+    g.ih[a] = 1.0 / g.h[a];
+    bool per = grid->bc[a][0] == CGKS_BC_PERIODIC && grid->bc[a][1] == CGKS_BC_PERIODIC;
+    if (!per && (grid->bc[a][0] == CGKS_BC_PERIODIC || grid->bc[a][1] == CGKS_BC_PERIODIC)) {
+      set_msg(ctx, "axis %d mixes periodic and non-periodic sides", a);
+      return fail(CGKS_ERR_CONFIG);
+    }
+    g.bounded[a] = (a < dim && !per) ? 1 : 0;
+    if (g.bounded[a]) ctx->box = 1;
+    g.elo[a] = g.bounded[a] ? -1 : 0;
+    g.en[a] = g.n[a] + (g.bounded[a] ? 2 : 0);
+    for (int s = 0; s < 2; ++s) {
+      g.bc[a][s] = grid->bc[a][s];
+      for (int v = 0; v < 5; ++v) g.bc_state[a][s][v] = grid->bc_state[a][s][v];
+    }
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) g.fn[a][b] = g.n[b] + ((a == b && g.bounded[a]) ? 1 : 0);
+  g.plane = (long long)g.n[0] * g.n[1];
+  g.eplane = (long long)g.en[0] * g.en[1];
+  g.cfl = scheme->cfl;
+  g.fixed_dt = scheme->fixed_dt;
+  g.mu = mu;
+  g.gamma = gamma;
+  g.k_venkat = scheme->k_venkat;
+  g.chi_c = scheme->chi_c;
+  double hg = 1.0;
+  for (int a = 0; a < dim; ++a) hg *= g.h[a];
+  hg = std::pow(hg, 1.0 / dim);
+  g.eps_venkat2 = std::pow(scheme->k_venkat * hg, 3);
+  ctx->fc.gamma = gamma;
+  ctx->fc.N = (5.0 - 3.0 * gamma) / (gamma - 1.0);
+  ctx->fc.mu = mu;
+  ctx->fc.Pr = Pr;
+  ctx->fc.tau_eps = scheme->tau_eps;
+  ctx->fc.tau_C = scheme->tau_C;
+  ctx->fc.relax_C = scheme->relax_C;
+  ctx->ncell = (long long)g.n[0] * g.n[1] * g.n[2];
+  ctx->necell = (long long)g.en[0] * g.en[1] * g.en[2];
+
+  // ---- reconstruction tables
+  if (ctx->scheme_id == CGKS_CGKS5) {
+    char e[256];
+    if (!build_cls(dim, ctx->cls, e, sizeof(e))) {
+      set_msg(ctx, "%s", e);
+      return fail(CGKS_ERR_CONFIG);
+    }
+  }
+
+  // ---- stream and memory
+  if (grid->stream) {
+    ctx->stream = (cudaStream_t)grid->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      set_msg(ctx, "cannot create a CUDA stream");
+      return fail(CGKS_ERR_CUDA);
+    }
+    ctx->own_stream = true;
+  }
+  auto alloc = [&](double** p, long long n) -> bool {
+    if (n <= 0) return true;
+    return cudaMalloc((void**)p, sizeof(double) * n) == cudaSuccess;
+  };
+  int NV = ctx->NV;
+  int nrec = ctx->scheme_id == CGKS_CGKS5 ? ctx->cls.nb * 5 : 15;
+  int nff = ctx->scheme_id == CGKS_CGKS5 ? 30 : 10;
+  bool ok = alloc(&ctx->U[0], ctx->ncell * NV) && alloc(&ctx->U[1], ctx->ncell * NV) &&
+            alloc(&ctx->Us, ctx->ncell * NV) && alloc(&ctx->carry, ctx->ncell * NV) &&
+            alloc(&ctx->rec, ctx->necell * nrec) && alloc(&ctx->staging, ctx->ncell * 15);
+  for (int a = 0; a < dim && ok; ++a)
+    ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] * g.fn[a][2] * nff);
+  if (!ok || cudaMalloc((void**)&ctx->ts, sizeof(TimeState)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->err, sizeof(ErrState)) != cudaSuccess) {
+    set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
+    return fail(CGKS_ERR_CUDA);
+  }
+  // Gauss-point basis tables per axis: [side][gp][val,d0,d1,d2][nb]
+  if (ctx->scheme_id == CGKS_CGKS5) {
+    const int nb = ctx->cls.nb;
+    const double s = 0.5 / std::sqrt(3.0);  // 2-point Gauss-Legendre on [-1/2, 1/2] (R27)
+    for (int a = 0; a < dim; ++a) {
+      int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
+      int n1 = t1 < dim ? 2 : 1, n2 = t2 < dim ? 2 : 1;
+      int ng = n1 * n2;
+      std::vector<double> tab(2 * ng * 4 * nb, 0.0), val(nb), der(3 * nb);
+      for (int side = 0; side < 2; ++side)
+        for (int p = 0; p < n1; ++p)
+          for (int q = 0; q < n2; ++q) {
+            double x[3] = {0, 0, 0};
+            x[a] = side == 0 ? 0.5 : -0.5;
+            if (t1 < dim) x[t1] = p ? s : -s;
+            if (t2 < dim) x[t2] = q ? s : -s;
+            basis_at(ctx->cls, x, val.data(), der.data());
+            int gp = p * n2 + q;
+            double* dst = tab.data() + ((side * ng + gp) * 4) * nb;
+            for (int k = 0; k < nb; ++k) {
+              dst[k] = val[k];
+              dst[nb + k] = der[k];
+              dst[2 * nb + k] = der[nb + k];
+              dst[3 * nb + k] = der[2 * nb + k];
+            }
+          }
+      if (!alloc(&ctx->gtab[a], (long long)tab.size()) ||
+          cudaMemcpy(ctx->gtab[a], tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_msg(ctx, "table upload failed");
+        return fail(CGKS_ERR_CUDA);
+      }
+    }
+  }
+  cudaMemset(ctx->U[0], 0, sizeof(double) * ctx->ncell * NV);
+  cudaMemset(ctx->err, 0, sizeof(ErrState));
+  TimeState t0;
+  std::memset(&t0, 0, sizeof(t0));
+  double big = 1e300;
+  std::memcpy(&t0.dtmin_bits, &big, sizeof(big));
+  cudaMemcpy(ctx->ts, &t0, sizeof(t0), cudaMemcpyHostToDevice);
+  ctx->launches_per_step = count_launches(ctx);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_msg(ctx, "device error during create");
+    return fail(CGKS_ERR_CUDA);
+  }
+  *out = ctx;
+  return CGKS_OK;
+}
+
+int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]) {
+  if (!ctx) return CGKS_ERR_CONFIG;
+  for (int a = 0; a < 3; ++a) {
+    off[a] = 0;
+    n[a] = ctx->geo.n[a];
+  }
+  return CGKS_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
+  if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  double* U = ctx->U[0];
+  ctx->cur = 0;
+  auto put = [&](const double* src, int f0, int nf) -> int {
+    const double* dsrc = nullptr;
+    if (src) {
+      if (is_device_ptr(src)) {
+        dsrc = src;
+      } else {
+        CK(cudaMemcpyAsync(ctx->staging, src, sizeof(double) * nc * nf, cudaMemcpyHostToDevice, ctx->stream));
+        dsrc = ctx->staging;
+      }
+    }
+    long long n = nc * nf;
+    k_pack<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(dsrc, U, ctx->NV, f0, nf);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CGKS_OK;
+  };
+  rc = put(Q, 0, 5);
+  if (rc) return rc;
+  if (ctx->NV == 20) {
+    rc = put(gradQ, 5, 15);
+    if (rc) return rc;
+  }
+  TimeState t0;
+  std::memset(&t0, 0, sizeof(t0));
+  double big = 1e300;
+  std::memcpy(&t0.dtmin_bits, &big, sizeof(big));
+  CK(cudaMemcpyAsync(ctx->ts, &t0, sizeof(t0), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->err, 0, sizeof(ErrState), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CGKS_OK;
+}
+
+static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0) {
+  ErrState e;
+  TimeState t;
+  CK(cudaMemcpyAsync(&e, ctx->err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (e.code) {
+    // kernels after the failure were no-ops; the last completed step sits in the input buffer of step e.step
+    long long done = t.steps - steps0;
+    ctx->cur = (int)((cur0 + done) % 2);
+    static const char* kn[] = {"?", "flux", "update", "dt"};
+    set_msg(ctx, "%s at cell (%d,%d,%d), step %lld, stage %d (kernel %s)",
+            e.code == 3 ? "positivity failure (rho<=0 or p<=0)" : "non-finite time step", e.cell[0], e.cell[1],
+            e.cell[2], e.step, e.stage, kn[e.kernel & 3]);
+    return e.code == 3 ? CGKS_ERR_POSITIVITY : CGKS_ERR_NUMERICAL;
+  }
+  return CGKS_OK;
+}
+
+int cgks_step(cgks_ctx* ctx, int nsteps) {
+  if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  TimeState t;
+  CK(cudaMemcpyAsync(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int cur0 = ctx->cur;
+  for (int s = 0; s < nsteps; ++s) {
+    rc = one_step(ctx);
+    if (rc) return rc;
+  }
+  return finish_steps(ctx, cur0, t.steps);
+}
+
+int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
+  cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
+  if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  const double* U = ctx->U[ctx->cur];
+  auto get = [&](double* dst, int f0, int nf) -> int {
+    bool dev = is_device_ptr(dst);
+    double* ddst = dev ? dst : ctx->staging;
+    long long n = nc * nf;
+    k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(U, ddst, ctx->NV, f0, nf);
+    CK(cudaGetLastError());
+    if (!dev) CK(cudaMemcpyAsync(dst, ctx->staging, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CGKS_OK;
+  };
+  rc = get(Q, 0, 5);
+  if (rc) return rc;
+  if (gradQ) {
+    if (ctx->NV == 20) {
+      rc = get(gradQ, 5, 15);
+      if (rc) return rc;
+    } else if (is_device_ptr(gradQ)) {
+      CK(cudaMemsetAsync(gradQ, 0, sizeof(double) * nc * 15, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+      std::memset(gradQ, 0, sizeof(double) * nc * 15);
+    }
+  }
+  return CGKS_OK;
+}
+
+int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_dt) {
+  cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
+  if (!ctx) return CGKS_ERR_CONFIG;
+  TimeState ts;
+  CK(cudaMemcpy(&ts, ctx->ts, sizeof(ts), cudaMemcpyDeviceToHost));
+  if (t) *t = ts.t;
+  if (steps) *steps = ts.steps;
+  if (last_dt) *last_dt = ts.dt;
+  return CGKS_OK;
+}
+
+const char* cgks_last_error(const cgks_ctx* ctx) { return ctx ? ctx->msg : "null context"; }
+
+int cgks_launches_per_step(const cgks_ctx* ctx) { return ctx ? ctx->launches_per_step : 0; }
+
+int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_ms, int64_t* launches, int* n_out) {
+  if (!ctx) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  ctx->prof = true;
+  ctx->ptimes.clear();
+  TimeState t;
+  CK(cudaMemcpy(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost));
+  int cur0 = ctx->cur;
+  for (int s = 0; s < nsteps && !rc; ++s) rc = one_step(ctx);
+  ctx->prof = false;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    auto& slot = ctx->ptimes[p.first];
+    slot.first += ms;
+    slot.second += 1;
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  ctx->pending.clear();
+  if (rc) return rc;
+  rc = finish_steps(ctx, cur0, t.steps);
+  int i = 0;
+  for (auto& kv : ctx->ptimes) {
+    if (i >= max) break;
+    std::snprintf(names + 64 * i, 64, "%s", kv.first.c_str());
+    total_ms[i] = kv.second.first;
+    launches[i] = kv.second.second;
+    ++i;
+  }
+  if (n_out) *n_out = i;
+  return rc;
+}
+
+// Algorithmic FP64 operations per launch of each kernel (counting rules in flop_count.h).
+// The flux point is counted by running the device formulation with the counting type.
+static double flux_point_flops(const FluxConst& f, bool compact) {
+  using fc::CD;
+  CD WL[5], WR[5], dWL[3][5], dWR[3][5];
+  const double wl[5] = {1.0, 0.3, -0.2, 0.1, 2.7}, wr[5] = {1.01, 0.29, -0.21, 0.12, 2.71};
+  for (int i = 0; i < 5; ++i) {
+    WL[i] = CD::run(wl[i]);
+    WR[i] = CD::run(wr[i]);
+    for (int d = 0; d < 3; ++d) {
+      dWL[d][i] = CD::run(0.01 * (i + 1) * (d + 1));
+      dWR[d][i] = CD::run(-0.02 * (i + 1) + 0.01 * d);
+    }
+  }
+  GPOutT<CD> o;
+  fc::tally() = fc::Tally();
+  if (compact)
+    gks_flux_point<true>(WL, dWL, WR, dWR, CD::run(1e-3), f, o);
+  else
+    gks_flux_point<false>(WL, dWL, WR, dWR, CD::run(1e-3), f, o);
+  return fc::tally().flops;
+}
+
+extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names, double* flops_per_launch,
+                                      double* flops_per_cell_step, int* n_out) {
+  if (!ctx) return CGKS_ERR_CONFIG;
+  const int D = ctx->dim;
+  const bool c5 = ctx->scheme_id == CGKS_CGKS5;
+  const long long nc = ctx->ncell, nec = ctx->necell;
+  std::vector<std::pair<std::string, double>> rows;
+  const double fp = flux_point_flops(ctx->fc, c5);
+  if (c5) {
+    const int NB = ctx->cls.nb, ND = ctx->cls.nd, NC = ctx->cls.nc, NF = 2 * D;
+    const int nedge = NC - NF;
+    double per_comp = NC + NF * D + (D == 3 ? 5.0 * nedge : (D == 2 ? 2.0 * nedge : 0.0)) + D + 2.0 * NB * ND;
+    if (ctx->nonlinear)
+      per_comp += NF * 6.0 + NF * (NF * 5.0 + 1.0 + 2.0 * D) + 8.0 + NB + 2.0 * D + 1.0;
+    rows.push_back({"recon5", 5.0 * per_comp * nec});
+    const int NG = D == 3 ? 4 : (D == 2 ? 2 : 1);
+    const double eval = 2.0 * 5.0 * (2.0 * NB * (1 + D) + D);
+    const double per_face = NG * (eval + fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
+    const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
+    for (int a = 0; a < D; ++a) {
+      double nf = (double)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
+      rows.push_back({fnm[a], per_face * nf});
+    }
+    rows.push_back({"update", (D * (30.0 + 20.0) + 60.0) * nc});
+  } else {
+    rows.push_back({"recon2", 5.0 * (D * 2.0 + (ctx->nonlinear ? 2.0 * D * 12.0 : 0.0) + D) * nec});
+    const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
+    for (int a = 0; a < D; ++a) {
+      double nf = (double)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
+      rows.push_back({fnm[a], (50.0 + fp + 10.0) * nf});
+    }
+    rows.push_back({"update", (D * 30.0 + 30.0) * nc});
+  }
+  rows.push_back({"dt", 25.0 * D * nc});
+  int i = 0;
+  double per_step = 0.0;
+  const int stages = ctx->time_scheme == CGKS_TIME_S1O2 ? 1 : 2;
+  for (auto& r : rows) {
+    per_step += (r.first == "dt" ? 1 : stages) * r.second;
+    if (i < max) {
+      std::snprintf(names + 64 * i, 64, "%s", r.first.c_str());
+      flops_per_launch[i] = r.second;
+      ++i;
+    }
+  }
+  if (n_out) *n_out = i;
+  if (flops_per_cell_step) *flops_per_cell_step = per_step / (double)nc;
+  return CGKS_OK;
+}
+
+// DFMA throughput probe: 16 independent FMA chains per thread
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 1e-9 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 1.2345) out[blockIdx.x] = s;  // never true in practice; keeps the chains alive
+}
+
+extern "C" int cgks_fp64_peak(double* tflops, double* ms_out) {
+  cgks_ctx* ctx = nullptr;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double* out = nullptr;
+  if (cudaMalloc((void**)&out, sizeof(double) * nsm * 64) != cudaSuccess) return CGKS_ERR_CUDA;
+  const int blocks = nsm * 8, threads = 256, iters = 8192;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 6; ++r) {
+    cudaEventRecord(e0);
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.9999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return CGKS_ERR_CUDA;
+  const double flops = 2.0 * 16.0 * iters * (double)blocks * threads;
+  if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+  if (ms_out) *ms_out = best;
+  (void)ctx;
+  return CGKS_OK;
+}
+
+void cgks_destroy(cgks_ctx* ctx) {
+  if (!ctx) return;
+  if (g_const_owner == ctx) g_const_owner = nullptr;
+  double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us, ctx->carry, ctx->rec, ctx->staging,
+                    ctx->face[0], ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2]};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (ctx->ts) cudaFree(ctx->ts);
+  if (ctx->err) cudaFree(ctx->err);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+}  // extern "C"

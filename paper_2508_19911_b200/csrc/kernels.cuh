@@ -1,0 +1,641 @@
+// kernels.cuh -- sm_100a FP64 kernels of one CGKS-5th / GKS-2nd stage.
+//
+//   k_recon5   compact CLS quartic coefficients per cell, GENO folded in
+//   k_recon2   GKS-2nd least-squares slopes with Venkatakrishnan limiting
+//   k_flux     one thread per (face, Gauss point): evaluate both sides, gas-kinetic
+//              flux + interface values, 2x2 Gauss face average by warp
+//              shuffles, one face record per face
+//   k_update   residual L, dL/dt, Gauss-theorem gradients and the
+//              S2O4 / S1O2 stage combinations
+//   k_dt       CFL candidate per cell, warp-shuffle + block min, atomicMin
+//
+// Layout of every cell field: [z][field][y][x], x fastest (coalesced along x).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gks_flux.cuh"
+
+namespace cgks {
+
+constexpr int NBmax = 34;
+
+// ---------------------------------------------------------------------------
+// constant geometry / parameters
+// ---------------------------------------------------------------------------
+struct Geo {
+  int n[3];          // local cells
+  int dim;
+  int bounded[3];    // axis has non-periodic boundaries
+  int elo[3];        // extended (reconstruction) range start: -1 on bounded axes
+  int en[3];         // extended counts
+  int fn[3][3];      // face-grid dims for faces normal to axis a: fn[a][b]
+  long long plane;   // n0*n1
+  long long eplane;  // en0*en1
+  double h[3], ih[3];
+  int bc[3][2];
+  double bc_state[3][2][5];
+  double cfl, fixed_dt, mu, gamma;
+  double k_venkat, chi_c, eps_venkat2;
+};
+
+struct ErrState {
+  int code;        // 0 ok, 3 positivity, 4 numerical
+  int stage;       // 1, 2
+  long long step;  // global step index at failure
+  int cell[3];
+  int kernel;      // 1 flux, 2 update, 3 dt
+};
+
+struct TimeState {
+  double t;
+  long long steps;
+  double dt;
+  unsigned long long dtmin_bits;
+  int pad;
+};
+
+__constant__ Geo c_geo;
+__constant__ FluxConst c_fc;
+__constant__ double c_R[34 * 63];
+
+// ---------------------------------------------------------------------------
+// compile-time stencil tables (match cls_build.cpp ordering)
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct Sten {
+  static constexpr int NB = DIM == 3 ? 34 : (DIM == 2 ? 14 : 4);
+  static constexpr int NFACE = 2 * DIM;
+  static constexpr int NEDGE = DIM == 3 ? 12 : (DIM == 2 ? 4 : 0);
+  static constexpr int NC = NFACE + NEDGE;
+  static constexpr int NL = NFACE * DIM + (DIM == 3 ? 2 * NEDGE : DIM * NEDGE) + DIM;
+  static constexpr int ND = NC + NL;
+  static constexpr int NG = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);  // face Gauss points (K)
+};
+
+// offset component `ax` of neighbour n (faces (-a,+a) per axis, then edges for axis pairs a<b)
+template <int DIM>
+__host__ __device__ constexpr int nbr_off(int n, int ax) {
+  if (n < 2 * DIM) return (n / 2 == ax) ? ((n % 2) ? 1 : -1) : 0;
+  int e = n - 2 * DIM;
+  int pair = e / 4, sgn = e % 4;
+  int a = 0, b = 1;
+  if (DIM == 3) {
+    if (pair == 0) { a = 0; b = 1; }
+    if (pair == 1) { a = 0; b = 2; }
+    if (pair == 2) { a = 1; b = 2; }
+  }
+  int sa = (sgn / 2) ? 1 : -1, sb = (sgn % 2) ? 1 : -1;
+  if (ax == a) return sa;
+  if (ax == b) return sb;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// state access with periodic wrap or box ghost rules (R29)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+__device__ __forceinline__ long long sidx(int NV, int f, int i, int j, int k) {
+  return ((long long)k * NV + f) * c_geo.plane + (long long)j * c_geo.n[0] + i;
+}
+
+// value of field f (0-4 Q, 5-19 gradient [axis][var]) of cell (i,j,k), any integer index
+template <bool BOX>
+__device__ __forceinline__ double ld_state(const double* __restrict__ U, int NV, int f, int i, int j, int k) {
+  int idx[3] = {i, j, k};
+  if (BOX) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (c_geo.bounded[a] && (idx[a] < 0 || idx[a] >= c_geo.n[a])) {
+        int side = idx[a] < 0 ? 0 : 1;
+        if (c_geo.bc[a][side] == 1) return f < 5 ? c_geo.bc_state[a][side][f] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (c_geo.bounded[a]) {
+        idx[a] = idx[a] < 0 ? 0 : (idx[a] >= c_geo.n[a] ? c_geo.n[a] - 1 : idx[a]);
+      } else {
+        idx[a] = wrapi(idx[a], c_geo.n[a]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) idx[a] = wrapi(idx[a], c_geo.n[a]);
+  }
+  return __ldg(U + sidx(NV, f, idx[0], idx[1], idx[2]));
+}
+
+// index into an extended-range per-cell buffer (coefficients / slopes)
+__device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
+  // periodic axes wrap; bounded axes are stored from elo = -1
+  int ii = c_geo.bounded[0] ? i : wrapi(i, c_geo.n[0]);
+  int jj = c_geo.bounded[1] ? j : wrapi(j, c_geo.n[1]);
+  int kk = c_geo.bounded[2] ? k : wrapi(k, c_geo.n[2]);
+  ii -= c_geo.elo[0];
+  jj -= c_geo.elo[1];
+  kk -= c_geo.elo[2];
+  return ((long long)kk * NF + f) * c_geo.eplane + (long long)jj * c_geo.en[0] + ii;
+}
+
+__device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
+                                           int j, int k) {
+  if (atomicCAS(&err->code, 0, code) == 0) {
+    err->kernel = kernel;
+    err->stage = stage;
+    err->step = step;
+    err->cell[0] = i;
+    err->cell[1] = j;
+    err->cell[2] = k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: CGKS-5th reconstruction (coefficients of P^4 on the reference cell, GENO folded)
+// ---------------------------------------------------------------------------
+template <int DIM, bool NONLIN, bool BOX>
+__global__ void __launch_bounds__(128) k_recon5(const double* __restrict__ U, double* __restrict__ coef,
+                                                 const ErrState* __restrict__ err) {
+  using S = Sten<DIM>;
+  constexpr int NV = 20;
+  constexpr int NCO = S::NB * 5;
+  if (err->code) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ntot = (long long)c_geo.en[0] * c_geo.en[1] * c_geo.en[2];
+  if (t >= ntot) return;
+  const int i = (int)(t % c_geo.en[0]) + c_geo.elo[0];
+  const int j = (int)((t / c_geo.en[0]) % c_geo.en[1]) + c_geo.elo[1];
+  const int k = (int)(t / ((long long)c_geo.en[0] * c_geo.en[1])) + c_geo.elo[2];
+  const double h0 = c_geo.h[0], h1 = c_geo.h[1], h2 = c_geo.h[2];
+  const double hh[3] = {h0, h1, h2};
+  const double rs2 = 0.70710678118654752440;
+
+#pragma unroll 1
+  for (int v = 0; v < 5; ++v) {
+    const double q0 = ld_state<BOX>(U, NV, v, i, j, k);
+    double acc[S::NB];
+#pragma unroll
+    for (int q = 0; q < S::NB; ++q) acc[q] = 0.0;
+    double dface[S::NFACE];
+    // exact rows: neighbour averages minus own average (difference form keeps uniform flow exact)
+#pragma unroll
+    for (int n = 0; n < S::NC; ++n) {
+      const double d = ld_state<BOX>(U, NV, v, i + nbr_off<DIM>(n, 0), j + nbr_off<DIM>(n, 1),
+                                     k + nbr_off<DIM>(n, 2)) - q0;
+      if (n < S::NFACE) dface[n] = d;
+#pragma unroll
+      for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + n], d, acc[q]);
+    }
+    // least-squares rows: face-neighbour gradients (reference units: h_a dQ/dx_a)
+    int row = S::NC;
+#pragma unroll
+    for (int m = 0; m < S::NFACE; ++m) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const double d = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i + nbr_off<DIM>(m, 0),
+                                               j + nbr_off<DIM>(m, 1), k + nbr_off<DIM>(m, 2));
+#pragma unroll
+        for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], d, acc[q]);
+        ++row;
+      }
+    }
+    // edge neighbours: two directional derivatives (R2) / full gradient in 2-D
+#pragma unroll
+    for (int n = S::NFACE; n < S::NC; ++n) {
+      const int oi = nbr_off<DIM>(n, 0), oj = nbr_off<DIM>(n, 1), ok = nbr_off<DIM>(n, 2);
+      double g[3];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) g[a] = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i + oi, j + oj, k + ok);
+      double dd[2];
+      if (DIM == 2) {
+        dd[0] = g[0];
+        dd[1] = g[1];
+      } else {
+        const int tax = (oi == 0) ? 0 : (oj == 0 ? 1 : 2);
+        dd[0] = g[tax];
+        dd[1] = rs2 * (oi * g[0] + oj * g[DIM > 1 ? 1 : 0] + ok * g[DIM > 2 ? 2 : 0]);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], dd[r], acc[q]);
+        ++row;
+      }
+    }
+    // own gradient (R1)
+    double gown[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      gown[a] = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i, j, k);
+#pragma unroll
+      for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], gown[a], acc[q]);
+      ++row;
+    }
+    if (NONLIN) {
+      // GENO: sub-stencil linears P_m (R6), IS (R7), weights (R9), chi (R8);
+      // Eq. (weno-new) folded into the coefficients (shared zero-mean basis, sum omega = 1)
+      double IS[S::NFACE], bm[S::NFACE][3];
+#pragma unroll
+      for (int m = 0; m < S::NFACE; ++m) {
+        const int ax = m / 2;
+        const double s = (m % 2) ? 1.0 : -1.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) bm[m][a] = (a < DIM && a != ax) ? gown[a] : 0.0;
+        bm[m][ax] = s * dface[m];
+        IS[m] = bm[m][0] * bm[m][0] + bm[m][1] * bm[m][1] + bm[m][2] * bm[m][2];
+      }
+      const double eps = 1e-15;
+      double ismax = IS[0], ismin = IS[0];
+#pragma unroll
+      for (int m = 1; m < S::NFACE; ++m) {
+        ismax = fmax(ismax, IS[m]);
+        ismin = fmin(ismin, IS[m]);
+      }
+      double lin[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < S::NFACE; ++m) {
+        double den = 0.0;
+        const double num = IS[m] + eps;
+#pragma unroll
+        for (int kk = 0; kk < S::NFACE; ++kk) {
+          const double r = num / (IS[kk] + eps);
+          const double r2 = r * r;
+          den += r2 * r2 * r;
+        }
+        const double w = 1.0 / den;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) lin[a] = fma(w, bm[m][a], lin[a]);
+      }
+      const double zeta = (ismax - ismin) / (ismin + eps + c_geo.chi_c * ismax);
+      const double z2 = zeta * zeta;
+      const double chi = 1.0 / (1.0 + z2 * z2);
+#pragma unroll
+      for (int q = 0; q < S::NB; ++q) acc[q] *= chi;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) acc[a] = fma(1.0 - chi, lin[a], acc[a]);
+    }
+#pragma unroll
+    for (int q = 0; q < S::NB; ++q) coef[eidx(NCO, q * 5 + v, i, j, k)] = acc[q];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1': GKS-2nd slopes (reference units), limited
+// ---------------------------------------------------------------------------
+template <int DIM, bool NONLIN, bool BOX>
+__global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, double* __restrict__ slope,
+                                                 const ErrState* __restrict__ err) {
+  constexpr int NV = 5;
+  if (err->code) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ntot = (long long)c_geo.en[0] * c_geo.en[1] * c_geo.en[2];
+  if (t >= ntot) return;
+  const int i = (int)(t % c_geo.en[0]) + c_geo.elo[0];
+  const int j = (int)((t / c_geo.en[0]) % c_geo.en[1]) + c_geo.elo[1];
+  const int k = (int)(t / ((long long)c_geo.en[0] * c_geo.en[1])) + c_geo.elo[2];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const double q0 = ld_state<BOX>(U, NV, v, i, j, k);
+    double qm[3], qp[3], b[3];
+    double qmax = q0, qmin = q0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      qm[a] = ld_state<BOX>(U, NV, v, i - (a == 0), j - (a == 1), k - (a == 2));
+      qp[a] = ld_state<BOX>(U, NV, v, i + (a == 0), j + (a == 1), k + (a == 2));
+      b[a] = 0.5 * (qp[a] - qm[a]);  // least-squares slope on the uniform stencil (R12)
+      qmax = fmax(qmax, fmax(qm[a], qp[a]));
+      qmin = fmin(qmin, fmin(qm[a], qp[a]));
+    }
+    double phi = 1.0;
+    if (NONLIN) {  // Venkatakrishnan (R11)
+      const double e2 = c_geo.eps_venkat2;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+#pragma unroll
+        for (int s = -1; s <= 1; s += 2) {
+          const double d2 = 0.5 * s * b[a];
+          double ph = 1.0;
+          if (d2 != 0.0) {
+            const double d1 = d2 > 0.0 ? qmax - q0 : qmin - q0;
+            ph = (d1 * d1 + e2 + 2.0 * d1 * d2) / (d1 * d1 + 2.0 * d2 * d2 + d1 * d2 + e2);
+          }
+          phi = fmin(phi, ph);
+        }
+      }
+      phi = fmax(0.0, fmin(1.0, phi));
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) slope[eidx(15, a * 5 + v, i, j, k)] = (a < DIM) ? phi * b[a] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: interface flux.  One thread per (face, Gauss point); NG consecutive lanes per face.
+// Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
+// The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
+// ---------------------------------------------------------------------------
+template <int DIM, int AX, bool COMPACT, bool BOX>
+__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
+                                               const double* __restrict__ gtab, double* __restrict__ face,
+                                               const TimeState* __restrict__ ts, ErrState* __restrict__ err,
+                                               int stage) {
+  using S = Sten<DIM>;
+  constexpr int NG = COMPACT ? S::NG : 1;
+  constexpr int NB = S::NB;
+  constexpr int NV = COMPACT ? 20 : 5;
+  constexpr int NF = COMPACT ? 30 : 10;
+  // Gauss-point basis tables of this axis: [side][gp][val, d0, d1, d2][NB]
+  __shared__ double tab[COMPACT ? 2 * NG * 4 * NB : 1];
+  if (COMPACT) {
+    for (int q = threadIdx.x; q < 2 * NG * 4 * NB; q += blockDim.x) tab[q] = gtab[q];
+    __syncthreads();
+  }
+  if (err->code) return;
+  const double dt = ts->dt;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int gp = (int)(t % NG);
+  const long long f = t / NG;
+  const int fn0 = c_geo.fn[AX][0], fn1 = c_geo.fn[AX][1], fn2 = c_geo.fn[AX][2];
+  const long long nfaces = (long long)fn0 * fn1 * fn2;
+  const bool valid = f < nfaces;
+  const long long fc = valid ? f : 0;
+  const int i = (int)(fc % fn0), j = (int)((fc / fn0) % fn1), k = (int)(fc / ((long long)fn0 * fn1));
+  const int li = i - (AX == 0), lj = j - (AX == 1), lk = k - (AX == 2);
+
+  double W[2][5], dW[2][3][5];  // global frame
+  if (COMPACT) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int ci = s ? i : li, cj = s ? j : lj, ck = s ? k : lk;
+      const double* tv = tab + ((s * NG + gp) * 4) * NB;
+#pragma unroll 1
+      for (int v = 0; v < 5; ++v) {
+        double w = ld_state<BOX>(U, NV, v, ci, cj, ck);
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          const double a = __ldg(rec + eidx(NB * 5, q * 5 + v, ci, cj, ck));
+          w = fma(a, tv[q], w);
+          d0 = fma(a, tv[NB + q], d0);
+          if (DIM > 1) d1 = fma(a, tv[2 * NB + q], d1);
+          if (DIM > 2) d2 = fma(a, tv[3 * NB + q], d2);
+        }
+        W[s][v] = w;
+        dW[s][0][v] = d0 * c_geo.ih[0];
+        dW[s][1][v] = d1 * c_geo.ih[1];
+        dW[s][2][v] = d2 * c_geo.ih[2];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int ci = s ? i : li, cj = s ? j : lj, ck = s ? k : lk;
+      const double side = s ? -0.5 : 0.5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double q = ld_state<BOX>(U, NV, v, ci, cj, ck);
+        const double sa = __ldg(rec + eidx(15, AX * 5 + v, ci, cj, ck));
+        W[s][v] = q + side * sa;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) dW[s][a][v] = __ldg(rec + eidx(15, a * 5 + v, ci, cj, ck)) * c_geo.ih[a];
+      }
+    }
+  }
+  // rotate into the normal frame (cyclic permutation: normal first), bit-exact
+  constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
+  double wl[5], wr[5], dl[3][5], dr[3][5];
+  wl[0] = W[0][0]; wl[1] = W[0][1 + P0]; wl[2] = W[0][1 + P1]; wl[3] = W[0][1 + P2]; wl[4] = W[0][4];
+  wr[0] = W[1][0]; wr[1] = W[1][1 + P0]; wr[2] = W[1][1 + P1]; wr[3] = W[1][1 + P2]; wr[4] = W[1][4];
+  const int pp[3] = {P0, P1, P2};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    dl[d][0] = dW[0][pp[d]][0];
+    dl[d][1] = dW[0][pp[d]][1 + P0];
+    dl[d][2] = dW[0][pp[d]][1 + P1];
+    dl[d][3] = dW[0][pp[d]][1 + P2];
+    dl[d][4] = dW[0][pp[d]][4];
+    dr[d][0] = dW[1][pp[d]][0];
+    dr[d][1] = dW[1][pp[d]][1 + P0];
+    dr[d][2] = dW[1][pp[d]][1 + P1];
+    dr[d][3] = dW[1][pp[d]][1 + P2];
+    dr[d][4] = dW[1][pp[d]][4];
+  }
+  GPOut o;
+  bool ok = gks_flux_point<COMPACT>(wl, dl, wr, dr, dt, c_fc, o);
+  if (valid && !ok) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
+  // back to the global frame, weight 1/NG, sum over the NG lanes of this face
+  double out[NF];
+  const double wgt = 1.0 / NG;
+  const double* src[6] = {o.Fn, o.Ft, o.QLn, o.QLt, o.QRn, o.QRt};
+#pragma unroll
+  for (int s = 0; s < NF / 5; ++s) {
+    out[s * 5 + 0] = wgt * src[s][0];
+    out[s * 5 + 1 + P0] = wgt * src[s][1];
+    out[s * 5 + 1 + P1] = wgt * src[s][2];
+    out[s * 5 + 1 + P2] = wgt * src[s][3];
+    out[s * 5 + 4] = wgt * src[s][4];
+  }
+  if (NG > 1) {
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+#pragma unroll
+      for (int m = 1; m < NG; m <<= 1) out[q] += __shfl_xor_sync(0xffffffffu, out[q], m);
+    }
+  }
+  if (valid && gp == 0) {
+    const long long fpl = (long long)fn0 * fn1;
+    const long long base = (long long)k * NF * fpl + (long long)j * fn0 + i;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) face[base + q * fpl] = out[q];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: residual, Gauss-theorem gradients and stage update
+//   MODE 0: S2O4 stage 1  (Uin = U^n -> Uout = U*, carry)
+//   MODE 1: S2O4 stage 2  (carry -> Uout = U^{n+1})
+//   MODE 2: S1O2          (Uin = U^n -> Uout = U^{n+1})
+// ---------------------------------------------------------------------------
+template <int DIM, bool COMPACT, int MODE>
+__global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, const double* __restrict__ fx,
+                                                 const double* __restrict__ fy, const double* __restrict__ fz,
+                                                 double* __restrict__ Uout, double* __restrict__ carry,
+                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err) {
+  constexpr int NV = COMPACT ? 20 : 5;
+  constexpr int NF = COMPACT ? 30 : 10;
+  if (err->code) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  if (t >= nc) return;
+  const int i = (int)(t % c_geo.n[0]);
+  const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
+  const int k = (int)(t / c_geo.plane);
+  const double dt = ts->dt;
+  double L[5] = {0, 0, 0, 0, 0}, Lt[5] = {0, 0, 0, 0, 0};
+  double Gn[3][5], Gt[3][5];
+  const double* F[3] = {fx, fy, fz};
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const int fn0 = c_geo.fn[a][0], fn1 = c_geo.fn[a][1];
+    const long long fpl = (long long)fn0 * fn1;
+    const int hi_i = i + (a == 0), hi_j = j + (a == 1), hi_k = k + (a == 2);
+    // periodic axes wrap the high face; bounded axes have n+1 faces
+    const int wi = c_geo.bounded[0] ? hi_i : wrapi(hi_i, c_geo.n[0]);
+    const int wj = c_geo.bounded[1] ? hi_j : wrapi(hi_j, c_geo.n[1]);
+    const int wk = c_geo.bounded[2] ? hi_k : wrapi(hi_k, c_geo.n[2]);
+    const long long lo = (long long)k * NF * fpl + (long long)j * fn0 + i;
+    const long long hi = (long long)wk * NF * fpl + (long long)wj * fn0 + wi;
+    const double ih = c_geo.ih[a];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      L[v] += (__ldg(F[a] + lo + v * fpl) - __ldg(F[a] + hi + v * fpl)) * ih;
+      Lt[v] += (__ldg(F[a] + lo + (5 + v) * fpl) - __ldg(F[a] + hi + (5 + v) * fpl)) * ih;
+      if (COMPACT) {
+        // own side: left-side value at i+1/2, right-side value at i-1/2 (R24)
+        Gn[a][v] = (__ldg(F[a] + hi + (10 + v) * fpl) - __ldg(F[a] + lo + (20 + v) * fpl)) * ih;
+        Gt[a][v] = (__ldg(F[a] + hi + (15 + v) * fpl) - __ldg(F[a] + lo + (25 + v) * fpl)) * ih;
+      }
+    }
+  }
+  double Qo[5];
+  if (MODE == 0) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const double q = __ldg(Uin + sidx(NV, v, i, j, k));
+      Qo[v] = q + 0.5 * dt * L[v] + 0.125 * dt * dt * Lt[v];
+      carry[sidx(NV, v, i, j, k)] = q + dt * L[v] + (dt * dt / 6.0) * Lt[v];
+      Uout[sidx(NV, v, i, j, k)] = Qo[v];
+    }
+    if (COMPACT) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double gn = a < DIM ? Gn[a][v] : 0.0, gt = a < DIM ? Gt[a][v] : 0.0;
+          Uout[sidx(NV, 5 + a * 5 + v, i, j, k)] = gn + 0.5 * dt * gt;
+          carry[sidx(NV, 5 + a * 5 + v, i, j, k)] = gn;
+        }
+    }
+  } else if (MODE == 1) {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Qo[v] = __ldg(carry + sidx(NV, v, i, j, k)) + (dt * dt / 3.0) * Lt[v];
+      Uout[sidx(NV, v, i, j, k)] = Qo[v];
+    }
+    if (COMPACT) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double gt = a < DIM ? Gt[a][v] : 0.0;
+          Uout[sidx(NV, 5 + a * 5 + v, i, j, k)] = __ldg(carry + sidx(NV, 5 + a * 5 + v, i, j, k)) + dt * gt;
+        }
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Qo[v] = __ldg(Uin + sidx(NV, v, i, j, k)) + dt * L[v] + 0.5 * dt * dt * Lt[v];
+      Uout[sidx(NV, v, i, j, k)] = Qo[v];
+    }
+    if (COMPACT) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double gn = a < DIM ? Gn[a][v] : 0.0, gt = a < DIM ? Gt[a][v] : 0.0;
+          Uout[sidx(NV, 5 + a * 5 + v, i, j, k)] = gn + dt * gt;
+        }
+    }
+  }
+  // positivity of the updated state (R30)
+  const double ke = 0.5 * (Qo[1] * Qo[1] + Qo[2] * Qo[2] + Qo[3] * Qo[3]) / Qo[0];
+  const double p = (c_geo.gamma - 1.0) * (Qo[4] - ke);
+  if (!(Qo[0] > 0.0) || !(p > 0.0)) flag_error(err, 3, 2, MODE == 0 ? 1 : 2, ts->steps, i, j, k);
+}
+
+// ---------------------------------------------------------------------------
+// K4: CFL time step (R25): per-cell candidate, warp-shuffle min, block min, atomicMin on the
+// bit pattern (order-preserving for positive doubles); NaN -> numerical error
+// ---------------------------------------------------------------------------
+template <int DIM>
+__global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV, TimeState* __restrict__ ts,
+                                             ErrState* __restrict__ err) {
+  __shared__ double red[8];
+  if (err->code) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  double cand = 1e300;
+  if (t < nc) {
+    const int i = (int)(t % c_geo.n[0]);
+    const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
+    const int k = (int)(t / c_geo.plane);
+    double q[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) q[v] = __ldg(U + sidx(NV, v, i, j, k));
+    const double ir = 1.0 / q[0];
+    const double u[3] = {q[1] * ir, q[2] * ir, q[3] * ir};
+    const double p = (c_geo.gamma - 1.0) * (q[4] - 0.5 * q[0] * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
+    if (!(q[0] > 0.0) || !(p > 0.0)) {
+      flag_error(err, 3, 3, 0, ts->steps, i, j, k);
+    } else {
+      const double c = sqrt(c_geo.gamma * p * ir);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        double d = c_geo.h[a] / (fabs(u[a]) + c);
+        if (c_geo.mu > 0.0) d = fmin(d, c_geo.h[a] * c_geo.h[a] / (3.0 * c_geo.mu * ir));
+        cand = fmin(cand, d);
+      }
+      if (!(cand == cand)) flag_error(err, 4, 3, 0, ts->steps, i, j, k);
+    }
+  }
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = cand;
+  __syncthreads();
+  if (w == 0) {
+    cand = l < (blockDim.x >> 5) ? red[l] : 1e300;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
+    if (l == 0) atomicMin(&ts->dtmin_bits, (unsigned long long)__double_as_longlong(cand));
+  }
+}
+
+__global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
+  if (err->code) return;
+  const double m = __longlong_as_double((long long)ts->dtmin_bits);
+  ts->dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
+  ts->dtmin_bits = (unsigned long long)__double_as_longlong(1e300);
+}
+
+__global__ void k_step_end(TimeState* ts, const ErrState* err) {
+  if (err->code) return;
+  ts->t += ts->dt;
+  ts->steps += 1;
+}
+
+// user layout [f][z][y][x]  <->  internal [z][f][y][x]
+__global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  if (t >= nc * nf) return;
+  const int f = (int)(t / nc);
+  const long long c = t % nc;
+  const int k = (int)(c / c_geo.plane);
+  const long long r = c % c_geo.plane;
+  dst[((long long)k * NV + f0 + f) * c_geo.plane + r] = src ? src[t] : 0.0;
+}
+
+__global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  if (t >= nc * nf) return;
+  const int f = (int)(t / nc);
+  const long long c = t % nc;
+  const int k = (int)(c / c_geo.plane);
+  const long long r = c % c_geo.plane;
+  dst[t] = src[((long long)k * NV + f0 + f) * c_geo.plane + r];
+}
+
+}  // namespace cgks

@@ -1,0 +1,208 @@
+"""GPU parity: the sm_100a library (through its C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances (BASELINE north_star): relative L-infinity <= 1e-10 per
+conservative variable and gradient after 10 steps, <= 1e-8 after 100 steps (R34).
+Uniform flow must be preserved bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from cgks_inputs import double_sod, hit, random_smooth, shock_vortex, tgv, uniform, vortex
+from parity_util import floors, rel_linf, worst
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    from paper_2508_19911_b200 import Solver
+    return Solver
+
+
+def _run_both(case, scheme, nsteps, time_scheme=None, **kw):
+    ts = time_scheme if time_scheme is not None else (2 if scheme == 1 else 1)
+    d = case.problem_kwargs()
+    d.update(kw)
+    prob = oracle.Problem(**d, scheme=scheme, time_scheme=ts)
+    Qo, Go, to, dto, rc = oracle.run(prob, case.Q, case.G, nsteps)
+    assert rc == 0
+    S = _gpu().from_case(case, scheme=scheme, time_scheme=ts, **kw)
+    S.set_state(np.ascontiguousarray(case.Q), np.ascontiguousarray(case.G))
+    S.step(nsteps)
+    Qg, Gg = S.get_state()
+    tg, sg, dtg = S.get_time()
+    S.close()
+    assert sg == nsteps
+    assert abs(tg - to) <= 1e-13 * to
+    return Qg, Gg, Qo, Go
+
+
+def _L(case):
+    return max(case.hi[a] - case.lo[a] for a in range(case.dim))
+
+
+def _check(Qg, Gg, Qo, Go, scheme, tol, L=1.0):
+    r = rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, L=L)
+    k, v = worst(r)
+    assert v <= tol, (k, v, r)
+    return r
+
+
+CASES_3D = [
+    ("cgks5-linear", 1, 0, 2, dict(mu=2e-3, Pr=0.72)),
+    ("cgks5-geno", 1, 1, 2, dict(mu=2e-3, Pr=0.72)),
+    ("cgks5-inviscid-s1o2", 1, 0, 1, dict(mu=0.0, Pr=1.0)),
+    ("gks2-linear-s1o2", 0, 0, 1, dict(mu=2e-3, Pr=0.72)),
+    ("gks2-venkat-s2o4", 0, 1, 2, dict(mu=2e-3, Pr=0.72)),
+]
+
+
+@pytest.mark.parametrize("name,scheme,nl,ts,kw", CASES_3D, ids=[c[0] for c in CASES_3D])
+def test_parity_3d_ragged_10_steps(name, scheme, nl, ts, kw):
+    # ragged sizes: several 32-wide x tiles plus a tail, odd y/z
+    case = random_smooth((37, 11, 9), seed=21, jump=0.4 if nl else 0.0)
+    case.nonlinear = nl
+    Qg, Gg, Qo, Go = _run_both(case, scheme, 10, time_scheme=ts, **kw)
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+
+
+@pytest.mark.parametrize("scheme,ts", [(1, 2), (0, 1), (0, 2)])
+def test_parity_vortex_config1(scheme, ts):
+    # BASELINE configs[0]: 40x40 isentropic vortex, CFL 0.5, accuracy mode; parity after 10 and 20 steps
+    case = vortex(40)
+    for n, tol in [(10, 1e-10), (20, 1e-10)]:
+        Qg, Gg, Qo, Go = _run_both(case, scheme, n, time_scheme=ts)
+        _check(Qg, Gg, Qo, Go, scheme, tol, _L(case))
+
+
+@pytest.mark.parametrize("scheme", [1, 0])
+def test_parity_100_steps(scheme):
+    case = random_smooth((12, 10, 8), seed=5)
+    Qg, Gg, Qo, Go = _run_both(case, scheme, 100, mu=1e-3, Pr=0.72)
+    _check(Qg, Gg, Qo, Go, scheme, 1e-8, _L(case))
+
+
+@pytest.mark.parametrize("scheme", [1, 0])
+def test_parity_shock_vortex_box_bc(scheme):
+    # config 4 geometry at reduced size: inflow/outflow in x, periodic y, nonlinear (R29)
+    case = shock_vortex(nx=96, ny=48)
+    Qg, Gg, Qo, Go = _run_both(case, scheme, 10)
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+
+
+@pytest.mark.parametrize("scheme", [1, 0])
+def test_parity_double_sod_1d(scheme):
+    case = double_sod(100)
+    Qg, Gg, Qo, Go = _run_both(case, scheme, 20)
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+
+
+@pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 1)])
+def test_uniform_flow_bitwise_gpu(scheme, nl):
+    case = uniform((19, 7, 6), state=(1.3, 0.4, -0.3, 0.2, 0.9))
+    Solver = _gpu()
+    S = Solver.from_case(case, scheme=scheme, nonlinear=nl, mu=1e-3, Pr=0.72)
+    S.set_state(case.Q, case.G)
+    S.step(10)
+    Qg, Gg = S.get_state()
+    S.close()
+    assert np.array_equal(Qg, case.Q)
+    assert np.all(Gg == 0.0)
+
+
+def test_positivity_error_keeps_last_state():
+    case = random_smooth((16, 8, 6), seed=2)
+    Q = case.Q.copy()
+    Solver = _gpu()
+    S = Solver.from_case(case, scheme=1)
+    S.set_state(Q, case.G)
+    S.step(2)
+    Q2, G2 = S.get_state()
+    # poison one cell of the current state and continue: the step must fail with code 3
+    Qb = Q2.copy()
+    Qb[0, 2, 3, 4] = -1.0
+    S.set_state(Qb, G2)
+    rc = S.step_rc(3)
+    assert rc == 3
+    assert "positivity" in S.last_error()
+    Q3, _ = S.get_state()
+    assert np.array_equal(Q3, Qb)
+    t, steps, _ = S.get_time()
+    assert steps == 0
+    S.close()
+
+
+def _sampled_one_step(case, scheme, samples, seed=0, nonlinear=None):
+    """Full-size parity in the bench launch configuration: one GPU step on the whole grid; the oracle
+    steps a 9^dim periodic box around each sampled cell (the one-step dependency radius is 4 cells,
+    2 per stage) with the global dt computed by the oracle from the full field."""
+    d = case.problem_kwargs()
+    if nonlinear is not None:
+        d["nonlinear"] = nonlinear
+    prob = oracle.Problem(**d, scheme=scheme, time_scheme=2 if scheme == 1 else 1)
+    dt = oracle.dt(prob, case.Q)
+    Solver = _gpu()
+    S = Solver.from_case(case, scheme=scheme, nonlinear=d["nonlinear"])
+    S.set_state(case.Q, case.G)
+    S.step(1)
+    Qg, Gg = S.get_state()
+    tg, _, _ = S.get_time()
+    S.close()
+    assert abs(tg - dt) <= 1e-14 * dt
+    rng = np.random.default_rng(seed)
+    dim = case.dim
+    nn = case.n
+    r = 4
+    errs = []
+    for _ in range(samples):
+        c = []
+        for a in range(3):
+            if a >= dim:
+                c.append(0)
+            elif case.bc[a][0] != 0:  # bounded axis: stay clear of the boundary (box is periodic)
+                c.append(int(rng.integers(r + 1, nn[a] - r - 1)))
+            else:
+                c.append(int(rng.integers(0, nn[a])))
+        idx = [np.arange(c[a] - r, c[a] + r + 1) % nn[a] if a < dim else np.array([0]) for a in range(3)]
+        Qb = case.Q[:, idx[2]][:, :, idx[1]][:, :, :, idx[0]]
+        Gb = case.G[:, :, idx[2]][:, :, :, idx[1]][:, :, :, :, idx[0]]
+        bn = tuple(len(idx[a]) for a in range(3))
+        h = [(case.hi[a] - case.lo[a]) / nn[a] for a in range(3)]
+        pb = oracle.Problem(**{**d, "n": bn, "lo": (0, 0, 0), "hi": tuple(bn[a] * h[a] for a in range(3)),
+                               "bc": ((0, 0), (0, 0), (0, 0))},
+                            scheme=scheme, time_scheme=2 if scheme == 1 else 1, fixed_dt=dt)
+        Qo, Go, _, _, rc = oracle.run(pb, Qb, Gb, 1)
+        assert rc == 0
+        cc = tuple(r if a < dim else 0 for a in range(3))
+        qo = Qo[:, cc[2], cc[1], cc[0]]
+        qg = Qg[:, c[2], c[1], c[0]]
+        qs, gs = floors(Qg, Gg if scheme == 1 else None, _L(case))  # R34 floors of the stepped field
+        errs.append(np.abs(qg - qo) / qs)
+        if scheme == 1:
+            go = Go[:, :, cc[2], cc[1], cc[0]]
+            gg = Gg[:, :, c[2], c[1], c[0]]
+            errs.append((np.abs(gg - go) / gs[None, :]).ravel())
+    return max(float(np.max(e)) for e in errs)
+
+
+def test_full_size_tgv128_cgks5_sampled():
+    # the bench workload: TGV 128^3, CGKS-5th linear, one step in the bench launch configuration
+    e = _sampled_one_step(tgv(128), 1, samples=12)
+    assert e <= 1e-10, e
+
+
+def test_full_size_tgv128_gks2_sampled():
+    e = _sampled_one_step(tgv(128), 0, samples=12)
+    assert e <= 1e-10, e
+
+
+@pytest.mark.slow
+def test_full_size_hit128_sampled():
+    e = _sampled_one_step(hit(128), 1, samples=8)
+    assert e <= 1e-10, e
+
+
+@pytest.mark.slow
+def test_full_size_shock_vortex_sampled():
+    # box boundaries: sample only interior cells (the 9-wide periodic box cannot represent the x boundary)
+    case = shock_vortex()
+    e = _sampled_one_step(case, 1, samples=16)
+    assert e <= 1e-10, e
