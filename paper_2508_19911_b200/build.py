@@ -8,12 +8,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcgks.so")
-SOURCES = ["cgks_api.cu", "cls_build.cpp"]
-HEADERS = ["kernels.cuh", "gks_flux.cuh", "cls_build.h", "flop_count.h"]
+SOURCES = ["cgks_api.cu", "cls_build.cpp", "stage_d1.cu", "stage_d2.cu", "stage_d3.cu"]
+HEADERS = ["kernels.cuh", "gks_flux.cuh", "cls_build.h", "flop_count.h", "recon_gen.cuh", "types.h", "driver.h",
+           "stage_impl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+BUILD = os.path.join(HERE, "build")
 
 
 def needs_build() -> bool:
@@ -26,18 +28,36 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    sys.path.insert(0, HERE)
+    import gen_recon
+    gen_recon.emit()
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lcudart"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    os.makedirs(BUILD, exist_ok=True)
     log = os.path.join(HERE, "build.log")
+    procs, objs = [], []
+    for s in SOURCES:  # one process per translation unit, in parallel
+        obj = os.path.join(BUILD, s + ".o")
+        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, s), "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    text, failed = "", False
+    for cmd, p in procs:
+        out, err = p.communicate()
+        text += " ".join(cmd) + "\n" + out + err
+        failed |= p.returncode != 0
+    if not failed:
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        text += " ".join(cmd) + "\n" + r.stdout + r.stderr
+        failed = r.returncode != 0
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr[-6000:])
+        f.write(text)
+    if failed:
+        sys.stderr.write(text[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stdout.write(r.stderr)
+        sys.stdout.write(text)
     return LIB
 
 

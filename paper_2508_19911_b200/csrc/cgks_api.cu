@@ -10,10 +10,19 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+
 #include "../../include/cgks.h"
 #include "cls_build.h"
+#include "driver.h"
 #include "flop_count.h"
-#include "kernels.cuh"
+#include "types.h"
+namespace cgks {
+template <int DIM>
+struct ReconGen;
+}
+#define CGKS_RECON_GEN_HOST_TABLES
+#include "recon_gen.cuh"
 
 using namespace cgks;
 
@@ -38,12 +47,15 @@ struct cgks_ctx {
   ErrState* err = nullptr;
   int cur = 0;
   ClsTables cls;
+  double Rp[ReconGen<3>::NNZ];  // parity-blocked CLS matrix packed in the generated FMA order
+  int nnz = 0;
   char msg[512] = {0};
   // profiling
   bool prof = false;
   std::map<std::string, std::pair<double, long long>> ptimes;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   int launches_per_step = 0;
+  const DimOps* ops = nullptr;
 };
 
 static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
@@ -68,114 +80,54 @@ static void set_msg(cgks_ctx* c, const char* fmt, ...) {
 
 static int upload_constants(cgks_ctx* ctx) {
   if (g_const_owner == ctx) return CGKS_OK;
-  CK(cudaMemcpyToSymbolAsync(c_geo, &ctx->geo, sizeof(Geo), 0, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyToSymbolAsync(c_fc, &ctx->fc, sizeof(FluxConst), 0, cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->scheme_id == CGKS_CGKS5)
-    CK(cudaMemcpyToSymbolAsync(c_R, ctx->cls.R, sizeof(double) * ctx->cls.nb * ctx->cls.nd, 0,
-                               cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->ops->upload(ctx->geo, ctx->fc, ctx->Rp, ctx->scheme_id == CGKS_CGKS5 ? ctx->nnz : 0, ctx->stream)) {
+    set_msg(ctx, "constant upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return CGKS_ERR_CUDA;
+  }
   g_const_owner = ctx;
   return CGKS_OK;
 }
 
-// launch helper with optional per-launch event timing
-template <typename... KArgs, typename... Args>
-static int launch(cgks_ctx* ctx, const char* name, void (*kern)(KArgs...), long long nthreads, int block,
-                  Args... args) {
-  if (nthreads <= 0) return CGKS_OK;
-  long long nblk = (nthreads + block - 1) / block;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->prof) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, ctx->stream);
-  }
-  kern<<<(unsigned)nblk, block, 0, ctx->stream>>>(args...);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_msg(ctx, "launch of %s failed: %s", name, cudaGetErrorString(e));
-    return CGKS_ERR_CUDA;
-  }
-  if (ctx->prof) {
-    cudaEventRecord(e1, ctx->stream);
-    ctx->pending.push_back({name, {e0, e1}});
-  }
-  return CGKS_OK;
-}
-
-#define LAUNCH(name, kern, n, blk, ...)                                \
-  do {                                                                 \
-    int rc_ = launch(ctx, name, kern, (long long)(n), blk, __VA_ARGS__); \
-    if (rc_) return rc_;                                               \
-  } while (0)
-
-// ---------------------------------------------------------------------------
-// one stage: reconstruction, fluxes along each active axis, update
-// ---------------------------------------------------------------------------
-template <int DIM, bool COMPACT, bool NONLIN, bool BOX>
-static int stage_t(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
-  if (COMPACT) {
-    LAUNCH("recon5", (k_recon5<DIM, NONLIN, BOX>), ctx->necell, 128, Uin, ctx->rec, ctx->err);
-  } else {
-    LAUNCH("recon2", (k_recon2<DIM, NONLIN, BOX>), ctx->necell, 256, Uin, ctx->rec, ctx->err);
-  }
-  constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
-  for (int a = 0; a < DIM; ++a) {
-    long long nf = (long long)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
-    if (a == 0)
-      LAUNCH("flux_x", (k_flux<DIM, 0, COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[0], ctx->face[0],
-             ctx->ts, ctx->err, stage);
-    if (a == 1)
-      LAUNCH("flux_y", (k_flux<DIM, (DIM > 1 ? 1 : 0), COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[1],
-             ctx->face[1], ctx->ts, ctx->err, stage);
-    if (a == 2)
-      LAUNCH("flux_z", (k_flux<DIM, (DIM > 2 ? 2 : 0), COMPACT, BOX>), nf * NG, 128, Uin, ctx->rec, ctx->gtab[2],
-             ctx->face[2], ctx->ts, ctx->err, stage);
-  }
-  if (mode == 0)
-    LAUNCH("update", (k_update<DIM, COMPACT, 0>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
-           Uout, ctx->carry, ctx->ts, ctx->err);
-  else if (mode == 1)
-    LAUNCH("update", (k_update<DIM, COMPACT, 1>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
-           Uout, ctx->carry, ctx->ts, ctx->err);
-  else
-    LAUNCH("update", (k_update<DIM, COMPACT, 2>), ctx->ncell, 256, Uin, ctx->face[0], ctx->face[1], ctx->face[2],
-           Uout, ctx->carry, ctx->ts, ctx->err);
-  return CGKS_OK;
-}
-
-template <int DIM>
-static int stage_dim(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
-  bool c = ctx->scheme_id == CGKS_CGKS5, nl = ctx->nonlinear != 0, b = ctx->box != 0;
-  if (c && !nl && !b) return stage_t<DIM, true, false, false>(ctx, Uin, Uout, mode, stage);
-  if (c && nl && !b) return stage_t<DIM, true, true, false>(ctx, Uin, Uout, mode, stage);
-  if (c && !nl && b) return stage_t<DIM, true, false, true>(ctx, Uin, Uout, mode, stage);
-  if (c && nl && b) return stage_t<DIM, true, true, true>(ctx, Uin, Uout, mode, stage);
-  if (!c && !nl && !b) return stage_t<DIM, false, false, false>(ctx, Uin, Uout, mode, stage);
-  if (!c && nl && !b) return stage_t<DIM, false, true, false>(ctx, Uin, Uout, mode, stage);
-  if (!c && !nl && b) return stage_t<DIM, false, false, true>(ctx, Uin, Uout, mode, stage);
-  return stage_t<DIM, false, true, true>(ctx, Uin, Uout, mode, stage);
+static LaunchEnv env_of(cgks_ctx* ctx) {
+  LaunchEnv e;
+  e.stream = ctx->stream;
+  e.prof = ctx->prof;
+  e.pending = &ctx->pending;
+  e.msg = ctx->msg;
+  e.msglen = (int)sizeof(ctx->msg);
+  return e;
 }
 
 static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
-  if (ctx->dim == 3) return stage_dim<3>(ctx, Uin, Uout, mode, stage);
-  if (ctx->dim == 2) return stage_dim<2>(ctx, Uin, Uout, mode, stage);
-  return stage_dim<1>(ctx, Uin, Uout, mode, stage);
-}
-
-static int launch_dt(cgks_ctx* ctx, const double* Uin) {
-  if (ctx->dim == 3) LAUNCH("dt", k_dt<3>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
-  if (ctx->dim == 2) LAUNCH("dt", k_dt<2>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
-  if (ctx->dim == 1) LAUNCH("dt", k_dt<1>, ctx->ncell, 256, Uin, ctx->NV, ctx->ts, ctx->err);
-  LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ctx->ts, (const ErrState*)ctx->err);
-  return CGKS_OK;
+  StageArgs a;
+  a.Uin = Uin;
+  a.Uout = Uout;
+  a.carry = ctx->carry;
+  a.rec = ctx->rec;
+  for (int d = 0; d < 3; ++d) {
+    a.face[d] = ctx->face[d];
+    a.gtab[d] = ctx->gtab[d];
+    a.nface[d] = (long long)ctx->geo.fn[d][0] * ctx->geo.fn[d][1] * ctx->geo.fn[d][2];
+  }
+  a.ts = ctx->ts;
+  a.err = ctx->err;
+  a.ncell = ctx->ncell;
+  a.necell = ctx->necell;
+  a.scheme = ctx->scheme_id;
+  a.nonlinear = ctx->nonlinear;
+  a.box = ctx->box;
+  LaunchEnv env = env_of(ctx);
+  int rc = ctx->ops->stage(env, a, mode, stage);
+  return rc ? CGKS_ERR_CUDA : CGKS_OK;
 }
 
 // one full time step from U[cur] into U[1-cur]
 static int one_step(cgks_ctx* ctx) {
   const double* Un = ctx->U[ctx->cur];
   double* Unext = ctx->U[1 - ctx->cur];
-  int rc = launch_dt(ctx, Un);
-  if (rc) return rc;
+  LaunchEnv env = env_of(ctx);
+  if (ctx->ops->dt(env, Un, ctx->NV, ctx->ts, ctx->err, ctx->ncell)) return CGKS_ERR_CUDA;
+  int rc;
   if (ctx->time_scheme == CGKS_TIME_S1O2) {
     rc = run_stage(ctx, Un, Unext, 2, 1);
   } else {
@@ -183,7 +135,7 @@ static int one_step(cgks_ctx* ctx) {
     if (!rc) rc = run_stage(ctx, ctx->Us, Unext, 1, 2);
   }
   if (rc) return rc;
-  LAUNCH("step_end", k_step_end, 1, 32, ctx->ts, (const ErrState*)ctx->err);
+  if (ctx->ops->step_end(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
   ctx->cur = 1 - ctx->cur;
   return CGKS_OK;
 }
@@ -250,6 +202,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     return fail(CGKS_ERR_CONFIG);
   }
   ctx->dim = dim;
+  ctx->ops = dim == 3 ? &kOps3 : (dim == 2 ? &kOps2 : &kOps1);
   ctx->sch = *scheme;
   ctx->scheme_id = scheme->id;
   ctx->nonlinear = scheme->nonlinear ? 1 : 0;
@@ -312,6 +265,39 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       set_msg(ctx, "%s", e);
       return fail(CGKS_ERR_CONFIG);
     }
+    // R' = R T^{-1} with T the parity-combination matrix (rows mutually orthogonal): T^{-1} = T^T diag(1/|T_c|^2)
+    const int nd = ctx->cls.nd, nb = ctx->cls.nb;
+    const signed char* T = dim == 3 ? &kGenT3[0][0] : (dim == 2 ? &kGenT2[0][0] : &kGenT1[0][0]);
+    const short* P = dim == 3 ? &kGenPairs3[0][0] : (dim == 2 ? &kGenPairs2[0][0] : &kGenPairs1[0][0]);
+    const int nnz = dim == 3 ? kGenNNZ3 : (dim == 2 ? kGenNNZ2 : kGenNNZ1);
+    const int gnd = dim == 3 ? kGenND3 : (dim == 2 ? kGenND2 : kGenND1);
+    if (gnd != nd) {
+      set_msg(ctx, "generated reconstruction tables do not match the CLS data layout");
+      return fail(CGKS_ERR_CONFIG);
+    }
+    std::vector<double> Rp((size_t)nb * nd, 0.0);
+    for (int c = 0; c < nd; ++c) {
+      double n2 = 0.0;
+      for (int r = 0; r < nd; ++r) n2 += (double)T[c * nd + r] * T[c * nd + r];
+      for (int kk = 0; kk < nb; ++kk) {
+        long double s = 0.0L;
+        for (int r = 0; r < nd; ++r) s += (long double)ctx->cls.R[kk * nd + r] * T[c * nd + r];
+        Rp[(size_t)kk * nd + c] = (double)(s / n2);
+      }
+    }
+    std::vector<char> inblock((size_t)nb * nd, 0);
+    double rmax = 0.0;
+    for (double x : Rp) rmax = std::max(rmax, std::fabs(x));
+    for (int q = 0; q < nnz; ++q) {
+      inblock[(size_t)P[2 * q] * nd + P[2 * q + 1]] = 1;
+      ctx->Rp[q] = Rp[(size_t)P[2 * q] * nd + P[2 * q + 1]];
+    }
+    for (size_t q = 0; q < Rp.size(); ++q)
+      if (!inblock[q] && std::fabs(Rp[q]) > 1e-12 * rmax) {
+        set_msg(ctx, "CLS matrix is not parity-block diagonal (entry %zu = %g)", q, Rp[q]);
+        return fail(CGKS_ERR_CONFIG);
+      }
+    ctx->nnz = nnz;
   }
 
   // ---- stream and memory
@@ -425,9 +411,7 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
         dsrc = ctx->staging;
       }
     }
-    long long n = nc * nf;
-    k_pack<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(dsrc, U, ctx->NV, f0, nf);
-    CK(cudaGetLastError());
+    if (ctx->ops->pack(ctx->stream, dsrc, U, ctx->NV, f0, nf, nc)) CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return CGKS_OK;
   };
@@ -492,8 +476,7 @@ int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
     bool dev = is_device_ptr(dst);
     double* ddst = dev ? dst : ctx->staging;
     long long n = nc * nf;
-    k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(U, ddst, ctx->NV, f0, nf);
-    CK(cudaGetLastError());
+    if (ctx->ops->unpack(ctx->stream, U, ddst, ctx->NV, f0, nf, nc)) CK(cudaGetLastError());
     if (!dev) CK(cudaMemcpyAsync(dst, ctx->staging, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return CGKS_OK;
@@ -599,7 +582,10 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
   if (c5) {
     const int NB = ctx->cls.nb, ND = ctx->cls.nd, NC = ctx->cls.nc, NF = 2 * D;
     const int nedge = NC - NF;
-    double per_comp = NC + NF * D + (D == 3 ? 5.0 * nedge : (D == 2 ? 2.0 * nedge : 0.0)) + D + 2.0 * NB * ND;
+    // parity-blocked matvec: 2 flops per block entry, butterfly additions, data formation
+    double per_comp = NC + NF * D + (D == 3 ? 5.0 * nedge : (D == 2 ? 2.0 * nedge : 0.0)) + D +
+                      2.0 * ctx->nnz + (ND - (D == 3 ? 3 : D));
+    (void)NB;
     if (ctx->nonlinear)
       per_comp += NF * 6.0 + NF * (NF * 5.0 + 1.0 + 2.0 * D) + 8.0 + NB + 2.0 * D + 1.0;
     rows.push_back({"recon5", 5.0 * per_comp * nec});

@@ -1,0 +1,52 @@
+// driver.h -- host-side interface between the C ABI (cgks_api.cu) and the per-dimension
+// translation units (stage_d1.cu, stage_d2.cu, stage_d3.cu) that hold the kernels.
+// Each dimension is compiled separately (parallel builds); each owns its constant memory,
+// so the ABI uploads the context's parameters through every unit it uses.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "types.h"
+
+namespace cgks {
+
+struct LaunchEnv {
+  cudaStream_t stream = nullptr;
+  bool prof = false;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>>* pending = nullptr;
+  char* msg = nullptr;
+  int msglen = 0;
+};
+
+struct StageArgs {
+  const double* Uin;
+  double* Uout;
+  double* carry;
+  double* rec;
+  double* face[3];
+  const double* gtab[3];
+  TimeState* ts;
+  ErrState* err;
+  long long ncell, necell;
+  long long nface[3];
+  int scheme;     // 0 GKS-2nd, 1 CGKS-5th
+  int nonlinear;
+  int box;
+};
+
+struct DimOps {
+  int (*upload)(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s);
+  // mode 0: S2O4 stage 1, 1: S2O4 stage 2, 2: S1O2
+  int (*stage)(LaunchEnv& env, const StageArgs& a, int mode, int stage);
+  int (*dt)(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell);
+  int (*step_end)(LaunchEnv& env, TimeState* ts, ErrState* err);
+  int (*pack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
+  int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
+};
+
+extern const DimOps kOps1, kOps2, kOps3;
+
+}  // namespace cgks

@@ -15,49 +15,22 @@
 #include <stdint.h>
 
 #include "gks_flux.cuh"
+#include "types.h"
+
+namespace cgks {
+template <int DIM>
+struct ReconGen;
+}
+#include "recon_gen.cuh"
 
 namespace cgks {
 
 constexpr int NBmax = 34;
 
-// ---------------------------------------------------------------------------
-// constant geometry / parameters
-// ---------------------------------------------------------------------------
-struct Geo {
-  int n[3];          // local cells
-  int dim;
-  int bounded[3];    // axis has non-periodic boundaries
-  int elo[3];        // extended (reconstruction) range start: -1 on bounded axes
-  int en[3];         // extended counts
-  int fn[3][3];      // face-grid dims for faces normal to axis a: fn[a][b]
-  long long plane;   // n0*n1
-  long long eplane;  // en0*en1
-  double h[3], ih[3];
-  int bc[3][2];
-  double bc_state[3][2][5];
-  double cfl, fixed_dt, mu, gamma;
-  double k_venkat, chi_c, eps_venkat2;
-};
-
-struct ErrState {
-  int code;        // 0 ok, 3 positivity, 4 numerical
-  int stage;       // 1, 2
-  long long step;  // global step index at failure
-  int cell[3];
-  int kernel;      // 1 flux, 2 update, 3 dt
-};
-
-struct TimeState {
-  double t;
-  long long steps;
-  double dt;
-  unsigned long long dtmin_bits;
-  int pad;
-};
-
-__constant__ Geo c_geo;
-__constant__ FluxConst c_fc;
-__constant__ double c_R[34 * 63];
+// per translation unit (one per dimension, see stage_impl.cuh): internal linkage
+static __constant__ Geo c_geo;
+static __constant__ FluxConst c_fc;
+static __constant__ double c_Rp[ReconGen<3>::NNZ];  // parity-blocked CLS matrix (gen_recon.py), packed
 
 // ---------------------------------------------------------------------------
 // compile-time stencil tables (match cls_build.cpp ordering)
@@ -154,11 +127,23 @@ __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, 
 // ---------------------------------------------------------------------------
 // K1: CGKS-5th reconstruction (coefficients of P^4 on the reference cell, GENO folded)
 // ---------------------------------------------------------------------------
+template <bool BOX>
+struct Recon5Loader {
+  const double* __restrict__ U;
+  int v, i, j, k;
+  double q0, h0, h1, h2;
+  __device__ __forceinline__ double q(int ox, int oy, int oz) const {
+    return ld_state<BOX>(U, 20, v, i + ox, j + oy, k + oz) - q0;
+  }
+  __device__ __forceinline__ double g(int a, int ox, int oy, int oz) const {
+    return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * ld_state<BOX>(U, 20, 5 + a * 5 + v, i + ox, j + oy, k + oz);
+  }
+};
+
 template <int DIM, bool NONLIN, bool BOX>
 __global__ void __launch_bounds__(128) k_recon5(const double* __restrict__ U, double* __restrict__ coef,
                                                  const ErrState* __restrict__ err) {
   using S = Sten<DIM>;
-  constexpr int NV = 20;
   constexpr int NCO = S::NB * 5;
   if (err->code) return;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,82 +152,31 @@ __global__ void __launch_bounds__(128) k_recon5(const double* __restrict__ U, do
   const int i = (int)(t % c_geo.en[0]) + c_geo.elo[0];
   const int j = (int)((t / c_geo.en[0]) % c_geo.en[1]) + c_geo.elo[1];
   const int k = (int)(t / ((long long)c_geo.en[0] * c_geo.en[1])) + c_geo.elo[2];
-  const double h0 = c_geo.h[0], h1 = c_geo.h[1], h2 = c_geo.h[2];
-  const double hh[3] = {h0, h1, h2};
-  const double rs2 = 0.70710678118654752440;
 
 #pragma unroll 1
   for (int v = 0; v < 5; ++v) {
-    const double q0 = ld_state<BOX>(U, NV, v, i, j, k);
+    Recon5Loader<BOX> L{U, v, i, j, k, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
+    L.q0 = ld_state<BOX>(U, 20, v, i, j, k);
     double acc[S::NB];
 #pragma unroll
     for (int q = 0; q < S::NB; ++q) acc[q] = 0.0;
-    double dface[S::NFACE];
-    // exact rows: neighbour averages minus own average (difference form keeps uniform flow exact)
-#pragma unroll
-    for (int n = 0; n < S::NC; ++n) {
-      const double d = ld_state<BOX>(U, NV, v, i + nbr_off<DIM>(n, 0), j + nbr_off<DIM>(n, 1),
-                                     k + nbr_off<DIM>(n, 2)) - q0;
-      if (n < S::NFACE) dface[n] = d;
-#pragma unroll
-      for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + n], d, acc[q]);
-    }
-    // least-squares rows: face-neighbour gradients (reference units: h_a dQ/dx_a)
-    int row = S::NC;
-#pragma unroll
-    for (int m = 0; m < S::NFACE; ++m) {
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) {
-        const double d = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i + nbr_off<DIM>(m, 0),
-                                               j + nbr_off<DIM>(m, 1), k + nbr_off<DIM>(m, 2));
-#pragma unroll
-        for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], d, acc[q]);
-        ++row;
-      }
-    }
-    // edge neighbours: two directional derivatives (R2) / full gradient in 2-D
-#pragma unroll
-    for (int n = S::NFACE; n < S::NC; ++n) {
-      const int oi = nbr_off<DIM>(n, 0), oj = nbr_off<DIM>(n, 1), ok = nbr_off<DIM>(n, 2);
-      double g[3];
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) g[a] = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i + oi, j + oj, k + ok);
-      double dd[2];
-      if (DIM == 2) {
-        dd[0] = g[0];
-        dd[1] = g[1];
-      } else {
-        const int tax = (oi == 0) ? 0 : (oj == 0 ? 1 : 2);
-        dd[0] = g[tax];
-        dd[1] = rs2 * (oi * g[0] + oj * g[DIM > 1 ? 1 : 0] + ok * g[DIM > 2 ? 2 : 0]);
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-#pragma unroll
-        for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], dd[r], acc[q]);
-        ++row;
-      }
-    }
-    // own gradient (R1)
-    double gown[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-      gown[a] = hh[a] * ld_state<BOX>(U, NV, 5 + a * 5 + v, i, j, k);
-#pragma unroll
-      for (int q = 0; q < S::NB; ++q) acc[q] = fma(c_R[q * S::ND + row], gown[a], acc[q]);
-      ++row;
-    }
+    // parity-blocked constrained least squares: data in difference form, so a
+    // uniform field gives exactly zero coefficients
+    ReconGen<DIM>::matvec(L, c_Rp, acc);
     if (NONLIN) {
       // GENO: sub-stencil linears P_m (R6), IS (R7), weights (R9), chi (R8);
       // Eq. (weno-new) folded into the coefficients (shared zero-mean basis, sum omega = 1)
-      double IS[S::NFACE], bm[S::NFACE][3];
+      double IS[S::NFACE], bm[S::NFACE][3], gown[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) gown[a] = L.g(a, 0, 0, 0);
 #pragma unroll
       for (int m = 0; m < S::NFACE; ++m) {
         const int ax = m / 2;
         const double s = (m % 2) ? 1.0 : -1.0;
+        const double dface = L.q(ax == 0 ? (int)s : 0, ax == 1 ? (int)s : 0, ax == 2 ? (int)s : 0);
 #pragma unroll
         for (int a = 0; a < 3; ++a) bm[m][a] = (a < DIM && a != ax) ? gown[a] : 0.0;
-        bm[m][ax] = s * dface[m];
+        bm[m][ax] = s * dface;
         IS[m] = bm[m][0] * bm[m][0] + bm[m][1] * bm[m][1] + bm[m][2] * bm[m][2];
       }
       const double eps = 1e-15;
@@ -602,21 +536,21 @@ __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV
   }
 }
 
-__global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
+static __global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
   if (err->code) return;
   const double m = __longlong_as_double((long long)ts->dtmin_bits);
   ts->dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
   ts->dtmin_bits = (unsigned long long)__double_as_longlong(1e300);
 }
 
-__global__ void k_step_end(TimeState* ts, const ErrState* err) {
+static __global__ void k_step_end(TimeState* ts, const ErrState* err) {
   if (err->code) return;
   ts->t += ts->dt;
   ts->steps += 1;
 }
 
 // user layout [f][z][y][x]  <->  internal [z][f][y][x]
-__global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
+static __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
   if (t >= nc * nf) return;
@@ -627,7 +561,7 @@ __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst,
   dst[((long long)k * NV + f0 + f) * c_geo.plane + r] = src ? src[t] : 0.0;
 }
 
-__global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
+static __global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
   if (t >= nc * nf) return;

@@ -1,0 +1,7 @@
+// stage_d2.cu -- kernels and launch sequence for 2-D grids (see stage_impl.cuh).
+#define CGKS_DIM 2
+#include "stage_impl.cuh"
+
+namespace cgks {
+const DimOps kOps2 = {upload_fn, stage_fn, dt_fn, step_end_fn, pack_fn, unpack_fn};
+}  // namespace cgks

@@ -1,0 +1,7 @@
+// stage_d3.cu -- kernels and launch sequence for 3-D grids (see stage_impl.cuh).
+#define CGKS_DIM 3
+#include "stage_impl.cuh"
+
+namespace cgks {
+const DimOps kOps3 = {upload_fn, stage_fn, dt_fn, step_end_fn, pack_fn, unpack_fn};
+}  // namespace cgks

@@ -1,0 +1,118 @@
+// stage_impl.cuh -- launch sequence of one stage for dimension CGKS_DIM (included once per
+// translation unit stage_d<D>.cu).
+#pragma once
+#ifndef CGKS_DIM
+#error "define CGKS_DIM before including stage_impl.cuh"
+#endif
+#include <cstdio>
+
+#include "driver.h"
+#include "kernels.cuh"
+
+namespace cgks {
+namespace {
+
+template <typename... KArgs, typename... Args>
+int launch(LaunchEnv& env, const char* name, void (*kern)(KArgs...), long long nthreads, int block, Args... args) {
+  if (nthreads <= 0) return 0;
+  const long long nblk = (nthreads + block - 1) / block;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (env.prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, env.stream);
+  }
+  kern<<<(unsigned)nblk, block, 0, env.stream>>>(args...);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
+    return 5;
+  }
+  if (env.prof) {
+    cudaEventRecord(e1, env.stream);
+    env.pending->push_back({name, {e0, e1}});
+  }
+  return 0;
+}
+
+#define LAUNCH(name, kern, n, blk, ...)                                 \
+  do {                                                                  \
+    int rc_ = launch(env, name, kern, (long long)(n), blk, __VA_ARGS__); \
+    if (rc_) return rc_;                                                \
+  } while (0)
+
+constexpr int D = CGKS_DIM;
+
+template <bool COMPACT, bool NONLIN, bool BOX>
+int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
+  if (COMPACT) {
+    LAUNCH("recon5", (k_recon5<D, NONLIN, BOX>), a.necell, 128, a.Uin, a.rec, a.err);
+  } else {
+    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  }
+  constexpr int NG = COMPACT ? Sten<D>::NG : 1;
+  LAUNCH("flux_x", (k_flux<D, 0, COMPACT, BOX>), a.nface[0] * NG, 128, a.Uin, a.rec, a.gtab[0], a.face[0], a.ts,
+         a.err, stage);
+  if (D > 1)
+    LAUNCH("flux_y", (k_flux<D, (D > 1 ? 1 : 0), COMPACT, BOX>), a.nface[1] * NG, 128, a.Uin, a.rec, a.gtab[1],
+           a.face[1], a.ts, a.err, stage);
+  if (D > 2)
+    LAUNCH("flux_z", (k_flux<D, (D > 2 ? 2 : 0), COMPACT, BOX>), a.nface[2] * NG, 128, a.Uin, a.rec, a.gtab[2],
+           a.face[2], a.ts, a.err, stage);
+  if (mode == 0)
+    LAUNCH("update", (k_update<D, COMPACT, 0>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err);
+  else if (mode == 1)
+    LAUNCH("update", (k_update<D, COMPACT, 1>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err);
+  else
+    LAUNCH("update", (k_update<D, COMPACT, 2>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err);
+  return 0;
+}
+
+int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
+  const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
+  if (c && !nl && !b) return stage_t<true, false, false>(env, a, mode, stage);
+  if (c && nl && !b) return stage_t<true, true, false>(env, a, mode, stage);
+  if (c && !nl && b) return stage_t<true, false, true>(env, a, mode, stage);
+  if (c && nl && b) return stage_t<true, true, true>(env, a, mode, stage);
+  if (!c && !nl && !b) return stage_t<false, false, false>(env, a, mode, stage);
+  if (!c && nl && !b) return stage_t<false, true, false>(env, a, mode, stage);
+  if (!c && !nl && b) return stage_t<false, false, true>(env, a, mode, stage);
+  return stage_t<false, true, true>(env, a, mode, stage);
+}
+
+int upload_fn(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s) {
+  if (cudaMemcpyToSymbolAsync(c_geo, &g, sizeof(Geo), 0, cudaMemcpyHostToDevice, s) != cudaSuccess) return 5;
+  if (cudaMemcpyToSymbolAsync(c_fc, &fc, sizeof(FluxConst), 0, cudaMemcpyHostToDevice, s) != cudaSuccess) return 5;
+  if (nnz > 0 && cudaMemcpyToSymbolAsync(c_Rp, Rp, sizeof(double) * nnz, 0, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return 5;
+  return 0;
+}
+
+int dt_fn(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell) {
+  LAUNCH("dt", k_dt<D>, ncell, 256, U, NV, ts, err);
+  LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ts, (const ErrState*)err);
+  return 0;
+}
+
+int step_end_fn(LaunchEnv& env, TimeState* ts, ErrState* err) {
+  LAUNCH("step_end", k_step_end, 1, 32, ts, (const ErrState*)err);
+  return 0;
+}
+
+int pack_fn(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell) {
+  const long long n = ncell * nf;
+  k_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst, NV, f0, nf);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+int unpack_fn(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell) {
+  const long long n = ncell * nf;
+  k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst, NV, f0, nf);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+}  // namespace
+}  // namespace cgks

@@ -1,0 +1,44 @@
+// types.h -- plain structs shared by host and device code (no device symbols).
+#pragma once
+#include <stdint.h>
+
+#include "gks_flux.cuh"
+
+namespace cgks {
+
+// ---------------------------------------------------------------------------
+// constant geometry / parameters
+// ---------------------------------------------------------------------------
+struct Geo {
+  int n[3];          // local cells
+  int dim;
+  int bounded[3];    // axis has non-periodic boundaries
+  int elo[3];        // extended (reconstruction) range start: -1 on bounded axes
+  int en[3];         // extended counts
+  int fn[3][3];      // face-grid dims for faces normal to axis a: fn[a][b]
+  long long plane;   // n0*n1
+  long long eplane;  // en0*en1
+  double h[3], ih[3];
+  int bc[3][2];
+  double bc_state[3][2][5];
+  double cfl, fixed_dt, mu, gamma;
+  double k_venkat, chi_c, eps_venkat2;
+};
+
+struct ErrState {
+  int code;        // 0 ok, 3 positivity, 4 numerical
+  int stage;       // 1, 2
+  long long step;  // global step index at failure
+  int cell[3];
+  int kernel;      // 1 flux, 2 update, 3 dt
+};
+
+struct TimeState {
+  double t;
+  long long steps;
+  double dt;
+  unsigned long long dtmin_bits;
+  int pad;
+};
+
+}  // namespace cgks
