@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcgks.so")
+LIB_PATH = os.environ.get("CGKS_LIB", os.path.join(_HERE, "libcgks.so"))  # override for experiments only
 
 CGKS_OK, CGKS_ERR_CONFIG, CGKS_ERR_POSITIVITY, CGKS_ERR_NUMERICAL, CGKS_ERR_CUDA, CGKS_ERR_COMM = 0, 2, 3, 4, 5, 6
 CGKS_BC_PERIODIC, CGKS_BC_INFLOW, CGKS_BC_OUTFLOW = 0, 1, 2

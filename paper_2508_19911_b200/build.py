@@ -15,6 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+# experiment knobs (defaults are the tuned values): extra -D flags, alternate output name
+EXTRA = os.environ.get("CGKS_NVCC_DEFS", "").split()
 BUILD = os.path.join(HERE, "build")
 
 
@@ -27,7 +29,7 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
     sys.path.insert(0, HERE)
     import gen_recon
     gen_recon.emit()
@@ -38,16 +40,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs, objs = [], []
     for s in SOURCES:  # one process per translation unit, in parallel
         obj = os.path.join(BUILD, s + ".o")
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, s), "-o", obj]
+        cmd = [NVCC] + FLAGS + EXTRA + ["-c", os.path.join(CSRC, s), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     text, failed = "", False
     for cmd, p in procs:
-        out, err = p.communicate()
-        text += " ".join(cmd) + "\n" + out + err
+        so, se = p.communicate()
+        text += " ".join(cmd) + "\n" + so + se
         failed |= p.returncode != 0
     if not failed:
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart"]
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out or LIB] + objs + ["-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         text += " ".join(cmd) + "\n" + r.stdout + r.stderr
         failed = r.returncode != 0
@@ -58,9 +60,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(text)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    o = None
+    for a in sys.argv[1:]:
+        if a.startswith("--out="):
+            o = a.split("=", 1)[1]
+    print(build(force=True, verbose="-v" in sys.argv, out=o))

@@ -108,6 +108,7 @@ static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
     a.face[d] = ctx->face[d];
     a.gtab[d] = ctx->gtab[d];
     a.nface[d] = (long long)ctx->geo.fn[d][0] * ctx->geo.fn[d][1] * ctx->geo.fn[d][2];
+    for (int e = 0; e < 3; ++e) a.fn[d][e] = ctx->geo.fn[d][e];
   }
   a.ts = ctx->ts;
   a.err = ctx->err;
@@ -550,25 +551,42 @@ int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_
 
 // Algorithmic FP64 operations per launch of each kernel (counting rules in flop_count.h).
 // The flux point is counted by running the device formulation with the counting type.
+// host "exchange" for counting: the other lane's value is mirrored (counts do not depend on it)
+struct XchgMirror {
+  fc::CD operator()(const fc::CD& x) const { return x; }
+  bool flag(bool b) const { return b; }
+};
+struct ParkHost {
+  fc::CD* slots;
+  void put(int s, const fc::CD& v) const { slots[s] = v; }
+  fc::CD get(int s) const { return slots[s]; }
+};
+
+// flops of one Gauss point = both cooperating lanes
 static double flux_point_flops(const FluxConst& f, bool compact) {
   using fc::CD;
-  CD WL[5], WR[5], dWL[3][5], dWR[3][5];
-  const double wl[5] = {1.0, 0.3, -0.2, 0.1, 2.7}, wr[5] = {1.01, 0.29, -0.21, 0.12, 2.71};
+  CD W[2][5], dW[2][3][5];
+  const double w0[5] = {1.0, 0.3, -0.2, 0.1, 2.7}, w1[5] = {1.01, 0.29, -0.21, 0.12, 2.71};
   for (int i = 0; i < 5; ++i) {
-    WL[i] = CD::run(wl[i]);
-    WR[i] = CD::run(wr[i]);
+    W[0][i] = CD::run(w0[i]);
+    W[1][i] = CD::run(w1[i]);
     for (int d = 0; d < 3; ++d) {
-      dWL[d][i] = CD::run(0.01 * (i + 1) * (d + 1));
-      dWR[d][i] = CD::run(-0.02 * (i + 1) + 0.01 * d);
+      dW[0][d][i] = CD::run(0.01 * (i + 1) * (d + 1));
+      dW[1][d][i] = CD::run(-0.02 * (i + 1) + 0.01 * d);
     }
   }
-  GPOutT<CD> o;
-  fc::tally() = fc::Tally();
-  if (compact)
-    gks_flux_point<true>(WL, dWL, WR, dWR, CD::run(1e-3), f, o);
-  else
-    gks_flux_point<false>(WL, dWL, WR, dWR, CD::run(1e-3), f, o);
-  return fc::tally().flops;
+  double total = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    GPOutT<CD> o;
+    CD slots[32];
+    fc::tally() = fc::Tally();
+    if (compact)
+      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots}, o);
+    else
+      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots}, o);
+    total += fc::tally().flops;
+  }
+  return total;
 }
 
 extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names, double* flops_per_launch,
@@ -590,7 +608,7 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
       per_comp += NF * 6.0 + NF * (NF * 5.0 + 1.0 + 2.0 * D) + 8.0 + NB + 2.0 * D + 1.0;
     rows.push_back({"recon5", 5.0 * per_comp * nec});
     const int NG = D == 3 ? 4 : (D == 2 ? 2 : 1);
-    const double eval = 2.0 * 5.0 * (2.0 * NB * (1 + D) + D);
+    const double eval = 2.0 * 5.0 * (2.0 * NB * (1 + D) + D);  // both sides of one Gauss point
     const double per_face = NG * (eval + fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
     const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
     for (int a = 0; a < D; ++a) {

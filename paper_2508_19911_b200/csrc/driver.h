@@ -32,6 +32,7 @@ struct StageArgs {
   ErrState* err;
   long long ncell, necell;
   long long nface[3];
+  int fn[3][3];   // face-grid dims per normal axis
   int scheme;     // 0 GKS-2nd, 1 CGKS-5th
   int nonlinear;
   int box;

@@ -265,123 +265,188 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 }
 
 // ---------------------------------------------------------------------------
-// K2: interface flux.  One thread per (face, Gauss point); NG consecutive lanes per face.
+// K2: interface flux.  Two lanes per (face, Gauss point): lane side 0 evaluates the left
+// cell at its +1/2 face, lane side 1 the right cell at its -1/2 face; they cooperate on
+// the gas-kinetic solver through shuffles (gks_flux_side).  2*NG consecutive lanes per face.
 // Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
 // The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
 // ---------------------------------------------------------------------------
+struct XchgDev {
+  __device__ __forceinline__ double operator()(double x) const { return __shfl_xor_sync(0xffffffffu, x, 1); }
+  __device__ __forceinline__ bool flag(bool b) const { return __shfl_xor_sync(0xffffffffu, (int)b, 1) != 0; }
+};
+
+#ifndef CGKS_FLUX_MINB
+#define CGKS_FLUX_MINB 3
+#endif
+
+// flux kernel geometry: 128 threads = FPB faces along x of one (j, k) row, 2*NG lanes per face
+template <int DIM, int AX, bool COMPACT>
+struct FluxTile {
+  static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
+  static constexpr int LPF = 2 * NG;                         // lanes per face
+  static constexpr int FPB = 128 / LPF;                      // faces per block
+  static constexpr int NT = AX == 0 ? FPB + 1 : 2 * FPB;     // tile cells
+  static constexpr int NB = Sten<DIM>::NB;
+  static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
+  static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
+  static constexpr int TS = 4 * NB + 1;                      // padded per-(side, gp) table stride (no bank conflicts)
+  static constexpr int TAB = COMPACT ? 2 * NG * TS : 0;      // Gauss-point basis tables
+  static constexpr size_t smem_bytes() {
+    return sizeof(double) * ((size_t)NFLD * NT + TAB + 20 * 128);
+  }
+};
+
 template <int DIM, int AX, bool COMPACT, bool BOX>
-__global__ void __launch_bounds__(128) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
+__global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
                                                const double* __restrict__ gtab, double* __restrict__ face,
                                                const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                int stage) {
-  using S = Sten<DIM>;
-  constexpr int NG = COMPACT ? S::NG : 1;
-  constexpr int NB = S::NB;
+  using FT = FluxTile<DIM, AX, COMPACT>;
+  constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT, FPB = FT::FPB;
   constexpr int NV = COMPACT ? 20 : 5;
   constexpr int NF = COMPACT ? 30 : 10;
-  // Gauss-point basis tables of this axis: [side][gp][val, d0, d1, d2][NB]
-  __shared__ double tab[COMPACT ? 2 * NG * 4 * NB : 1];
-  if (COMPACT) {
-    for (int q = threadIdx.x; q < 2 * NG * 4 * NB; q += blockDim.x) tab[q] = gtab[q];
-    __syncthreads();
-  }
+  constexpr int NR = COMPACT ? 20 : 10;  // values each lane reduces over the Gauss points
+  extern __shared__ double smem[];
+  double* tile = smem;                            // [NFLD][NT]: reconstruction fields, then Q
+  double* tab = smem + FT::NFLD * NT;             // [side][gp][val, d0, d1, d2][NB]
+  double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
   if (err->code) return;
-  const double dt = ts->dt;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int gp = (int)(t % NG);
-  const long long f = t / NG;
-  const int fn0 = c_geo.fn[AX][0], fn1 = c_geo.fn[AX][1], fn2 = c_geo.fn[AX][2];
-  const long long nfaces = (long long)fn0 * fn1 * fn2;
-  const bool valid = f < nfaces;
-  const long long fc = valid ? f : 0;
-  const int i = (int)(fc % fn0), j = (int)((fc / fn0) % fn1), k = (int)(fc / ((long long)fn0 * fn1));
-  const int li = i - (AX == 0), lj = j - (AX == 1), lk = k - (AX == 2);
-
-  double W[2][5], dW[2][3][5];  // global frame
-  if (COMPACT) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int ci = s ? i : li, cj = s ? j : lj, ck = s ? k : lk;
-      const double* tv = tab + ((s * NG + gp) * 4) * NB;
-#pragma unroll 1
-      for (int v = 0; v < 5; ++v) {
-        double w = ld_state<BOX>(U, NV, v, ci, cj, ck);
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NB; ++q) {
-          const double a = __ldg(rec + eidx(NB * 5, q * 5 + v, ci, cj, ck));
-          w = fma(a, tv[q], w);
-          d0 = fma(a, tv[NB + q], d0);
-          if (DIM > 1) d1 = fma(a, tv[2 * NB + q], d1);
-          if (DIM > 2) d2 = fma(a, tv[3 * NB + q], d2);
+  const int fn0 = c_geo.fn[AX][0];
+  const int i0 = blockIdx.x * FPB, j = blockIdx.y, k = blockIdx.z;
+  // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous rows).
+  // Each thread serves one tile cell (index math once) and a strided subset of its fields.
+  {
+    constexpr int TPC = 128 / NT;  // threads per cell
+    const int c = threadIdx.x % NT, fsub = threadIdx.x / NT;
+    if (fsub < TPC) {
+      int ci, cj = j, ck = k;
+      if (AX == 0) {
+        ci = i0 - 1 + c;
+      } else {
+        ci = i0 + (c < FPB ? c : c - FPB);
+        if (c < FPB) {
+          if (AX == 1) cj -= 1;
+          if (AX == 2) ck -= 1;
         }
-        W[s][v] = w;
-        dW[s][0][v] = d0 * c_geo.ih[0];
-        dW[s][1][v] = d1 * c_geo.ih[1];
-        dW[s][2][v] = d2 * c_geo.ih[2];
+      }
+      const int imax = c_geo.n[0] - 1 + (c_geo.bounded[0] ? 1 : 0);  // clamp the ragged row tail
+      if (ci > imax) ci = imax;
+      const double* rb = rec + eidx(FT::NREC, 0, ci, cj, ck);
+      const long long st = c_geo.eplane;
+      for (int fld = fsub; fld < FT::NREC; fld += TPC) tile[fld * NT + c] = __ldg(rb + fld * st);
+      for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
+    }
+  }
+  if (COMPACT)
+    for (int q = threadIdx.x; q < 2 * NG * 4 * NB; q += blockDim.x) {
+      const int blk = q / (4 * NB);
+      tab[blk * FT::TS + q % (4 * NB)] = gtab[q];
+    }
+  __syncthreads();
+
+  const double dt = ts->dt;
+  const int lane = threadIdx.x;
+  const int side = lane & 1;
+  const int gp = (lane >> 1) % NG;
+  const int fl = lane / FT::LPF;  // face within the block
+  const int i = i0 + fl;
+  const bool valid = i < fn0;
+  // tile column of this lane's cell
+  const int c = AX == 0 ? fl + side : (side ? FPB + fl : fl);
+  const double* tc = tile + c;
+
+  double W[5], dW[3][5];  // global frame, this lane's side
+  if (COMPACT) {
+    // evaluation of the side's quartic at this Gauss point: basis values of the
+    // Gauss point (4 per coefficient) are read once and applied to the 5 components
+    const double* tv = tab + (side * NG + gp) * FT::TS;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      W[v] = tc[(FT::NREC + v) * NT];
+      dW[0][v] = dW[1][v] = dW[2][v] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const double b0 = tv[q], b1 = tv[NB + q];
+      const double b2 = DIM > 1 ? tv[2 * NB + q] : 0.0, b3 = DIM > 2 ? tv[3 * NB + q] : 0.0;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double a = tc[(q * 5 + v) * NT];
+        W[v] = fma(a, b0, W[v]);
+        dW[0][v] = fma(a, b1, dW[0][v]);
+        if (DIM > 1) dW[1][v] = fma(a, b2, dW[1][v]);
+        if (DIM > 2) dW[2][v] = fma(a, b3, dW[2][v]);
       }
     }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      dW[0][v] *= c_geo.ih[0];
+      dW[1][v] *= c_geo.ih[1];
+      dW[2][v] *= c_geo.ih[2];
+    }
   } else {
+    const double hs = side ? -0.5 : 0.5;
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int ci = s ? i : li, cj = s ? j : lj, ck = s ? k : lk;
-      const double side = s ? -0.5 : 0.5;
+    for (int v = 0; v < 5; ++v) {
+      const double q = tc[(FT::NREC + v) * NT];
+      W[v] = q + hs * tc[(AX * 5 + v) * NT];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        const double q = ld_state<BOX>(U, NV, v, ci, cj, ck);
-        const double sa = __ldg(rec + eidx(15, AX * 5 + v, ci, cj, ck));
-        W[s][v] = q + side * sa;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) dW[s][a][v] = __ldg(rec + eidx(15, a * 5 + v, ci, cj, ck)) * c_geo.ih[a];
-      }
+      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * NT] * c_geo.ih[a];
     }
   }
   // rotate into the normal frame (cyclic permutation: normal first), bit-exact
   constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
-  double wl[5], wr[5], dl[3][5], dr[3][5];
-  wl[0] = W[0][0]; wl[1] = W[0][1 + P0]; wl[2] = W[0][1 + P1]; wl[3] = W[0][1 + P2]; wl[4] = W[0][4];
-  wr[0] = W[1][0]; wr[1] = W[1][1 + P0]; wr[2] = W[1][1 + P1]; wr[3] = W[1][1 + P2]; wr[4] = W[1][4];
   const int pp[3] = {P0, P1, P2};
+  double wn[5], dn[3][5];
+  wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    dl[d][0] = dW[0][pp[d]][0];
-    dl[d][1] = dW[0][pp[d]][1 + P0];
-    dl[d][2] = dW[0][pp[d]][1 + P1];
-    dl[d][3] = dW[0][pp[d]][1 + P2];
-    dl[d][4] = dW[0][pp[d]][4];
-    dr[d][0] = dW[1][pp[d]][0];
-    dr[d][1] = dW[1][pp[d]][1 + P0];
-    dr[d][2] = dW[1][pp[d]][1 + P1];
-    dr[d][3] = dW[1][pp[d]][1 + P2];
-    dr[d][4] = dW[1][pp[d]][4];
+    dn[d][0] = dW[pp[d]][0];
+    dn[d][1] = dW[pp[d]][1 + P0];
+    dn[d][2] = dW[pp[d]][1 + P1];
+    dn[d][3] = dW[pp[d]][1 + P2];
+    dn[d][4] = dW[pp[d]][4];
   }
   GPOut o;
-  bool ok = gks_flux_point<COMPACT>(wl, dl, wr, dr, dt, c_fc, o);
-  if (valid && !ok) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
-  // back to the global frame, weight 1/NG, sum over the NG lanes of this face
-  double out[NF];
+  const bool ok = gks_flux_side<COMPACT>(side, wn, dn, dt, c_fc, XchgDev(), ParkDev{scratch + lane}, o);
+  if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
+  // back to the global frame, weight 1/NG; side 0: Fn Ft (QLn QLt), side 1: QRn QRt
+  double out[NR];
   const double wgt = 1.0 / NG;
-  const double* src[6] = {o.Fn, o.Ft, o.QLn, o.QLt, o.QRn, o.QRt};
 #pragma unroll
-  for (int s = 0; s < NF / 5; ++s) {
-    out[s * 5 + 0] = wgt * src[s][0];
-    out[s * 5 + 1 + P0] = wgt * src[s][1];
-    out[s * 5 + 1 + P1] = wgt * src[s][2];
-    out[s * 5 + 1 + P2] = wgt * src[s][3];
-    out[s * 5 + 4] = wgt * src[s][4];
+  for (int s = 0; s < NR / 5; ++s) {
+    double x[5];
+#pragma unroll
+    for (int cc = 0; cc < 5; ++cc) {
+      const double a0 = s == 0 ? o.Fn[cc] : (s == 1 ? o.Ft[cc] : (s == 2 ? o.QLn[cc] : o.QLt[cc]));
+      const double a1 = (s % 2 == 0) ? o.QLn[cc] : o.QLt[cc];
+      x[cc] = side == 0 ? a0 : a1;
+    }
+    out[s * 5 + 0] = wgt * x[0];
+    out[s * 5 + 1 + P0] = wgt * x[1];
+    out[s * 5 + 1 + P1] = wgt * x[2];
+    out[s * 5 + 1 + P2] = wgt * x[3];
+    out[s * 5 + 4] = wgt * x[4];
   }
   if (NG > 1) {
 #pragma unroll
-    for (int q = 0; q < NF; ++q) {
+    for (int q = 0; q < NR; ++q) {
 #pragma unroll
-      for (int m = 1; m < NG; m <<= 1) out[q] += __shfl_xor_sync(0xffffffffu, out[q], m);
+      for (int m = 2; m < 2 * NG; m <<= 1) out[q] += __shfl_xor_sync(0xffffffffu, out[q], m);
     }
   }
   if (valid && gp == 0) {
+    const int fn1 = c_geo.fn[AX][1];
     const long long fpl = (long long)fn0 * fn1;
     const long long base = (long long)k * NF * fpl + (long long)j * fn0 + i;
+    if (side == 0) {
 #pragma unroll
-    for (int q = 0; q < NF; ++q) face[base + q * fpl] = out[q];
+      for (int q = 0; q < NR; ++q) face[base + q * fpl] = out[q];
+    } else if (COMPACT) {
+#pragma unroll
+      for (int q = 0; q < 10; ++q) face[base + (20 + q) * fpl] = out[q];
+    }
   }
 }
 

@@ -43,6 +43,37 @@ int launch(LaunchEnv& env, const char* name, void (*kern)(KArgs...), long long n
 
 constexpr int D = CGKS_DIM;
 
+// flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
+template <bool COMPACT, bool BOX, int AX>
+int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
+  using FT = FluxTile<D, AX, COMPACT>;
+  auto kern = k_flux<D, AX, COMPACT, BOX>;
+  static bool attr = false;
+  const size_t smem = FT::smem_bytes();
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
+    attr = true;
+  }
+  const dim3 grid((unsigned)((a.fn[AX][0] + FT::FPB - 1) / FT::FPB), (unsigned)a.fn[AX][1], (unsigned)a.fn[AX][2]);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (env.prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, env.stream);
+  }
+  kern<<<grid, 128, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
+    return 5;
+  }
+  if (env.prof) {
+    cudaEventRecord(e1, env.stream);
+    env.pending->push_back({name, {e0, e1}});
+  }
+  return 0;
+}
+
 template <bool COMPACT, bool NONLIN, bool BOX>
 int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   if (COMPACT) {
@@ -50,15 +81,12 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   } else {
     LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
-  constexpr int NG = COMPACT ? Sten<D>::NG : 1;
-  LAUNCH("flux_x", (k_flux<D, 0, COMPACT, BOX>), a.nface[0] * NG, 128, a.Uin, a.rec, a.gtab[0], a.face[0], a.ts,
-         a.err, stage);
-  if (D > 1)
-    LAUNCH("flux_y", (k_flux<D, (D > 1 ? 1 : 0), COMPACT, BOX>), a.nface[1] * NG, 128, a.Uin, a.rec, a.gtab[1],
-           a.face[1], a.ts, a.err, stage);
-  if (D > 2)
-    LAUNCH("flux_z", (k_flux<D, (D > 2 ? 2 : 0), COMPACT, BOX>), a.nface[2] * NG, 128, a.Uin, a.rec, a.gtab[2],
-           a.face[2], a.ts, a.err, stage);
+  {
+    int rc = flux_launch<COMPACT, BOX, 0>(env, "flux_x", a, stage);
+    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0)>(env, "flux_y", a, stage);
+    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0)>(env, "flux_z", a, stage);
+    if (rc) return rc;
+  }
   if (mode == 0)
     LAUNCH("update", (k_update<D, COMPACT, 0>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
            a.carry, a.ts, a.err);
