@@ -328,32 +328,36 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
     return fail(CGKS_ERR_CUDA);
   }
-  // Gauss-point basis tables per axis: [side][gp][val,d0,d1,d2][nb]
+  // face evaluation tables per axis: [side][quantity][nb] (quantity 0 value, 1 d/dn, 2 d/dtA, 3 d/dtB);
+  // entry = (+-1/2)^{d_n} s^{d_tA + d_tB} / d! with one exponent lowered for derivatives, minus the
+  // own-cell average of delta^d/d! for the value; the Gauss-point signs are applied in the kernel.
   if (ctx->scheme_id == CGKS_CGKS5) {
-    const int nb = ctx->cls.nb;
-    const double s = 0.5 / std::sqrt(3.0);  // 2-point Gauss-Legendre on [-1/2, 1/2] (R27)
+    const int nb = ctx->cls.nb, nq = dim + 1;
+    const double sg = 0.5 / std::sqrt(3.0);  // 2-point Gauss-Legendre on [-1/2, 1/2] (R27)
+    auto f = [](double x, int n) {
+      double r = 1.0;
+      for (int i = 1; i <= n; ++i) r *= x / i;
+      return r;
+    };
     for (int a = 0; a < dim; ++a) {
-      int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
-      int n1 = t1 < dim ? 2 : 1, n2 = t2 < dim ? 2 : 1;
-      int ng = n1 * n2;
-      std::vector<double> tab(2 * ng * 4 * nb, 0.0), val(nb), der(3 * nb);
-      for (int side = 0; side < 2; ++side)
-        for (int p = 0; p < n1; ++p)
-          for (int q = 0; q < n2; ++q) {
-            double x[3] = {0, 0, 0};
-            x[a] = side == 0 ? 0.5 : -0.5;
-            if (t1 < dim) x[t1] = p ? s : -s;
-            if (t2 < dim) x[t2] = q ? s : -s;
-            basis_at(ctx->cls, x, val.data(), der.data());
-            int gp = p * n2 + q;
-            double* dst = tab.data() + ((side * ng + gp) * 4) * nb;
-            for (int k = 0; k < nb; ++k) {
-              dst[k] = val[k];
-              dst[nb + k] = der[k];
-              dst[2 * nb + k] = der[nb + k];
-              dst[3 * nb + k] = der[2 * nb + k];
+      const int tA = dim == 3 ? (a + 1) % 3 : (dim == 2 ? 1 - a : -1);
+      const int tB = dim == 3 ? (a + 2) % 3 : -1;
+      std::vector<double> tab((size_t)2 * nq * nb, 0.0);
+      for (int side = 0; side < 2; ++side) {
+        const double dn = side == 0 ? 0.5 : -0.5;
+        for (int q = 0; q < nq; ++q)
+          for (int kk = 0; kk < nb; ++kk) {
+            int e[3] = {ctx->cls.expo[kk][0], ctx->cls.expo[kk][1], ctx->cls.expo[kk][2]};
+            int low = q == 1 ? a : (q == 2 ? tA : (q == 3 ? tB : -1));
+            double val = 0.0;
+            if (low < 0 || e[low] > 0) {
+              if (low >= 0) e[low] -= 1;
+              val = f(dn, e[a]) * (tA >= 0 ? f(sg, e[tA]) : 1.0) * (tB >= 0 ? f(sg, e[tB]) : 1.0);
+              if (q == 0) val -= ctx->cls.avg0[kk];
             }
+            tab[((size_t)side * nq + q) * nb + kk] = val;
           }
+      }
       if (!alloc(&ctx->gtab[a], (long long)tab.size()) ||
           cudaMemcpy(ctx->gtab[a], tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         set_msg(ctx, "table upload failed");
@@ -608,8 +612,10 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
       per_comp += NF * 6.0 + NF * (NF * 5.0 + 1.0 + 2.0 * D) + 8.0 + NB + 2.0 * D + 1.0;
     rows.push_back({"recon5", 5.0 * per_comp * nec});
     const int NG = D == 3 ? 4 : (D == 2 ? 2 : 1);
-    const double eval = 2.0 * 5.0 * (2.0 * NB * (1 + D) + D);  // both sides of one Gauss point
-    const double per_face = NG * (eval + fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
+    // face-plane parity evaluation: per face side and quantity one pass over the coefficients
+    // (2 flops per coefficient and component) plus the sign combinations at the NG points
+    const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * (2.0 * (NG - 1) + 1.0)) + 2.0 * 5.0 * D * NG;
+    const double per_face = eval_face + NG * (fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
     const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
     for (int a = 0; a < D; ++a) {
       double nf = (double)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];

@@ -112,6 +112,13 @@ __device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
   return ((long long)kk * NF + f) * c_geo.eplane + (long long)jj * c_geo.en[0] + ii;
 }
 
+// 8-byte asynchronous global -> shared copy (cp.async.ca, LDGSTS) and the matching wait
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
                                            int j, int k) {
   if (atomicCAS(&err->code, 0, code) == 0) {
@@ -290,8 +297,9 @@ struct FluxTile {
   static constexpr int NB = Sten<DIM>::NB;
   static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
   static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
-  static constexpr int TS = 4 * NB + 1;                      // padded per-(side, gp) table stride (no bank conflicts)
-  static constexpr int TAB = COMPACT ? 2 * NG * TS : 0;      // Gauss-point basis tables
+  static constexpr int NQ = DIM + 1;                         // value + DIM derivatives
+  static constexpr int TS = NB + 1;                          // padded per-(side, quantity) row (no bank conflicts)
+  static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
   static constexpr size_t smem_bytes() {
     return sizeof(double) * ((size_t)NFLD * NT + TAB + 20 * 128);
   }
@@ -334,15 +342,19 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       if (ci > imax) ci = imax;
       const double* rb = rec + eidx(FT::NREC, 0, ci, cj, ck);
       const long long st = c_geo.eplane;
-      for (int fld = fsub; fld < FT::NREC; fld += TPC) tile[fld * NT + c] = __ldg(rb + fld * st);
-      for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
+      // asynchronous global -> shared copies (LDGSTS): all in flight at once
+      for (int fld = fsub; fld < FT::NREC; fld += TPC) cp_async8(tile + fld * NT + c, rb + fld * st);
+      if (BOX) {
+        for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
+      } else {
+        const double* ub = U + sidx(NV, 0, wrapi(ci, c_geo.n[0]), wrapi(cj, c_geo.n[1]), wrapi(ck, c_geo.n[2]));
+        for (int v = fsub; v < 5; v += TPC) cp_async8(tile + (FT::NREC + v) * NT + c, ub + v * c_geo.plane);
+      }
     }
+    cp_async_wait_all();
   }
   if (COMPACT)
-    for (int q = threadIdx.x; q < 2 * NG * 4 * NB; q += blockDim.x) {
-      const int blk = q / (4 * NB);
-      tab[blk * FT::TS + q % (4 * NB)] = gtab[q];
-    }
+    for (int q = threadIdx.x; q < 2 * FT::NQ * NB; q += blockDim.x) tab[(q / NB) * FT::TS + q % NB] = gtab[q];
   __syncthreads();
 
   const double dt = ts->dt;
@@ -356,36 +368,80 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const int c = AX == 0 ? fl + side : (side ? FPB + fl : fl);
   const double* tc = tile + c;
 
-  double W[5], dW[3][5];  // global frame, this lane's side
+  // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)
+  constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
+  double wn[5], dn[3][5];
   if (COMPACT) {
-    // evaluation of the side's quartic at this Gauss point: basis values of the
-    // Gauss point (4 per coefficient) are read once and applied to the 5 components
-    const double* tv = tab + (side * NG + gp) * FT::TS;
+    // Evaluation of the side's quartic at the face Gauss points in the face-plane
+    // parity form: with the normal coordinate fixed, p_d at (+-s, +-s) is a sign character of
+    // the transverse exponents times a constant, so one pass over the coefficients gives the
+    // value or one derivative at all NG Gauss points.  Lane gp computes quantity q = gp
+    // (0 value, 1 d/dn, 2 d/dtA, 3 d/dtB) and scatters the NG results through shared memory.
+    constexpr int NQ = FT::NQ;
+    constexpr int TA = DIM == 3 ? P1 : (DIM == 2 ? 1 - AX : 0);  // active transverse axes
+    constexpr int TB = DIM == 3 ? P2 : 0;
+    const double* Tb = tab + side * NQ * FT::TS;
+    double* xs = scratch;  // exchange slots [q*5 + v][128]
+    for (int q = gp; q < NQ; q += NG) {
+      const double* T = Tb + q * FT::TS;
+      double S[5][NG];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      W[v] = tc[(FT::NREC + v) * NT];
-      dW[0][v] = dW[1][v] = dW[2][v] = 0.0;
-    }
+      for (int v = 0; v < 5; ++v)
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const double b0 = tv[q], b1 = tv[NB + q];
-      const double b2 = DIM > 1 ? tv[2 * NB + q] : 0.0, b3 = DIM > 2 ? tv[3 * NB + q] : 0.0;
+        for (int cc = 0; cc < NG; ++cc) S[v][cc] = 0.0;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        const double a = tc[(q * 5 + v) * NT];
-        W[v] = fma(a, b0, W[v]);
-        dW[0][v] = fma(a, b1, dW[0][v]);
-        if (DIM > 1) dW[1][v] = fma(a, b2, dW[1][v]);
-        if (DIM > 2) dW[2][v] = fma(a, b3, dW[2][v]);
+      for (int kk = 0; kk < NB; ++kk) {
+        const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
+                                 : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
+        const double t = T[kk];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * NT], t, S[v][cls]);
+      }
+      const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);  // derivative along tA / tB flips that parity
+#pragma unroll
+      for (int g2 = 0; g2 < NG; ++g2) {
+        const double sA = (g2 & 1) ? 1.0 : -1.0, sB = (g2 & 2) ? 1.0 : -1.0;
+        const double chi = ((flip & 1) ? sA : 1.0) * ((flip & 2) ? sB : 1.0);
+        double* dst = xs + (lane - 2 * gp + 2 * g2);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          double val = S[v][0];
+          if (NG > 1) val = fma(sA, S[v][1], val);
+          if (NG > 2) val = fma(sB, S[v][2], fma(sA * sB, S[v][3], val));
+          dst[(q * 5 + v) * 128] = chi * val;
+        }
       }
     }
+    __syncwarp();
+    double W[5], dW[NQ][5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      dW[0][v] *= c_geo.ih[0];
-      dW[1][v] *= c_geo.ih[1];
-      dW[2][v] *= c_geo.ih[2];
+      W[v] = tc[(FT::NREC + v) * NT] + xs[v * 128 + lane];
+#pragma unroll
+      for (int q = 1; q < NQ; ++q) dW[q][v] = xs[(q * 5 + v) * 128 + lane];
+    }
+    __syncwarp();  // the exchange slots are reused as parking slots by gks_flux_side
+    // physical derivatives along AX, TA, TB, placed in the normal-frame slots
+    double g[3][5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      g[0][v] = g[1][v] = g[2][v] = 0.0;
+      g[AX][v] = dW[1][v] * c_geo.ih[AX];
+      if (DIM > 1) g[TA][v] = dW[2 % NQ][v] * c_geo.ih[TA];
+      if (DIM > 2) g[TB][v] = dW[3 % NQ][v] * c_geo.ih[TB];
+    }
+    wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
+    const int pp[3] = {P0, P1, P2};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      dn[d][0] = g[pp[d]][0];
+      dn[d][1] = g[pp[d]][1 + P0];
+      dn[d][2] = g[pp[d]][1 + P1];
+      dn[d][3] = g[pp[d]][1 + P2];
+      dn[d][4] = g[pp[d]][4];
     }
   } else {
+    double W[5], dW[3][5];
     const double hs = side ? -0.5 : 0.5;
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
@@ -394,19 +450,16 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
 #pragma unroll
       for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * NT] * c_geo.ih[a];
     }
-  }
-  // rotate into the normal frame (cyclic permutation: normal first), bit-exact
-  constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
-  const int pp[3] = {P0, P1, P2};
-  double wn[5], dn[3][5];
-  wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
+    wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
+    const int pp[3] = {P0, P1, P2};
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    dn[d][0] = dW[pp[d]][0];
-    dn[d][1] = dW[pp[d]][1 + P0];
-    dn[d][2] = dW[pp[d]][1 + P1];
-    dn[d][3] = dW[pp[d]][1 + P2];
-    dn[d][4] = dW[pp[d]][4];
+    for (int d = 0; d < 3; ++d) {
+      dn[d][0] = dW[pp[d]][0];
+      dn[d][1] = dW[pp[d]][1 + P0];
+      dn[d][2] = dW[pp[d]][1 + P1];
+      dn[d][3] = dW[pp[d]][1 + P2];
+      dn[d][4] = dW[pp[d]][4];
+    }
   }
   GPOut o;
   const bool ok = gks_flux_side<COMPACT>(side, wn, dn, dt, c_fc, XchgDev(), ParkDev{scratch + lane}, o);

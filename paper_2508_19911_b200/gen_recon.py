@@ -163,6 +163,12 @@ def emit():
         lines.append(f"// dim {dim}: {n} data, {nb} coefficients, {len(pairs)} FMA per component")
         lines.append(f"template <> struct ReconGen<{dim}> {{")
         lines.append(f"  static constexpr int ND = {n}, NB = {nb}, NNZ = {len(pairs)};")
+        ex = ",".join("{%d,%d,%d}" % b for b in B)
+        lines.append("  // basis exponents d of p_d (Eq. base), in coefficient order")
+        lines.append("  __host__ __device__ static constexpr int expo(int k, int a) {")
+        lines.append(f"    constexpr int E[{nb}][3] = {{{ex}}};")
+        lines.append("    return E[k][a];")
+        lines.append("  }")
         lines.append("  // raw item i -> combination coefficients; combination c: class and raw items")
         lines.append("  // L.q(ox,oy,oz): neighbour average minus own average; L.g(a,ox,oy,oz): h_a dQ/dx_a of the neighbour")
         lines.append("  template <typename Load>")
