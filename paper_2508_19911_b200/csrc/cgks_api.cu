@@ -109,6 +109,7 @@ static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
     a.gtab[d] = ctx->gtab[d];
     a.nface[d] = (long long)ctx->geo.fn[d][0] * ctx->geo.fn[d][1] * ctx->geo.fn[d][2];
     for (int e = 0; e < 3; ++e) a.fn[d][e] = ctx->geo.fn[d][e];
+    a.en[d] = ctx->geo.en[d];
   }
   a.ts = ctx->ts;
   a.err = ctx->err;

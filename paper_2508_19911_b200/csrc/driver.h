@@ -33,6 +33,7 @@ struct StageArgs {
   long long ncell, necell;
   long long nface[3];
   int fn[3][3];   // face-grid dims per normal axis
+  int en[3];      // extended (reconstruction) range per axis
   int scheme;     // 0 GKS-2nd, 1 CGKS-5th
   int nonlinear;
   int box;

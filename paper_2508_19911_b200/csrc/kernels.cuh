@@ -134,36 +134,86 @@ __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, 
 // ---------------------------------------------------------------------------
 // K1: CGKS-5th reconstruction (coefficients of P^4 on the reference cell, GENO folded)
 // ---------------------------------------------------------------------------
-template <bool BOX>
-struct Recon5Loader {
-  const double* __restrict__ U;
-  int v, i, j, k;
+// Block tile of the reconstruction: TX x TY x TZ cells, stencil data of one component
+// (Q_v and the three gradient components) staged with a one-cell halo in shared memory by
+// cp.async, double-buffered over the five components.
+template <int DIM>
+struct ReconTile {
+  static constexpr int TX = 32;
+  static constexpr int TY = DIM == 3 ? 4 : (DIM == 2 ? 8 : 1);
+  static constexpr int TZ = DIM == 3 ? 2 : 1;
+  static constexpr int NTH = TX * TY * TZ;
+  static constexpr int HX = TX + 2, HY = DIM >= 2 ? TY + 2 : 1, HZ = DIM == 3 ? TZ + 2 : 1;
+  static constexpr int HALO = HX * HY * HZ;
+  static constexpr int NFS = 1 + DIM;  // staged fields per component: Q_v, dQ_v/dx_a
+  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO; }
+};
+
+template <int DIM>
+struct Recon5TileLoader {
+  const double* __restrict__ s;  // staged fields of this component, at this thread's cell
   double q0, h0, h1, h2;
-  __device__ __forceinline__ double q(int ox, int oy, int oz) const {
-    return ld_state<BOX>(U, 20, v, i + ox, j + oy, k + oz) - q0;
+  static constexpr int HALO = ReconTile<DIM>::HALO;
+  static constexpr int SY = ReconTile<DIM>::HX, SZ = ReconTile<DIM>::HX * ReconTile<DIM>::HY;
+  __device__ __forceinline__ double at(int f, int ox, int oy, int oz) const {
+    return s[f * HALO + oz * SZ + oy * SY + ox];
   }
+  __device__ __forceinline__ double q(int ox, int oy, int oz) const { return at(0, ox, oy, oz) - q0; }
   __device__ __forceinline__ double g(int a, int ox, int oy, int oz) const {
-    return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * ld_state<BOX>(U, 20, 5 + a * 5 + v, i + ox, j + oy, k + oz);
+    return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * at(1 + a, ox, oy, oz);
   }
 };
 
-template <int DIM, bool NONLIN, bool BOX>
-__global__ void __launch_bounds__(128) k_recon5(const double* __restrict__ U, double* __restrict__ coef,
-                                                 const ErrState* __restrict__ err) {
-  using S = Sten<DIM>;
-  constexpr int NCO = S::NB * 5;
-  if (err->code) return;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long ntot = (long long)c_geo.en[0] * c_geo.en[1] * c_geo.en[2];
-  if (t >= ntot) return;
-  const int i = (int)(t % c_geo.en[0]) + c_geo.elo[0];
-  const int j = (int)((t / c_geo.en[0]) % c_geo.en[1]) + c_geo.elo[1];
-  const int k = (int)(t / ((long long)c_geo.en[0] * c_geo.en[1])) + c_geo.elo[2];
+// stage fields (Q_v, G_{a,v}) of the block's halo tile into buf
+template <int DIM, bool BOX>
+__device__ __forceinline__ void recon_stage(const double* __restrict__ U, double* buf, int v, int x0, int y0,
+                                            int z0) {
+  using RT = ReconTile<DIM>;
+  for (int idx = threadIdx.x; idx < RT::NFS * RT::HALO; idx += RT::NTH) {
+    const int f = idx / RT::HALO, h = idx % RT::HALO;
+    const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
+    const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
+    const int fld = f == 0 ? v : 5 + (f - 1) * 5 + v;
+    if (BOX) {
+      buf[idx] = ld_state<true>(U, 20, fld, i, j, kk);
+    } else {
+      cp_async8(buf + idx, U + sidx(20, fld, wrapi(i, c_geo.n[0]), wrapi(j, c_geo.n[1]), wrapi(kk, c_geo.n[2])));
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
 
+template <int DIM, bool NONLIN, bool BOX>
+__global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double* __restrict__ U,
+                                                                    double* __restrict__ coef,
+                                                                    const ErrState* __restrict__ err) {
+  using S = Sten<DIM>;
+  using RT = ReconTile<DIM>;
+  constexpr int NCO = S::NB * 5;
+  extern __shared__ double rsm[];
+  if (err->code) return;
+  const int tx = threadIdx.x % RT::TX, ty = (threadIdx.x / RT::TX) % RT::TY, tz = threadIdx.x / (RT::TX * RT::TY);
+  // block origin in the extended (reconstruction) index range
+  const int x0 = blockIdx.x * RT::TX + c_geo.elo[0];
+  const int y0 = blockIdx.y * RT::TY + c_geo.elo[1];
+  const int z0 = blockIdx.z * RT::TZ + c_geo.elo[2];
+  const int i = x0 + tx, j = y0 + ty, k = z0 + tz;
+  const bool valid = (i < c_geo.elo[0] + c_geo.en[0]) && (j < c_geo.elo[1] + c_geo.en[1]) &&
+                     (k < c_geo.elo[2] + c_geo.en[2]);
+  const int own = (DIM == 3 ? (tz + 1) * RT::HX * RT::HY : 0) + (DIM >= 2 ? (ty + 1) * RT::HX : 0) + tx + 1;
+  recon_stage<DIM, BOX>(U, rsm, 0, x0, y0, z0);
 #pragma unroll 1
   for (int v = 0; v < 5; ++v) {
-    Recon5Loader<BOX> L{U, v, i, j, k, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
-    L.q0 = ld_state<BOX>(U, 20, v, i, j, k);
+    double* cur = rsm + (v & 1) * RT::NFS * RT::HALO;
+    if (v < 4) {
+      recon_stage<DIM, BOX>(U, rsm + ((v + 1) & 1) * RT::NFS * RT::HALO, v + 1, x0, y0, z0);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    Recon5TileLoader<DIM> L{cur + own, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
+    L.q0 = L.at(0, 0, 0, 0);
     double acc[S::NB];
 #pragma unroll
     for (int q = 0; q < S::NB; ++q) acc[q] = 0.0;
@@ -216,8 +266,11 @@ __global__ void __launch_bounds__(128) k_recon5(const double* __restrict__ U, do
 #pragma unroll
       for (int a = 0; a < DIM; ++a) acc[a] = fma(1.0 - chi, lin[a], acc[a]);
     }
+    if (valid) {
 #pragma unroll
-    for (int q = 0; q < S::NB; ++q) coef[eidx(NCO, q * 5 + v, i, j, k)] = acc[q];
+      for (int q = 0; q < S::NB; ++q) coef[eidx(NCO, q * 5 + v, i, j, k)] = acc[q];
+    }
+    __syncthreads();  // this buffer is refilled by the prefetch two components ahead
   }
 }
 

@@ -43,6 +43,38 @@ int launch(LaunchEnv& env, const char* name, void (*kern)(KArgs...), long long n
 
 constexpr int D = CGKS_DIM;
 
+// reconstruction: one block per TX x TY x TZ cells of the extended range, shared-memory halo tile
+template <bool NONLIN, bool BOX>
+int recon5_launch(LaunchEnv& env, const StageArgs& a) {
+  using RT = ReconTile<D>;
+  auto kern = k_recon5<D, NONLIN, BOX>;
+  static bool attr = false;
+  const size_t smem = RT::smem_bytes();
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
+    attr = true;
+  }
+  const dim3 grid((unsigned)((a.en[0] + RT::TX - 1) / RT::TX), (unsigned)((a.en[1] + RT::TY - 1) / RT::TY),
+                  (unsigned)((a.en[2] + RT::TZ - 1) / RT::TZ));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (env.prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, env.stream);
+  }
+  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (env.msg) std::snprintf(env.msg, env.msglen, "launch of recon5 failed: %s", cudaGetErrorString(e));
+    return 5;
+  }
+  if (env.prof) {
+    cudaEventRecord(e1, env.stream);
+    env.pending->push_back({"recon5", {e0, e1}});
+  }
+  return 0;
+}
+
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
 template <bool COMPACT, bool BOX, int AX>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
@@ -77,7 +109,8 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
 template <bool COMPACT, bool NONLIN, bool BOX>
 int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   if (COMPACT) {
-    LAUNCH("recon5", (k_recon5<D, NONLIN, BOX>), a.necell, 128, a.Uin, a.rec, a.err);
+    int rc = recon5_launch<NONLIN, BOX>(env, a);
+    if (rc) return rc;
   } else {
     LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
