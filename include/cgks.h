@@ -94,6 +94,28 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
 /* Offset and size of this rank's block in the global grid. */
 int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]);
 
+/* Pure host function (no CUDA): the z-slab decomposition used by cgks_create.  For a global
+ * grid n and nproc = (1,1,P), rank r owns planes [off[2], off[2] + nloc[2]) with
+ * nloc[2] = n[2]/P; nbr = (lower, upper) neighbour ranks (periodic in z).  Returns
+ * CGKS_ERR_CONFIG for unsupported layouts (nproc[0|1] > 1, P not dividing n[2], bad rank). */
+int cgks_decompose(const int64_t n[3], const int nproc[3], int rank, int64_t off[3], int64_t nloc[3], int nbr[2]);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (rank 0 creates it and broadcasts it to
+ * the other ranks, e.g. with torch.distributed, before cgks_create).  Loads libnccl.so.2 at
+ * run time (CGKS_NCCL_LIB overrides the name).  CGKS_ERR_COMM if NCCL is unavailable. */
+int cgks_nccl_unique_id(void* out128);
+
+/* Multi-rank contexts (grid.nproc = (1,1,P), P > 1):
+ *   - with grid.nccl_id set, each process owns one rank; cgks_step exchanges a 2-plane halo
+ *     of all fields with the z neighbours (ncclSend/ncclRecv, one group per stage) and
+ *     reduces dt with ncclAllReduce(min);
+ *   - with grid.nccl_id == NULL the P contexts of one process (same device) form an
+ *     in-process decomposition advanced in lock-step by cgks_step_group (halo copies,
+ *     shared time state); cgks_step refuses such contexts.
+ * ctxs[r] must be rank r (0..n-1) of the same decomposition.  Results equal the undecomposed
+ * run bit for bit (same per-cell arithmetic, same global dt). */
+int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps);
+
 /* Set the state (user layout, rank-local block).  gradQ may be NULL (zero gradients;
  * not recommended for CGKS-5th, R26; ignored by GKS-2nd).  Resets t and the step count. */
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);

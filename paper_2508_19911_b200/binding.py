@@ -58,7 +58,8 @@ _lib = None
 
 EXPORTS = ["cgks_scheme_defaults", "cgks_create", "cgks_local_extent", "cgks_set_state", "cgks_step",
            "cgks_get_state", "cgks_get_time", "cgks_last_error", "cgks_launches_per_step", "cgks_profile",
-           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_destroy"]
+           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group",
+           "cgks_destroy"]
 
 
 def load(path: str = LIB_PATH):
@@ -86,6 +87,11 @@ def load(path: str = LIB_PATH):
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]
     L.cgks_algorithmic_flops.argtypes = [vp, ctypes.c_int, ctypes.c_char_p, dp, dp, ctypes.POINTER(ctypes.c_int)]
     L.cgks_fp64_peak.argtypes = [dp, dp]
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    L.cgks_decompose.argtypes = [i64p, ctypes.POINTER(ctypes.c_int), ctypes.c_int, i64p, i64p,
+                                 ctypes.POINTER(ctypes.c_int)]
+    L.cgks_nccl_unique_id.argtypes = [ctypes.c_void_p]
+    L.cgks_step_group.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int]
     L.cgks_destroy.argtypes = [vp]
     L.cgks_destroy.restype = None
     _lib = L
@@ -100,6 +106,35 @@ def fp64_peak():
     if rc:
         raise CgksError(rc, "fp64 probe failed")
     return t.value, m.value
+
+
+def decompose(n, nproc, rank):
+    """Host-only z-slab decomposition of the library: (offset, local size, (lower, upper) neighbours)."""
+    nn = (ctypes.c_int64 * 3)(*[int(x) for x in n])
+    npr = (ctypes.c_int * 3)(*[int(x) for x in nproc])
+    off = (ctypes.c_int64 * 3)()
+    nl = (ctypes.c_int64 * 3)()
+    nb = (ctypes.c_int * 2)()
+    rc = load().cgks_decompose(nn, npr, int(rank), off, nl, nb)
+    if rc:
+        raise CgksError(rc, "unsupported decomposition")
+    return tuple(off), tuple(nl), (nb[0], nb[1])
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load().cgks_nccl_unique_id(buf)
+    if rc:
+        raise CgksError(rc, "cannot create an ncclUniqueId (libnccl.so.2 not loadable)")
+    return buf.raw
+
+
+def step_group(solvers, nsteps):
+    """Advance the in-process slab contexts (ranks 0..n-1, nccl_id=None) in lock-step."""
+    arr = (ctypes.c_void_p * len(solvers))(*[s.ctx.value for s in solvers])
+    rc = load().cgks_step_group(arr, len(solvers), int(nsteps))
+    if rc:
+        raise CgksError(rc, solvers[0].last_error())
 
 
 def scheme_defaults(scheme_id: int) -> cgks_scheme:
@@ -142,7 +177,8 @@ class Solver:
                         g.bc_state[a][s][v] = float(np.asarray(bc_state)[a, s, v])
         g.rank = int(rank)
         self._nccl_id = nccl_id
-        g.nccl_id = None if nccl_id is None else ctypes.cast(ctypes.c_char_p(bytes(nccl_id)), ctypes.c_void_p)
+        self._nccl_buf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        g.nccl_id = None if nccl_id is None else ctypes.cast(self._nccl_buf, ctypes.c_void_p)
         g.stream = None if stream is None else ctypes.c_void_p(int(stream))
         sc = scheme_defaults(scheme)
         sc.nonlinear = int(nonlinear)

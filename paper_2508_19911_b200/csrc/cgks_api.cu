@@ -11,6 +11,7 @@
 #include <vector>
 
 #include <algorithm>
+#include <dlfcn.h>
 
 #include "../../include/cgks.h"
 #include "cls_build.h"
@@ -26,8 +27,62 @@ struct ReconGen;
 
 using namespace cgks;
 
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (only multi-rank contexts need it).  Types mirror nccl.h.
+// ---------------------------------------------------------------------------
+namespace nccl {
+typedef struct ncclComm* Comm;
+typedef struct {
+  char internal[128];
+} UniqueId;
+enum { Uint64 = 5, Float64 = 8 };
+enum { Min = 3 };
+struct Api {
+  void* h = nullptr;
+  int (*GetUniqueId)(UniqueId*) = nullptr;
+  int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  int (*CommDestroy)(Comm) = nullptr;
+  int (*Send)(const void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+static Api g_api;
+static bool load() {
+  if (g_api.h) return true;
+  const char* env = std::getenv("CGKS_NCCL_LIB");
+  const char* cands[] = {env, "libnccl.so.2", "libnccl.so"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    g_api.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (g_api.h) break;
+  }
+  if (!g_api.h) return false;
+#define SYM(name) g_api.name = reinterpret_cast<decltype(g_api.name)>(dlsym(g_api.h, "nccl" #name))
+  SYM(GetUniqueId);
+  SYM(CommInitRank);
+  SYM(CommDestroy);
+  SYM(Send);
+  SYM(Recv);
+  SYM(AllReduce);
+  SYM(GroupStart);
+  SYM(GroupEnd);
+  SYM(GetErrorString);
+#undef SYM
+  return g_api.GetUniqueId && g_api.CommInitRank && g_api.Send && g_api.Recv && g_api.AllReduce &&
+         g_api.GroupStart && g_api.GroupEnd;
+}
+}  // namespace nccl
+
 struct cgks_ctx {
   int device = 0;
+  // z-slab decomposition (nproc = (1,1,P)): rank, size, z offset of this slab
+  int rank = 0, nranks = 1;
+  long long zoff_global = 0;
+  nccl::Comm comm = nullptr;
+  int comm_mode = 0;  // 0 single, 1 NCCL, 2 in-process group (cgks_step_group)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   Geo geo;
@@ -123,17 +178,71 @@ static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
   return rc ? CGKS_ERR_CUDA : CGKS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// z-slab halo: 2 ghost planes per side of every field (R: dependency radius 2 per stage).
+// With the [z][field][y][x] layout each halo is one contiguous block of 2 planes.
+// ---------------------------------------------------------------------------
+static long long plane_block(const cgks_ctx* c) { return (long long)c->NV * c->geo.plane; }
+static double* low_send(const cgks_ctx* c, double* X) { return X + (long long)c->geo.zoff * plane_block(c); }
+static double* high_send(const cgks_ctx* c, double* X) {
+  return X + (long long)(c->geo.zoff + c->geo.n[2] - 2) * plane_block(c);
+}
+static double* low_ghost(const cgks_ctx* c, double* X) { return X; }
+static double* high_ghost(const cgks_ctx* c, double* X) {
+  return X + (long long)(c->geo.zoff + c->geo.n[2]) * plane_block(c);
+}
+
+static int nccl_check(cgks_ctx* ctx, int r, const char* what) {
+  if (r == 0) return CGKS_OK;
+  set_msg(ctx, "NCCL %s failed: %s", what, nccl::g_api.GetErrorString ? nccl::g_api.GetErrorString(r) : "?");
+  return CGKS_ERR_COMM;
+}
+
+// halo exchange of buffer X with the two z neighbours through NCCL (one group per stage)
+static int exchange_nccl(cgks_ctx* ctx, double* X) {
+  const int P = ctx->nranks, r = ctx->rank;
+  const int lo = (r + P - 1) % P, hi = (r + 1) % P;
+  const size_t cnt = (size_t)(2 * plane_block(ctx));
+  auto& A = nccl::g_api;
+  int e = A.GroupStart();
+  if (!e) e = A.Send(low_send(ctx, X), cnt, nccl::Float64, lo, ctx->comm, ctx->stream);
+  if (!e) e = A.Send(high_send(ctx, X), cnt, nccl::Float64, hi, ctx->comm, ctx->stream);
+  if (!e) e = A.Recv(high_ghost(ctx, X), cnt, nccl::Float64, hi, ctx->comm, ctx->stream);
+  if (!e) e = A.Recv(low_ghost(ctx, X), cnt, nccl::Float64, lo, ctx->comm, ctx->stream);
+  int e2 = A.GroupEnd();
+  return nccl_check(ctx, e ? e : e2, "halo exchange");
+}
+
+static int exchange(cgks_ctx* ctx, double* X) {
+  if (!ctx->geo.halo[2]) return CGKS_OK;
+  if (ctx->comm_mode == 1) return exchange_nccl(ctx, X);
+  return CGKS_OK;  // group mode exchanges in cgks_step_group
+}
+
+static int dt_reduce(cgks_ctx* ctx) {
+  if (ctx->comm_mode != 1) return CGKS_OK;
+  // min over ranks of the candidate bit pattern (order-preserving for positive doubles)
+  int e = nccl::g_api.AllReduce(&ctx->ts->dtmin_bits, &ctx->ts->dtmin_bits, 1, nccl::Uint64, nccl::Min, ctx->comm,
+                                ctx->stream);
+  return nccl_check(ctx, e, "allreduce(min) of dt");
+}
+
 // one full time step from U[cur] into U[1-cur]
 static int one_step(cgks_ctx* ctx) {
-  const double* Un = ctx->U[ctx->cur];
+  double* Un = ctx->U[ctx->cur];
   double* Unext = ctx->U[1 - ctx->cur];
   LaunchEnv env = env_of(ctx);
   if (ctx->ops->dt(env, Un, ctx->NV, ctx->ts, ctx->err, ctx->ncell)) return CGKS_ERR_CUDA;
-  int rc;
+  int rc = dt_reduce(ctx);
+  if (rc) return rc;
+  if (ctx->ops->dt_final(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
+  rc = exchange(ctx, Un);
+  if (rc) return rc;
   if (ctx->time_scheme == CGKS_TIME_S1O2) {
     rc = run_stage(ctx, Un, Unext, 2, 1);
   } else {
     rc = run_stage(ctx, Un, ctx->Us, 0, 1);
+    if (!rc) rc = exchange(ctx, ctx->Us);
     if (!rc) rc = run_stage(ctx, ctx->Us, Unext, 1, 2);
   }
   if (rc) return rc;
@@ -192,12 +301,24 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "unknown scheme id %d", scheme->id);
     return fail(CGKS_ERR_CONFIG);
   }
-  int nranks = 1;
-  for (int a = 0; a < 3; ++a) nranks *= grid->nproc[a] > 0 ? grid->nproc[a] : 1;
-  if (nranks != 1) {
-    set_msg(ctx, "multi-rank decomposition is not available in this build");
+  // z-slab decomposition: nproc = (1, 1, P)
+  const int P = grid->nproc[2] > 0 ? grid->nproc[2] : 1;
+  if ((grid->nproc[0] > 1) || (grid->nproc[1] > 1)) {
+    set_msg(ctx, "only z-slab decompositions nproc = (1,1,P) are supported");
     return fail(CGKS_ERR_CONFIG);
   }
+  if (P > 1) {
+    const bool zper = grid->bc[2][0] == CGKS_BC_PERIODIC && grid->bc[2][1] == CGKS_BC_PERIODIC;
+    if (grid->n[2] <= 1 || !zper || grid->n[2] % P != 0 || grid->n[2] / P < 4 || grid->rank < 0 ||
+        grid->rank >= P) {
+      set_msg(ctx, "z-slab decomposition needs a 3-D grid, periodic z, nz divisible by P, >= 4 planes per "
+                   "rank and 0 <= rank < P (nz=%lld P=%d rank=%d)",
+              (long long)grid->n[2], P, grid->rank);
+      return fail(CGKS_ERR_CONFIG);
+    }
+  }
+  ctx->nranks = P;
+  ctx->rank = P > 1 ? grid->rank : 0;
   int dim = grid->n[2] > 1 ? 3 : (grid->n[1] > 1 ? 2 : 1);
   if ((dim < 3 && grid->n[2] != 1) || (dim < 2 && grid->n[1] != 1)) {
     set_msg(ctx, "active axes must be the leading ones");
@@ -222,13 +343,19 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     g.n[a] = (int)grid->n[a];
     g.h[a] = (grid->hi[a] - grid->lo[a]) / grid->n[a];
     g.ih[a] = 1.0 / g.h[a];
+    if (a == 2 && P > 1) {  // this rank's slab; ghost planes filled by the halo exchange
+      g.n[2] = (int)(grid->n[2] / P);
+      g.halo[2] = 1;
+      g.zoff = 2;
+      ctx->zoff_global = (long long)ctx->rank * g.n[2];
+    }
     bool per = grid->bc[a][0] == CGKS_BC_PERIODIC && grid->bc[a][1] == CGKS_BC_PERIODIC;
     if (!per && (grid->bc[a][0] == CGKS_BC_PERIODIC || grid->bc[a][1] == CGKS_BC_PERIODIC)) {
       set_msg(ctx, "axis %d mixes periodic and non-periodic sides", a);
       return fail(CGKS_ERR_CONFIG);
     }
-    g.bounded[a] = (a < dim && !per) ? 1 : 0;
-    if (g.bounded[a]) ctx->box = 1;
+    g.bounded[a] = ((a < dim && !per) || g.halo[a]) ? 1 : 0;
+    if (a < dim && !per) ctx->box = 1;
     g.elo[a] = g.bounded[a] ? -1 : 0;
     g.en[a] = g.n[a] + (g.bounded[a] ? 2 : 0);
     for (int s = 0; s < 2; ++s) {
@@ -319,8 +446,9 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   int NV = ctx->NV;
   int nrec = ctx->scheme_id == CGKS_CGKS5 ? ctx->cls.nb * 5 : 15;
   int nff = ctx->scheme_id == CGKS_CGKS5 ? 30 : 10;
-  bool ok = alloc(&ctx->U[0], ctx->ncell * NV) && alloc(&ctx->U[1], ctx->ncell * NV) &&
-            alloc(&ctx->Us, ctx->ncell * NV) && alloc(&ctx->carry, ctx->ncell * NV) &&
+  const long long nstore = (long long)g.plane * (g.n[2] + 2 * g.zoff) * NV;  // incl. z ghost planes
+  bool ok = alloc(&ctx->U[0], nstore) && alloc(&ctx->U[1], nstore) && alloc(&ctx->Us, nstore) &&
+            alloc(&ctx->carry, nstore) &&
             alloc(&ctx->rec, ctx->necell * nrec) && alloc(&ctx->staging, ctx->ncell * 15);
   for (int a = 0; a < dim && ok; ++a)
     ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] * g.fn[a][2] * nff);
@@ -366,7 +494,27 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       }
     }
   }
-  cudaMemset(ctx->U[0], 0, sizeof(double) * ctx->ncell * NV);
+  cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
+  // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
+  // group stepped by cgks_step_group (halo copies on one device)
+  if (P > 1) {
+    if (grid->nccl_id) {
+      if (!nccl::load()) {
+        set_msg(ctx, "cannot load libnccl.so.2 (set CGKS_NCCL_LIB)");
+        return fail(CGKS_ERR_COMM);
+      }
+      nccl::UniqueId id;
+      std::memcpy(id.internal, grid->nccl_id, sizeof(id.internal));
+      int e = nccl::g_api.CommInitRank(&ctx->comm, P, id, ctx->rank);
+      if (e) {
+        set_msg(ctx, "ncclCommInitRank failed (%d)", e);
+        return fail(CGKS_ERR_COMM);
+      }
+      ctx->comm_mode = 1;
+    } else {
+      ctx->comm_mode = 2;
+    }
+  }
   cudaMemset(ctx->err, 0, sizeof(ErrState));
   TimeState t0;
   std::memset(&t0, 0, sizeof(t0));
@@ -388,7 +536,116 @@ int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]) {
     off[a] = 0;
     n[a] = ctx->geo.n[a];
   }
+  off[2] = ctx->zoff_global;
   return CGKS_OK;
+}
+
+int cgks_decompose(const int64_t n[3], const int nproc[3], int rank, int64_t off[3], int64_t nloc[3], int nbr[2]) {
+  const int P = nproc[2] > 0 ? nproc[2] : 1;
+  if ((nproc[0] > 1) || (nproc[1] > 1) || rank < 0 || rank >= P || n[2] % P != 0) return CGKS_ERR_CONFIG;
+  for (int a = 0; a < 3; ++a) {
+    off[a] = 0;
+    nloc[a] = n[a];
+  }
+  nloc[2] = n[2] / P;
+  off[2] = (int64_t)rank * nloc[2];
+  nbr[0] = (rank + P - 1) % P;
+  nbr[1] = (rank + 1) % P;
+  return CGKS_OK;
+}
+
+int cgks_nccl_unique_id(void* out128) {
+  if (!out128) return CGKS_ERR_CONFIG;
+  if (!nccl::load()) return CGKS_ERR_COMM;
+  nccl::UniqueId id;
+  if (nccl::g_api.GetUniqueId(&id)) return CGKS_ERR_COMM;
+  std::memcpy(out128, id.internal, sizeof(id.internal));
+  return CGKS_OK;
+}
+
+static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0);
+
+// In-process group of slab contexts on one device, stepped in lock-step: one shared time state,
+// all work on the first context's stream, halos copied between the contexts' buffers.
+int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
+  if (!ctxs || n < 1 || nsteps < 0) return CGKS_ERR_CONFIG;
+  cgks_ctx* c0 = ctxs[0];
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || ctxs[r]->rank != r || ctxs[r]->nranks != n || ctxs[r]->comm_mode == 1 ||
+        std::memcmp(&ctxs[r]->geo, &c0->geo, sizeof(Geo)) != 0 || ctxs[r]->device != c0->device ||
+        ctxs[r]->cur != c0->cur) {
+      set_msg(c0, "cgks_step_group: contexts must be ranks 0..n-1 of one in-process decomposition");
+      return CGKS_ERR_CONFIG;
+    }
+  }
+  cgks_ctx* ctx = c0;
+  int rc = upload_constants(c0);
+  if (rc) return rc;
+  // borrow the first context's stream, time state and error flag
+  std::vector<cudaStream_t> st(n);
+  std::vector<TimeState*> ts(n);
+  std::vector<ErrState*> er(n);
+  for (int r = 0; r < n; ++r) {
+    st[r] = ctxs[r]->stream;
+    ts[r] = ctxs[r]->ts;
+    er[r] = ctxs[r]->err;
+    ctxs[r]->stream = c0->stream;
+    ctxs[r]->ts = c0->ts;
+    ctxs[r]->err = c0->err;
+    g_const_owner = c0;  // identical geometry: one upload serves all
+  }
+  TimeState t;
+  CK(cudaMemcpyAsync(&t, c0->ts, sizeof(t), cudaMemcpyDeviceToHost, c0->stream));
+  CK(cudaStreamSynchronize(c0->stream));
+  const int cur0 = c0->cur;
+  auto xchg = [&](int which) -> int {  // which: 0 = U[cur], 1 = Us
+    if (n == 1) return CGKS_OK;
+    const size_t bytes = sizeof(double) * (size_t)(2 * plane_block(c0));
+    for (int r = 0; r < n; ++r) {
+      cgks_ctx* me = ctxs[r];
+      cgks_ctx* lo = ctxs[(r + n - 1) % n];
+      cgks_ctx* hi = ctxs[(r + 1) % n];
+      double* Xm = which ? me->Us : me->U[me->cur];
+      double* Xl = which ? lo->Us : lo->U[lo->cur];
+      double* Xh = which ? hi->Us : hi->U[hi->cur];
+      if (cudaMemcpyAsync(low_ghost(me, Xm), high_send(lo, Xl), bytes, cudaMemcpyDeviceToDevice, c0->stream) ||
+          cudaMemcpyAsync(high_ghost(me, Xm), low_send(hi, Xh), bytes, cudaMemcpyDeviceToDevice, c0->stream))
+        return CGKS_ERR_CUDA;
+    }
+    return CGKS_OK;
+  };
+  for (int s = 0; s < nsteps && !rc; ++s) {
+    LaunchEnv env = env_of(c0);
+    for (int r = 0; r < n && !rc; ++r)
+      if (ctxs[r]->ops->dt(env, ctxs[r]->U[ctxs[r]->cur], ctxs[r]->NV, c0->ts, c0->err, ctxs[r]->ncell))
+        rc = CGKS_ERR_CUDA;
+    if (!rc && c0->ops->dt_final(env, c0->ts, c0->err)) rc = CGKS_ERR_CUDA;
+    if (!rc) rc = xchg(0);
+    if (c0->time_scheme == CGKS_TIME_S1O2) {
+      for (int r = 0; r < n && !rc; ++r)
+        rc = run_stage(ctxs[r], ctxs[r]->U[ctxs[r]->cur], ctxs[r]->U[1 - ctxs[r]->cur], 2, 1);
+    } else {
+      for (int r = 0; r < n && !rc; ++r) rc = run_stage(ctxs[r], ctxs[r]->U[ctxs[r]->cur], ctxs[r]->Us, 0, 1);
+      if (!rc) rc = xchg(1);
+      for (int r = 0; r < n && !rc; ++r) rc = run_stage(ctxs[r], ctxs[r]->Us, ctxs[r]->U[1 - ctxs[r]->cur], 1, 2);
+    }
+    if (!rc && c0->ops->step_end(env, c0->ts, c0->err)) rc = CGKS_ERR_CUDA;
+    for (int r = 0; r < n; ++r) ctxs[r]->cur = 1 - ctxs[r]->cur;
+  }
+  if (!rc) rc = finish_steps(c0, cur0, t.steps);
+  for (int r = 1; r < n; ++r) ctxs[r]->cur = c0->cur;
+  // copy the shared time state to every member, restore their resources
+  for (int r = 0; r < n; ++r) {
+    ctxs[r]->stream = st[r];
+    ctxs[r]->ts = ts[r];
+    ctxs[r]->err = er[r];
+    if (r > 0) {
+      cudaMemcpyAsync(ts[r], ts[0], sizeof(TimeState), cudaMemcpyDeviceToDevice, c0->stream);
+      cudaMemcpyAsync(er[r], er[0], sizeof(ErrState), cudaMemcpyDeviceToDevice, c0->stream);
+    }
+  }
+  cudaStreamSynchronize(c0->stream);
+  return rc;
 }
 
 static bool is_device_ptr(const void* p) {
@@ -458,6 +715,10 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0) {
 
 int cgks_step(cgks_ctx* ctx, int nsteps) {
   if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
+  if (ctx->comm_mode == 2) {
+    set_msg(ctx, "context belongs to an in-process decomposition: use cgks_step_group");
+    return CGKS_ERR_CONFIG;
+  }
   int rc = upload_constants(ctx);
   if (rc) return rc;
   TimeState t;
@@ -698,6 +959,7 @@ extern "C" int cgks_fp64_peak(double* tflops, double* ms_out) {
 
 void cgks_destroy(cgks_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us, ctx->carry, ctx->rec, ctx->staging,
                     ctx->face[0], ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2]};

@@ -43,7 +43,8 @@ struct DimOps {
   int (*upload)(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s);
   // mode 0: S2O4 stage 1, 1: S2O4 stage 2, 2: S1O2
   int (*stage)(LaunchEnv& env, const StageArgs& a, int mode, int stage);
-  int (*dt)(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell);
+  int (*dt)(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell);  // local min
+  int (*dt_final)(LaunchEnv& env, TimeState* ts, ErrState* err);  // dt = CFL * (global) min
   int (*step_end)(LaunchEnv& env, TimeState* ts, ErrState* err);
   int (*pack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);

@@ -70,8 +70,11 @@ __host__ __device__ constexpr int nbr_off(int n, int ax) {
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
 __device__ __forceinline__ long long sidx(int NV, int f, int i, int j, int k) {
-  return ((long long)k * NV + f) * c_geo.plane + (long long)j * c_geo.n[0] + i;
+  return ((long long)(k + c_geo.zoff) * NV + f) * c_geo.plane + (long long)j * c_geo.n[0] + i;
 }
+
+// periodic wrap, except on decomposed axes whose ghost cells are stored
+__device__ __forceinline__ int wrap_ax(int a, int i) { return c_geo.halo[a] ? i : wrapi(i, c_geo.n[a]); }
 
 // value of field f (0-4 Q, 5-19 gradient [axis][var]) of cell (i,j,k), any integer index
 template <bool BOX>
@@ -80,13 +83,14 @@ __device__ __forceinline__ double ld_state(const double* __restrict__ U, int NV,
   if (BOX) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (c_geo.bounded[a] && (idx[a] < 0 || idx[a] >= c_geo.n[a])) {
+      if (c_geo.bounded[a] && !c_geo.halo[a] && (idx[a] < 0 || idx[a] >= c_geo.n[a])) {
         int side = idx[a] < 0 ? 0 : 1;
         if (c_geo.bc[a][side] == 1) return f < 5 ? c_geo.bc_state[a][side][f] : 0.0;
       }
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
+      if (c_geo.halo[a]) continue;
       if (c_geo.bounded[a]) {
         idx[a] = idx[a] < 0 ? 0 : (idx[a] >= c_geo.n[a] ? c_geo.n[a] - 1 : idx[a]);
       } else {
@@ -95,7 +99,7 @@ __device__ __forceinline__ double ld_state(const double* __restrict__ U, int NV,
     }
   } else {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) idx[a] = wrapi(idx[a], c_geo.n[a]);
+    for (int a = 0; a < 3; ++a) idx[a] = wrap_ax(a, idx[a]);
   }
   return __ldg(U + sidx(NV, f, idx[0], idx[1], idx[2]));
 }
@@ -177,7 +181,7 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
     if (BOX) {
       buf[idx] = ld_state<true>(U, 20, fld, i, j, kk);
     } else {
-      cp_async8(buf + idx, U + sidx(20, fld, wrapi(i, c_geo.n[0]), wrapi(j, c_geo.n[1]), wrapi(kk, c_geo.n[2])));
+      cp_async8(buf + idx, U + sidx(20, fld, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk)));
     }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       if (BOX) {
         for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
       } else {
-        const double* ub = U + sidx(NV, 0, wrapi(ci, c_geo.n[0]), wrapi(cj, c_geo.n[1]), wrapi(ck, c_geo.n[2]));
+        const double* ub = U + sidx(NV, 0, wrap_ax(0, ci), wrap_ax(1, cj), wrap_ax(2, ck));
         for (int v = fsub; v < 5; v += TPC) cp_async8(tile + (FT::NREC + v) * NT + c, ub + v * c_geo.plane);
       }
     }
@@ -729,7 +733,7 @@ static __global__ void k_pack(const double* __restrict__ src, double* __restrict
   const long long c = t % nc;
   const int k = (int)(c / c_geo.plane);
   const long long r = c % c_geo.plane;
-  dst[((long long)k * NV + f0 + f) * c_geo.plane + r] = src ? src[t] : 0.0;
+  dst[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.plane + r] = src ? src[t] : 0.0;
 }
 
 static __global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
@@ -740,7 +744,7 @@ static __global__ void k_unpack(const double* __restrict__ src, double* __restri
   const long long c = t % nc;
   const int k = (int)(c / c_geo.plane);
   const long long r = c % c_geo.plane;
-  dst[t] = src[((long long)k * NV + f0 + f) * c_geo.plane + r];
+  dst[t] = src[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.plane + r];
 }
 
 }  // namespace cgks

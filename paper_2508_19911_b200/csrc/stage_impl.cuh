@@ -154,6 +154,10 @@ int upload_fn(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cuda
 
 int dt_fn(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell) {
   LAUNCH("dt", k_dt<D>, ncell, 256, U, NV, ts, err);
+  return 0;
+}
+
+int dt_final_fn(LaunchEnv& env, TimeState* ts, ErrState* err) {
   LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ts, (const ErrState*)err);
   return 0;
 }

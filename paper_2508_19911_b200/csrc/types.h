@@ -12,7 +12,9 @@ namespace cgks {
 struct Geo {
   int n[3];          // local cells
   int dim;
-  int bounded[3];    // axis has non-periodic boundaries
+  int bounded[3];    // axis has non-periodic boundaries, or is a decomposed axis (ghost storage)
+  int halo[3];       // axis is decomposed: ghost cells are stored (filled by the halo exchange)
+  int zoff;          // storage offset of z-plane 0 (2 ghost planes when z is decomposed)
   int elo[3];        // extended (reconstruction) range start: -1 on bounded axes
   int en[3];         // extended counts
   int fn[3][3];      // face-grid dims for faces normal to axis a: fn[a][b]
