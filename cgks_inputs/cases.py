@@ -163,12 +163,20 @@ def _pt1d(kind, x):
             "k2": np.cos(2 * x), "one": np.ones_like(x)}[kind]
 
 
-def tgv(n: int = 64, Ma: float = 0.1, Re: float = 1600.0, Pr: float = 0.72, gamma: float = 1.4) -> Case:
-    nn = (n, n, n)
-    lo, hi = (-PI, -PI, -PI), (PI, PI, PI)
+def tgv(n: int = 64, Ma: float = 0.1, Re: float = 1600.0, Pr: float = 0.72, gamma: float = 1.4,
+        zrep: int = 1, z0: int = 0, nzb: int = None) -> Case:
+    """TGV on [-pi,pi]^2 x [-pi, -pi + 2 pi zrep] with n x n x (n zrep) cells (zrep periods along z,
+    for weak scaling); optionally only the z-planes [z0, z0+nzb) of it (one rank's slab)."""
+    nzg = n * zrep
+    if nzb is None:
+        nzb = nzg
+    nn = (n, n, nzg)
+    lo, hi = (-PI, -PI, -PI), (PI, PI, -PI + 2 * PI * zrep)
     h = 2 * PI / n
     edges = -PI + h * np.arange(n + 1)
     a, b = edges[:-1], edges[1:]
+    zed = -PI + h * np.arange(z0, z0 + nzb + 1)
+    az, bz = zed[:-1], zed[1:]
     p0 = 1.0 / (gamma * Ma * Ma)  # Ma = U0/sqrt(gamma p0/rho0), U0 = rho0 = 1 (P:392-394)
     # separable terms: list of (coef, kx, ky, kz)
     terms = {
@@ -181,14 +189,14 @@ def tgv(n: int = 64, Ma: float = 0.1, Re: float = 1600.0, Pr: float = 0.72, gamm
             (0.5, "sin2", "cos2", "cos2"), (0.5, "cos2", "sin2", "cos2")],
         0: [(1.0, "one", "one", "one")],
     }
-    Q = np.zeros((5, n, n, n))
-    G = np.zeros((3, 5, n, n, n))
+    Q = np.zeros((5, nzb, n, n))
+    G = np.zeros((3, 5, nzb, n, n))
     for v, tl in terms.items():
         for (c, kx, ky, kz) in tl:
-            Ax, Ay, Az = _avg1d(kx, a, b), _avg1d(ky, a, b), _avg1d(kz, a, b)
+            Ax, Ay, Az = _avg1d(kx, a, b), _avg1d(ky, a, b), _avg1d(kz, az, bz)
             Dx = (_pt1d(kx, b) - _pt1d(kx, a)) / h
             Dy = (_pt1d(ky, b) - _pt1d(ky, a)) / h
-            Dz = (_pt1d(kz, b) - _pt1d(kz, a)) / h
+            Dz = (_pt1d(kz, bz) - _pt1d(kz, az)) / h
             Q[v] += c * Az[:, None, None] * Ay[None, :, None] * Ax[None, None, :]
             G[0, v] += c * Az[:, None, None] * Ay[None, :, None] * Dx[None, None, :]
             G[1, v] += c * Az[:, None, None] * Dy[None, :, None] * Ax[None, None, :]
