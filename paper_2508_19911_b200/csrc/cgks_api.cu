@@ -824,11 +824,14 @@ struct XchgMirror {
 };
 struct ParkHost {
   fc::CD* slots;
+  double* marks;
   void put(int s, const fc::CD& v) const { slots[s] = v; }
   fc::CD get(int s) const { return slots[s]; }
+  void mark(int m) const { marks[m] = fc::tally().flops; }
 };
 
-// flops of one Gauss point = both cooperating lanes
+// flops of one Gauss point: both cooperating lanes, the parts of the equilibrium phase that both
+// lanes execute redundantly (to avoid divergence) counted once
 static double flux_point_flops(const FluxConst& f, bool compact) {
   using fc::CD;
   CD W[2][5], dW[2][3][5];
@@ -845,12 +848,13 @@ static double flux_point_flops(const FluxConst& f, bool compact) {
   for (int side = 0; side < 2; ++side) {
     GPOutT<CD> o;
     CD slots[32];
+    double marks[5] = {0, 0, 0, 0, 0};
     fc::tally() = fc::Tally();
     if (compact)
-      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots}, o);
+      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots, marks}, o);
     else
-      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots}, o);
-    total += fc::tally().flops;
+      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots, marks}, o);
+    total += fc::tally().flops - (side == 1 ? (marks[2] - marks[1]) + (marks[4] - marks[3]) : 0.0);
   }
   return total;
 }

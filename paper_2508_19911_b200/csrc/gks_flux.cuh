@@ -185,6 +185,7 @@ struct ParkDev {
   double* base;  // base + slot * 128 + lane
   __device__ __forceinline__ void put(int s, double v) const { base[s * 128] = v; }
   __device__ __forceinline__ double get(int s) const { return base[s * 128]; }
+  __device__ __forceinline__ void mark(int) const {}  // phase markers (used by the host flop count)
 };
 
 // ---------------------------------------------------------------------------
@@ -259,6 +260,7 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     }
   }
   bool good = ok && ok_other;
+  park.mark(1);  // start of the equilibrium phase (identical in both lanes)
   const T pL = side == 0 ? p : other_p, pR = side == 0 ? other_p : p;
   // ---- (G) interface equilibrium g0 (R13, R14)
   const T r0 = x1[0], i0 = 1.0 / r0;
@@ -320,13 +322,29 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
       for (int i = 0; i < 5; ++i) b[i] = x1[5 + 5 * d + i] * i0;
       micro_slope(U0, V0, Ww0, l0, fc.N, b, ab[d]);
     }
-    // MQa = rho0 <(abar.u) psi>, MF0 = rho0 <u psi>
-    T MQa[1][5], MF0[5];
+    park.mark(2);  // end of the first duplicated block
+    // MQa = rho0 <(abar.u) psi> (lane side 0) and MF1 = rho0 <u (abar.u) psi> (lane side 1) are the same
+    // three contractions with the normal-velocity moments shifted by one order: one code path,
+    // moments shifted by `side`, then one exchange
+    T MQa[1][5], MF1[1][5];
+    {
+      T U0s[6];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) MQa[0][i] = MF0[i] = 0.0;
-    sym_mv<1, 0, 0, 1, true>(U0f, t0, &ab[0], MQa, MF0);
-    sym_mv<0, 1, 0, 1, false>(U0f, t0, &ab[1], MQa, (T*)nullptr);
-    sym_mv<0, 0, 1, 1, false>(U0f, t0, &ab[2], MQa, (T*)nullptr);
+      for (int kk = 0; kk < 6; ++kk) U0s[kk] = side ? U0f[kk + 1] : U0f[kk];
+      T Xs[1][5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) Xs[0][i] = 0.0;
+      sym_mv<1, 0, 0, 1, false>(U0s, t0, &ab[0], Xs, (T*)nullptr);
+      sym_mv<0, 1, 0, 1, false>(U0s, t0, &ab[1], Xs, (T*)nullptr);
+      sym_mv<0, 0, 1, 1, false>(U0s, t0, &ab[2], Xs, (T*)nullptr);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const T y = xchg(Xs[0][i]);
+        MQa[0][i] = side ? y : Xs[0][i];
+        MF1[0][i] = side ? Xs[0][i] : y;
+      }
+    }
+    park.mark(3);  // start of the second duplicated block
     // Abar from compatibility (R16): <(abar.u + Abar) psi> = 0
     T Ab[1][5];
     {
@@ -335,14 +353,11 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
       for (int i = 0; i < 5; ++i) b[i] = -MQa[0][i];
       micro_slope(U0, V0, Ww0, l0, fc.N, b, Ab[0]);
     }
-    // MF2 = rho0 <u Abar psi>, MF1 = rho0 <u (abar.u) psi>
-    T MF2[1][5], MF1[1][5];
+    // MF0 = rho0 <u psi>, MF2 = rho0 <u Abar psi>
+    T MF2[1][5], MF0[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) MF2[0][i] = MF1[0][i] = 0.0;
-    sym_mv<1, 0, 0, 1, false>(U0f, t0, Ab, MF2, (T*)nullptr);
-    sym_mv<2, 0, 0, 1, false>(U0f, t0, &ab[0], MF1, (T*)nullptr);
-    sym_mv<1, 1, 0, 1, false>(U0f, t0, &ab[1], MF1, (T*)nullptr);
-    sym_mv<1, 0, 1, 1, false>(U0f, t0, &ab[2], MF1, (T*)nullptr);
+    for (int i = 0; i < 5; ++i) MF2[0][i] = MF0[i] = 0.0;
+    sym_mv<1, 0, 0, 1, true>(U0f, t0, Ab, MF2, MF0);
     const T sMF0 = r0 * qF(MF0, U0, V0, Ww0, uu2), sMF1 = r0 * qF(MF1[0], U0, V0, Ww0, uu2),
             sMF2 = r0 * qF(MF2[0], U0, V0, Ww0, uu2), sMQa = r0 * qF(MQa[0], U0, V0, Ww0, uu2);
 #pragma unroll
@@ -357,6 +372,7 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     acc[20] += (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) + al[2] * (sMF2 + U0 * sMQa);
     acc[21] += be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
   }
+  park.mark(4);  // end of the equilibrium phase
   // ---- (A2) own side: compatibility coefficients A (R16), Euler time derivative (R23),
   // half-range flux and state terms of this side
   T sacc[22];
