@@ -111,6 +111,12 @@ struct cgks_ctx {
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   int launches_per_step = 0;
   const DimOps* ops = nullptr;
+  // CUDA graphs of one time step starting from U[0] and from U[1] (captured on first use,
+  // replayed by cgks_step); captured on a private stream, launched on the context's stream
+  bool use_graph = true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  bool capturing = false;
 };
 
 static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
@@ -145,7 +151,7 @@ static int upload_constants(cgks_ctx* ctx) {
 
 static LaunchEnv env_of(cgks_ctx* ctx) {
   LaunchEnv e;
-  e.stream = ctx->stream;
+  e.stream = ctx->capturing ? ctx->cap_stream : ctx->stream;
   e.prof = ctx->prof;
   e.pending = &ctx->pending;
   e.msg = ctx->msg;
@@ -204,11 +210,12 @@ static int exchange_nccl(cgks_ctx* ctx, double* X) {
   const int lo = (r + P - 1) % P, hi = (r + 1) % P;
   const size_t cnt = (size_t)(2 * plane_block(ctx));
   auto& A = nccl::g_api;
+  cudaStream_t st = ctx->capturing ? ctx->cap_stream : ctx->stream;
   int e = A.GroupStart();
-  if (!e) e = A.Send(low_send(ctx, X), cnt, nccl::Float64, lo, ctx->comm, ctx->stream);
-  if (!e) e = A.Send(high_send(ctx, X), cnt, nccl::Float64, hi, ctx->comm, ctx->stream);
-  if (!e) e = A.Recv(high_ghost(ctx, X), cnt, nccl::Float64, hi, ctx->comm, ctx->stream);
-  if (!e) e = A.Recv(low_ghost(ctx, X), cnt, nccl::Float64, lo, ctx->comm, ctx->stream);
+  if (!e) e = A.Send(low_send(ctx, X), cnt, nccl::Float64, lo, ctx->comm, st);
+  if (!e) e = A.Send(high_send(ctx, X), cnt, nccl::Float64, hi, ctx->comm, st);
+  if (!e) e = A.Recv(high_ghost(ctx, X), cnt, nccl::Float64, hi, ctx->comm, st);
+  if (!e) e = A.Recv(low_ghost(ctx, X), cnt, nccl::Float64, lo, ctx->comm, st);
   int e2 = A.GroupEnd();
   return nccl_check(ctx, e ? e : e2, "halo exchange");
 }
@@ -223,7 +230,7 @@ static int dt_reduce(cgks_ctx* ctx) {
   if (ctx->comm_mode != 1) return CGKS_OK;
   // min over ranks of the candidate bit pattern (order-preserving for positive doubles)
   int e = nccl::g_api.AllReduce(&ctx->ts->dtmin_bits, &ctx->ts->dtmin_bits, 1, nccl::Uint64, nccl::Min, ctx->comm,
-                                ctx->stream);
+                                ctx->capturing ? ctx->cap_stream : ctx->stream);
   return nccl_check(ctx, e, "allreduce(min) of dt");
 }
 
@@ -522,6 +529,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   std::memcpy(&t0.dtmin_bits, &big, sizeof(big));
   cudaMemcpy(ctx->ts, &t0, sizeof(t0), cudaMemcpyHostToDevice);
   ctx->launches_per_step = count_launches(ctx);
+  ctx->use_graph = std::getenv("CGKS_NO_GRAPH") == nullptr;
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_msg(ctx, "device error during create");
     return fail(CGKS_ERR_CUDA);
@@ -713,6 +721,33 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0) {
   return CGKS_OK;
 }
 
+// capture one time step starting from U[c] into a CUDA graph (stage driver of section 8(a) a5)
+static int capture_step(cgks_ctx* ctx, int c) {
+  if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  const int saved = ctx->cur;
+  ctx->cur = c;
+  ctx->capturing = true;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal);
+  int rc = e == cudaSuccess ? one_step(ctx) : CGKS_ERR_CUDA;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &g);
+  ctx->capturing = false;
+  ctx->cur = saved;
+  if (rc || e != cudaSuccess || e2 != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return rc ? rc : CGKS_ERR_CUDA;
+  }
+  e = cudaGraphInstantiate(&ctx->graph[c], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    ctx->graph[c] = nullptr;
+    cudaGetLastError();
+    return CGKS_ERR_CUDA;
+  }
+  return CGKS_OK;
+}
+
 int cgks_step(cgks_ctx* ctx, int nsteps) {
   if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
   if (ctx->comm_mode == 2) {
@@ -725,9 +760,18 @@ int cgks_step(cgks_ctx* ctx, int nsteps) {
   CK(cudaMemcpyAsync(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   int cur0 = ctx->cur;
+  if (ctx->use_graph && nsteps > 0) {
+    for (int c = 0; c < 2 && ctx->use_graph; ++c)
+      if (!ctx->graph[c] && capture_step(ctx, c)) ctx->use_graph = false;  // fall back to direct launches
+  }
   for (int s = 0; s < nsteps; ++s) {
-    rc = one_step(ctx);
-    if (rc) return rc;
+    if (ctx->use_graph) {
+      CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
+      ctx->cur = 1 - ctx->cur;
+    } else {
+      rc = one_step(ctx);
+      if (rc) return rc;
+    }
   }
   return finish_steps(ctx, cur0, t.steps);
 }
@@ -963,6 +1007,9 @@ extern "C" int cgks_fp64_peak(double* tflops, double* ms_out) {
 
 void cgks_destroy(cgks_ctx* ctx) {
   if (!ctx) return;
+  for (int c = 0; c < 2; ++c)
+    if (ctx->graph[c]) cudaGraphExecDestroy(ctx->graph[c]);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us, ctx->carry, ctx->rec, ctx->staging,

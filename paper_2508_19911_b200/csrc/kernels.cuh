@@ -408,10 +408,10 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
         for (int v = fsub; v < 5; v += TPC) cp_async8(tile + (FT::NREC + v) * NT + c, ub + v * c_geo.plane);
       }
     }
-    cp_async_wait_all();
   }
   if (COMPACT)
-    for (int q = threadIdx.x; q < 2 * FT::NQ * NB; q += blockDim.x) tab[(q / NB) * FT::TS + q % NB] = gtab[q];
+    for (int q = threadIdx.x; q < 2 * FT::NQ * NB; q += blockDim.x) cp_async8(tab + (q / NB) * FT::TS + q % NB, gtab + q);
+  cp_async_wait_all();
   __syncthreads();
 
   const double dt = ts->dt;
