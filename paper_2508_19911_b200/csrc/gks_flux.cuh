@@ -180,6 +180,69 @@ HD T qF(const T* v, T U0, T V0, T W0, T uu2) {
   return v[4] - (U0 * v[1] + V0 * v[2] + W0 * v[3]) + uu2 * v[0];
 }
 
+// ---------------------------------------------------------------------------
+// Full-Maxwellian contractions as Jacobian-vector products.  The micro-slope a of a
+// perturbation dW is the first-order expansion of the Maxwellian, g(W + e dW) = g(W)(1 + e a.psi),
+// so rho <X a psi> = D[rho <X psi>](W) dW for any velocity weight X.  With X = u_al this is the
+// Euler-flux Jacobian, with X = u_n u_al the Jacobian of H_al = rho <u_n u_al psi>; both have
+// closed forms (BGK gas with N internal degrees of freedom, N + 3 = 2/(gamma-1)).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Dprim {
+  T dr, du[3], dp, udu;
+};
+
+// primitive perturbation (d rho, dU, dp) of a conservative perturbation d at (rho, U)
+template <typename T>
+HD Dprim<T> dprim(T ir, const T* U, T uu2, double gm1, const T* d) {
+  Dprim<T> q;
+  q.dr = d[0];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) q.du[i] = (d[1 + i] - U[i] * d[0]) * ir;
+  q.dp = gm1 * (d[4] - (U[0] * d[1] + U[1] * d[2] + U[2] * d[3]) + uu2 * d[0]);
+  q.udu = U[0] * q.du[0] + U[1] * q.du[1] + U[2] * q.du[2];
+  return q;
+}
+
+// acc += s DF_al(W) d, F_al = (m_al, m_al U + p e_al, U_al (E + p)) the Euler flux along al
+template <int AL, typename T, typename S>
+HD void jvp_flux(T rho, const T* U, T p, T E, const T* d, const Dprim<T>& q, S s, T* acc) {
+  const T mA = rho * U[AL];
+  acc[0] += s * d[1 + AL];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    T v = d[1 + AL] * U[b] + mA * q.du[b];
+    if (b == AL) v += q.dp;
+    acc[1 + b] += s * v;
+  }
+  acc[4] += s * (q.du[AL] * (E + p) + U[AL] * (d[4] + q.dp));
+}
+
+// acc += DH_al(W) d, H_al = rho <u_n u_al psi> (n = 0, the face normal):
+//   H[0] = rho U_n U_al + p d_{n al}
+//   H[b] = rho U_n U_al U_b + p (d_{n al} U_b + d_{n b} U_al + d_{al b} U_n)
+//   H[4] = ((rho |U|^2 + (N+7) p) U_n U_al + (p |U|^2 + (N+5) p^2/rho) d_{n al}) / 2
+template <int AL, typename T>
+HD void jvp_flux2(T rho, T ir, const T* U, T p, T uu, double K5, double K7, const Dprim<T>& q, T* acc) {
+  const T UnUa = U[0] * U[AL];
+  const T dUnUa = q.du[0] * U[AL] + U[0] * q.du[AL];
+  acc[0] += q.dr * UnUa + rho * dUnUa;
+  if (AL == 0) acc[0] += q.dp;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    T v = q.dr * UnUa * U[b] + rho * (dUnUa * U[b] + UnUa * q.du[b]);
+    if (AL == 0) v += q.dp * U[b] + p * q.du[b];
+    if (b == 0) v += q.dp * U[AL] + p * q.du[AL];
+    if (AL == b) v += q.dp * U[0] + p * q.du[0];
+    acc[1 + b] += v;
+  }
+  const T c1 = rho * uu + K7 * p;
+  const T dc1 = q.dr * uu + 2.0 * rho * q.udu + K7 * q.dp;
+  T v4 = dc1 * UnUa + c1 * dUnUa;
+  if (AL == 0) v4 += q.dp * uu + 2.0 * p * q.udu + K5 * p * ir * (2.0 * q.dp - p * ir * q.dr);
+  acc[4] += 0.5 * v4;
+}
+
 // per-lane parking slots (shared memory on the device) for values that live across phases
 struct ParkDev {
   double* base;  // base + slot * 128 + lane
@@ -241,7 +304,22 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     }
   }
   x1[20] = p;
-  // park what the own-side phase A2 needs (a, W): frees registers during the equilibrium phase
+  // Euler time derivative of this side (R23): dW/dt = rho <A psi> = -sum_al DF_al(W) dW_al (full
+  // moments, compatibility R16), as Jacobian-vector products
+  {
+    const T Uv[3] = {U, V, Ww};
+    const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
+    T dtw[5] = {0, 0, 0, 0, 0};
+    const Dprim<T> q0 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[0]);
+    jvp_flux<0>(rho, Uv, p, W[4], dW[0], q0, -1.0, dtw);
+    const Dprim<T> q1 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[1]);
+    jvp_flux<1>(rho, Uv, p, W[4], dW[1], q1, -1.0, dtw);
+    const Dprim<T> q2 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[2]);
+    jvp_flux<2>(rho, Uv, p, W[4], dW[2], q2, -1.0, dtw);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) park.put(15 + i, dtw[i]);
+  }
+  // park what the own-side phase A2 needs (a, dW/dt): frees registers during the equilibrium phase
 #pragma unroll
   for (int d = 0; d < 3; ++d)
 #pragma unroll
@@ -310,59 +388,41 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     acc[21] = -U0 * sW * (be[0] + be[3]);
   }
   {
-    T U0f[7];
-    full_moments(U0, l0, U0f);
-    Tang<T> t0;
-    tang_table(V0, Ww0, l0, fc.N, t0);
-    T ab[3][5];
+    // equilibrium terms (full Maxwellian g0): MF0 = F_n(W0), MQa = rho0 <(abar.u) psi> =
+    // sum_al DF_al(W0) dW0_al, MF1 = rho0 <u (abar.u) psi> = sum_al DH_al(W0) dW0_al,
+    // MF2 = rho0 <u Abar psi> = DF_n(W0) (rho0 <Abar psi>) = -DF_n(W0) MQa (compatibility R16)
+    const T U0v[3] = {U0, V0, Ww0};
+    const T uu0 = 2.0 * uu2;
+    const double K5 = fc.N + 5.0, K7 = fc.N + 7.0;
+    T MQa[1][5], MF1[1][5], MF2[1][5], MF0[5];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      T b[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) b[i] = x1[5 + 5 * d + i] * i0;
-      micro_slope(U0, V0, Ww0, l0, fc.N, b, ab[d]);
-    }
-    park.mark(2);  // end of the first duplicated block
-    // MQa = rho0 <(abar.u) psi> (lane side 0) and MF1 = rho0 <u (abar.u) psi> (lane side 1) are the same
-    // three contractions with the normal-velocity moments shifted by one order: one code path,
-    // moments shifted by `side`, then one exchange
-    T MQa[1][5], MF1[1][5];
+    for (int i = 0; i < 5; ++i) MQa[0][i] = MF1[0][i] = MF2[0][i] = 0.0;
     {
-      T U0s[6];
-#pragma unroll
-      for (int kk = 0; kk < 6; ++kk) U0s[kk] = side ? U0f[kk + 1] : U0f[kk];
-      T Xs[1][5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) Xs[0][i] = 0.0;
-      sym_mv<1, 0, 0, 1, false>(U0s, t0, &ab[0], Xs, (T*)nullptr);
-      sym_mv<0, 1, 0, 1, false>(U0s, t0, &ab[1], Xs, (T*)nullptr);
-      sym_mv<0, 0, 1, 1, false>(U0s, t0, &ab[2], Xs, (T*)nullptr);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const T y = xchg(Xs[0][i]);
-        MQa[0][i] = side ? y : Xs[0][i];
-        MF1[0][i] = side ? Xs[0][i] : y;
-      }
+      const T* d0 = x1 + 5;
+      const Dprim<T> q0 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d0);
+      jvp_flux<0>(r0, U0v, p0, x1[4], d0, q0, 1.0, MQa[0]);
+      jvp_flux2<0>(r0, i0, U0v, p0, uu0, K5, K7, q0, MF1[0]);
+      const T* d1 = x1 + 10;
+      const Dprim<T> q1 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d1);
+      jvp_flux<1>(r0, U0v, p0, x1[4], d1, q1, 1.0, MQa[0]);
+      jvp_flux2<1>(r0, i0, U0v, p0, uu0, K5, K7, q1, MF1[0]);
+      const T* d2 = x1 + 15;
+      const Dprim<T> q2 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d2);
+      jvp_flux<2>(r0, U0v, p0, x1[4], d2, q2, 1.0, MQa[0]);
+      jvp_flux2<2>(r0, i0, U0v, p0, uu0, K5, K7, q2, MF1[0]);
+      const Dprim<T> qa = dprim(i0, U0v, uu2, fc.gamma - 1.0, MQa[0]);
+      jvp_flux<0>(r0, U0v, p0, x1[4], MQa[0], qa, -1.0, MF2[0]);
     }
-    park.mark(3);  // start of the second duplicated block
-    // Abar from compatibility (R16): <(abar.u + Abar) psi> = 0
-    T Ab[1][5];
-    {
-      T b[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) b[i] = -MQa[0][i];
-      micro_slope(U0, V0, Ww0, l0, fc.N, b, Ab[0]);
-    }
-    // MF0 = rho0 <u psi>, MF2 = rho0 <u Abar psi>
-    T MF2[1][5], MF0[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) MF2[0][i] = MF0[i] = 0.0;
-    sym_mv<1, 0, 0, 1, true>(U0f, t0, Ab, MF2, MF0);
-    const T sMF0 = r0 * qF(MF0, U0, V0, Ww0, uu2), sMF1 = r0 * qF(MF1[0], U0, V0, Ww0, uu2),
-            sMF2 = r0 * qF(MF2[0], U0, V0, Ww0, uu2), sMQa = r0 * qF(MQa[0], U0, V0, Ww0, uu2);
+    MF0[0] = r0 * U0;
+    MF0[1] = r0 * U0 * U0 + p0;
+    MF0[2] = r0 * U0 * V0;
+    MF0[3] = r0 * U0 * Ww0;
+    MF0[4] = U0 * (x1[4] + p0);
+    const T sMF0 = qF(MF0, U0, V0, Ww0, uu2), sMF1 = qF(MF1[0], U0, V0, Ww0, uu2),
+            sMF2 = qF(MF2[0], U0, V0, Ww0, uu2), sMQa = qF(MQa[0], U0, V0, Ww0, uu2);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      const T mf0 = r0 * MF0[i], mf1 = r0 * MF1[0][i], mf2 = r0 * MF2[0][i], mqa = r0 * MQa[0][i];
+      const T mf0 = MF0[i], mf1 = MF1[0][i], mf2 = MF2[0][i], mqa = MQa[0][i];
       acc[i] += al[0] * mf0 + al[1] * mf1 + al[2] * mf2;
       acc[5 + i] += be[0] * mf0 + be[1] * mf1 + be[2] * mf2;
       acc[10 + i] += (al[1] - al[2]) * mqa;  // MQ1 = MQa, MQ2 = -MQa (compatibility)
@@ -372,7 +432,10 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     acc[20] += (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) + al[2] * (sMF2 + U0 * sMQa);
     acc[21] += be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
   }
-  park.mark(4);  // end of the equilibrium phase
+  // the whole equilibrium phase is executed identically by both lanes (counted once)
+  park.mark(2);
+  park.mark(3);
+  park.mark(4);
   // ---- (A2) own side: compatibility coefficients A (R16), Euler time derivative (R23),
   // half-range flux and state terms of this side
   T sacc[22];
@@ -387,19 +450,13 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     tang_table(V, Ww, lam, fc.N, tg);
     T A[1][5];
     {
-      T Uf[7];
-      full_moments(U, lam, Uf);
-      T b[1][5];
+      T b[5];
 #pragma unroll
-      for (int i = 0; i < 5; ++i) b[0][i] = 0.0;
-      sym_mv<1, 0, 0, 1, false>(Uf, tg, &a2[0], b, (T*)nullptr);
-      sym_mv<0, 1, 0, 1, false>(Uf, tg, &a2[1], b, (T*)nullptr);
-      sym_mv<0, 0, 1, 1, false>(Uf, tg, &a2[2], b, (T*)nullptr);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) b[0][i] = -b[0][i];
-      micro_slope(U, V, Ww, lam, fc.N, b[0], A[0]);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) dtW[i] = rho * b[0][i];
+      for (int i = 0; i < 5; ++i) {
+        dtW[i] = park.get(15 + i);
+        b[i] = dtW[i] * ir;
+      }
+      micro_slope(U, V, Ww, lam, fc.N, b, A[0]);  // A = M^{-1}(-<(a.u) psi>) (R16)
     }
     T Uh[7];
     half_moments(U, lam, sgn, Uh);
