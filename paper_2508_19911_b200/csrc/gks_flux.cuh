@@ -53,20 +53,6 @@ HD void half_moments(T U, T lam, double side, T* M) {
   for (int k = 0; k < 5; ++k) M[k + 2] = U * M[k + 1] + (k + 1) * r * M[k];
 }
 
-// micro-slope: the unique a = sum_j a_j psi_j with <a psi>_full = b, closed form for a
-// Maxwellian (U, V, W, lam) with N internal degrees of freedom
-template <typename T>
-HD void micro_slope(T U, T V, T W, T lam, double N, const T* b, T* a) {
-  const T uu = U * U + V * V + W * W;
-  const T K3 = (N + 3.0) / (2.0 * lam);
-  a[4] = (4.0 * lam * lam / (N + 3.0)) * (2.0 * b[4] - 2.0 * (U * b[1] + V * b[2] + W * b[3]) + (uu - K3) * b[0]);
-  const T tl = 2.0 * lam;
-  a[1] = tl * (b[1] - U * b[0]) - U * a[4];
-  a[2] = tl * (b[2] - V * b[0]) - V * a[4];
-  a[3] = tl * (b[3] - W * b[0]) - W * a[4];
-  a[0] = b[0] - U * a[1] - V * a[2] - W * a[3] - 0.5 * a[4] * (uu + K3);
-}
-
 // outputs of one Gauss point, normal frame
 template <typename T>
 struct GPOutT {
@@ -76,101 +62,108 @@ struct GPOutT {
 typedef GPOutT<double> GPOut;
 
 // ---------------------------------------------------------------------------
-// Tangential moment table of a Maxwellian: t(a,b,c) = <v^a w^b eta^c>, eta = v^2 + w^2 + xi^2
-// (v, w and xi are full-range Gaussians, so every psi_i psi_j moment factorises into a
-// normal-velocity moment U_k times one of these 19 numbers).
+// Half-range moment vectors and their directional derivatives.
+// c_X = <X psi> for X = u^p v^q w^r (q + r <= 1), psi = (1, u, v, w, (u^2 + eta)/2), eta =
+// v^2 + w^2 + xi^2, of a Maxwellian restricted to u > 0 or u < 0: the normal factor is a
+// half-range moment M_k = <u^k>, the transverse factor one of 8 full-Gaussian expectations.
+// Because the micro-slope of a perturbation dW is the first-order expansion of the Maxwellian
+// on any fixed velocity domain, rho <X a psi>_half = D[rho c_X](W) dW: every half-range term
+// of Eq. (flux) with a micro-slope is a directional derivative of rho c_X (no 5x5 solves).
 // ---------------------------------------------------------------------------
 template <typename T>
-struct Tang {
-  T v1, w1, e1, v2, vw, w2, ve, we, e2, v3, v2w, vw2, v2e, vwe, ve2, w3, w2e, we2;
+struct Tg {
+  T V, W, V2, W2, VW, e1, ve, we;  // <v>, <w>, <v^2>, <w^2>, <vw>, <eta>, <v eta>, <w eta>
 };
 
 template <typename T>
-HD void tang_table(T V, T W, T lam, double N, Tang<T>& t) {
-  const T s = 0.5 / lam;  // variance 1/(2 lam)
-  // full 1-D moments
-  const T V2 = V * V + s, W2 = W * W + s;
-  const T V3 = V * V2 + 2.0 * s * V, W3 = W * W2 + 2.0 * s * W;
-  const T V4 = V * V3 + 3.0 * s * V2, W4 = W * W3 + 3.0 * s * W2;
-  const T V5 = V * V4 + 4.0 * s * V3, W5 = W * W4 + 4.0 * s * W3;
-  const T X1 = N * s, X2 = N * (N + 2.0) * s * s;  // <xi^2>, <xi^4>
-  t.v1 = V;
-  t.w1 = W;
-  t.v2 = V2;
-  t.w2 = W2;
-  t.vw = V * W;
-  t.v3 = V3;
-  t.w3 = W3;
-  t.v2w = V2 * W;
-  t.vw2 = V * W2;
-  t.e1 = V2 + W2 + X1;
-  t.ve = V3 + V * (W2 + X1);
-  t.we = W3 + W * (V2 + X1);
-  t.v2e = V4 + V2 * (W2 + X1);
-  t.vwe = W * V3 + V * W3 + t.vw * X1;
-  t.w2e = W4 + W2 * (V2 + X1);
-  t.e2 = V4 + W4 + X2 + 2.0 * (V2 * W2 + X1 * (V2 + W2));
-  t.ve2 = V5 + V * (W4 + X2) + 2.0 * (V3 * W2 + X1 * (V3 + V * W2));
-  t.we2 = W5 + W * (V4 + X2) + 2.0 * (W3 * V2 + X1 * (W3 + W * V2));
+HD void tg_value(T V, T W, T s, double N, Tg<T>& t) {
+  const T VV = V * V, WW = W * W;
+  const T Z = VV + WW + (4.0 + N) * s;
+  t.V = V;
+  t.W = W;
+  t.V2 = VV + s;
+  t.W2 = WW + s;
+  t.VW = V * W;
+  t.e1 = VV + WW + (2.0 + N) * s;
+  t.ve = V * Z;
+  t.we = W * Z;
 }
 
-// Entries of the symmetric moment matrix M_ij = <X psi_i psi_j>, X = u^p v^q w^r (q + r <= 1),
-// psi_4 = (u^2 + eta)/2; upper entries e = 0..14 in the order (00,01,02,03,04,11,12,13,14,22,
-// 23,24,33,34,44).  Entries are produced one at a time and applied to several vectors at
-// once (sym_mv), so a matrix never occupies 15 registers.
-__host__ __device__ constexpr int sym_i(int e) {
-  return e < 5 ? 0 : (e < 9 ? 1 : (e < 12 ? 2 : (e < 14 ? 3 : 4)));
-}
-__host__ __device__ constexpr int sym_j(int e) {
-  return e < 5 ? e : (e < 9 ? e - 4 : (e < 12 ? e - 7 : (e < 14 ? e - 9 : 4)));
+// derivative of the transverse expectations along (dV, dW, ds)
+template <typename T>
+HD void tg_deriv(T V, T W, T s, double N, T dV, T dW, T ds, Tg<T>& d) {
+  const T Z = V * V + W * W + (4.0 + N) * s;
+  const T dZ = 2.0 * (V * dV + W * dW) + (4.0 + N) * ds;
+  d.V = dV;
+  d.W = dW;
+  d.V2 = 2.0 * V * dV + ds;
+  d.W2 = 2.0 * W * dW + ds;
+  d.VW = V * dW + W * dV;
+  d.e1 = 2.0 * (V * dV + W * dW) + (2.0 + N) * ds;
+  d.ve = dV * Z + V * dZ;
+  d.we = dW * Z + W * dZ;
 }
 
+template <int q, int r, typename T>
+HD void tg_pick(const Tg<T>& t, T& g000, T& g100, T& g010, T& g001, bool deriv) {
+  if (q == 0 && r == 0) {
+    g000 = deriv ? T(0.0) : T(1.0);
+    g100 = t.V;
+    g010 = t.W;
+    g001 = t.e1;
+  } else if (q == 1) {
+    g000 = t.V;
+    g100 = t.V2;
+    g010 = t.VW;
+    g001 = t.ve;
+  } else {
+    g000 = t.W;
+    g100 = t.VW;
+    g010 = t.W2;
+    g001 = t.we;
+  }
+}
+
+// c += s * c_X (value)
+template <int p, int q, int r, typename T, typename S>
+HD void col_value(const T* M, const Tg<T>& t, S s, T* c) {
+  T g000, g100, g010, g001;
+  tg_pick<q, r>(t, g000, g100, g010, g001, false);
+  c[0] += s * (M[p] * g000);
+  c[1] += s * (M[p + 1] * g000);
+  c[2] += s * (M[p] * g100);
+  c[3] += s * (M[p] * g010);
+  c[4] += s * (0.5 * (M[p + 2] * g000 + M[p] * g001));
+}
+
+// c += rho dc_X + drho c_X: directional derivative of rho c_X
 template <int p, int q, int r, typename T>
-HD T sym_entry(int e, const T* U, const Tang<T>& t) {
-  // tangential factors g(a,b,c) = <v^(q+a) w^(r+b) eta^c> of this X
-  const T g000 = (q == 0 && r == 0) ? T(1.0) : (q == 1 ? t.v1 : t.w1);
-  const T g100 = (q == 0 && r == 0) ? t.v1 : (q == 1 ? t.v2 : t.vw);
-  const T g010 = (q == 0 && r == 0) ? t.w1 : (q == 1 ? t.vw : t.w2);
-  const T g001 = (q == 0 && r == 0) ? t.e1 : (q == 1 ? t.ve : t.we);
-  const T g200 = (q == 0 && r == 0) ? t.v2 : (q == 1 ? t.v3 : t.v2w);
-  const T g110 = (q == 0 && r == 0) ? t.vw : (q == 1 ? t.v2w : t.vw2);
-  const T g101 = (q == 0 && r == 0) ? t.ve : (q == 1 ? t.v2e : t.vwe);
-  const T g020 = (q == 0 && r == 0) ? t.w2 : (q == 1 ? t.vw2 : t.w3);
-  const T g011 = (q == 0 && r == 0) ? t.we : (q == 1 ? t.vwe : t.w2e);
-  const T g002 = (q == 0 && r == 0) ? t.e2 : (q == 1 ? t.ve2 : t.we2);
-  switch (e) {
-    case 0: return U[p] * g000;
-    case 1: return U[p + 1] * g000;
-    case 2: return U[p] * g100;
-    case 3: return U[p] * g010;
-    case 4: return 0.5 * (U[p + 2] * g000 + U[p] * g001);
-    case 5: return U[p + 2] * g000;
-    case 6: return U[p + 1] * g100;
-    case 7: return U[p + 1] * g010;
-    case 8: return 0.5 * (U[p + 3] * g000 + U[p + 1] * g001);
-    case 9: return U[p] * g200;
-    case 10: return U[p] * g110;
-    case 11: return 0.5 * (U[p + 2] * g100 + U[p] * g101);
-    case 12: return U[p] * g020;
-    case 13: return 0.5 * (U[p + 2] * g010 + U[p] * g011);
-    default: return 0.25 * (U[p + 4] * g000 + 2.0 * U[p + 2] * g001 + U[p] * g002);
-  }
+HD void col_deriv(const T* M, const T* dM, const Tg<T>& t, const Tg<T>& dt, T rho, T drho, T* c) {
+  T g000, g100, g010, g001, h000, h100, h010, h001;
+  tg_pick<q, r>(t, g000, g100, g010, g001, false);
+  tg_pick<q, r>(dt, h000, h100, h010, h001, true);
+  const T v0 = M[p] * g000, v1 = M[p + 1] * g000, v2 = M[p] * g100, v3 = M[p] * g010;
+  const T v4 = 0.5 * (M[p + 2] * g000 + M[p] * g001);
+  const T d0 = dM[p] * g000 + M[p] * h000;
+  const T d1 = dM[p + 1] * g000 + M[p + 1] * h000;
+  const T d2 = dM[p] * g100 + M[p] * h100;
+  const T d3 = dM[p] * g010 + M[p] * h010;
+  const T d4 = 0.5 * (dM[p + 2] * g000 + M[p + 2] * h000 + dM[p] * g001 + M[p] * h001);
+  c[0] += rho * d0 + drho * v0;
+  c[1] += rho * d1 + drho * v1;
+  c[2] += rho * d2 + drho * v2;
+  c[3] += rho * d3 + drho * v3;
+  c[4] += rho * d4 + drho * v4;
 }
 
-// out[v] += M a[v] for NV vectors; with COL0 also col0 += M e_0 (= <X psi>)
-template <int p, int q, int r, int NV, bool COL0, typename T>
-HD void sym_mv(const T* U, const Tang<T>& t, const T (*a)[5], T (*out)[5], T* col0) {
+// derivative of the normal moments M_0..M_4 along (dU, dlam):
+// dM_k/dU = 2 lam (M_{k+1} - U M_k), dM_k/dlam = s M_k - (M_{k+2} - 2 U M_{k+1} + U^2 M_k)
+template <typename T>
+HD void moments_deriv(const T* M, T U, T lam, T s, T dU, T dlam, T* dM) {
+  const T tl = 2.0 * lam * dU;
 #pragma unroll
-  for (int e = 0; e < 15; ++e) {
-    const int i = sym_i(e), j = sym_j(e);
-    const T m = sym_entry<p, q, r>(e, U, t);
-    if (COL0 && i == 0) col0[j] += m;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      out[v][i] += m * a[v][j];
-      if (i != j) out[v][j] += m * a[v][i];
-    }
-  }
+  for (int k = 0; k < 5; ++k)
+    dM[k] = tl * (M[k + 1] - U * M[k]) + dlam * (s * M[k] - (M[k + 2] - 2.0 * U * M[k + 1] + U * U * M[k]));
 }
 
 // heat-flux functional of a flux-moment vector about U0 (R20):
@@ -245,20 +238,23 @@ HD void jvp_flux2(T rho, T ir, const T* U, T p, T uu, double K5, double K7, cons
 
 // per-lane parking slots (shared memory on the device) for values that live across phases
 struct ParkDev {
-  double* base;  // base + slot * 128 + lane
-  __device__ __forceinline__ void put(int s, double v) const { base[s * 128] = v; }
-  __device__ __forceinline__ double get(int s) const { return base[s * 128]; }
+  double* a;  // slots 0..19: a + slot * 128 (+ lane)
+  double* b;  // slots 20..39: b + (slot - 20) * 128 (+ lane)
+  __device__ __forceinline__ double* at(int s) const { return s < 20 ? a + s * 128 : b + (s - 20) * 128; }
+  __device__ __forceinline__ void put(int s, double v) const { *at(s) = v; }
+  __device__ __forceinline__ double get(int s) const { return *at(s); }
   __device__ __forceinline__ void mark(int) const {}  // phase markers (used by the host flop count)
 };
 
 // ---------------------------------------------------------------------------
 // One side of the interface solver at one Gauss point (two cooperating lanes per Gauss
 // point: side 0 = left state restricted to u > 0, side 1 = right state restricted to u < 0).
-// Phases: (A1) own half-range contributions to W0 and dW0 -> exchange (lane xor 1) ->
-// (G) interface equilibrium g0, collision time and combined time coefficients, equilibrium
-// terms of Eq. (flux) folded into F^n, F_t^n, Q^n, Q_t^n and the heat-flux scalars ->
-// (A2) own compatibility coefficients A and own half-range flux/state terms -> exchange ->
-// Prandtl fix and own side relaxation.  Both lanes run the same instruction stream.
+// Phases: (S) all half-range terms of this side (W0 and dW0 parts, MF3..MF5, MQ4, MQ5), as
+// values and directional derivatives of half-range moment vectors -> one exchange (lane xor 1)
+// sums the two sides -> (G) interface equilibrium g0, collision time and combined time
+// coefficients, equilibrium terms as Jacobian-vector products, everything folded into F^n,
+// F_t^n, Q^n, Q_t^n and the heat-flux scalars -> Prandtl fix and own side relaxation.
+// Both lanes run the same instruction stream.
 // Inputs in the normal frame: W (5) conservative state of this side, dW[dir][var] physical
 // derivatives (dir 0 = normal).  Outputs (normal frame): side 0 holds Fn, Ft, QLn, QLt;
 // side 1 holds Fn, Ft and its QRn, QRt in the QLn/QLt slots.  Returns false if a state
@@ -269,73 +265,89 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
                       const P& park, GPOutT<T>& o) {
   const T gm1 = fc.gamma - 1.0;
   const double sgn = side == 0 ? 1.0 : -1.0;
-  // ---- (A1) primitives, moments and micro-slopes of this side (R15)
+  // ---- (S) this side: primitives, half-range moments, and all half-range terms of Eq. (flux)
   const T rho = W[0], ir = 1.0 / rho;
   const T U = W[1] * ir, V = W[2] * ir, Ww = W[3] * ir;
-  const T p = gm1 * (W[4] - 0.5 * rho * (U * U + V * V + Ww * Ww));
+  const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
+  const T p = gm1 * (W[4] - rho * uu2s);
   const bool ok = (rho > 0.0) && (p > 0.0);
   const T lam = ok ? T(0.5) * rho / p : T(1.0);
-  T a[3][5];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    T b[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) b[i] = dW[d][i] * ir;
-    micro_slope(U, V, Ww, lam, fc.N, b, a[d]);
-  }
-  T x1[21];
-  {
-    T Uh[7];
-    half_moments(U, lam, sgn, Uh);  // H(u) or 1-H(u)
-    Tang<T> tg;
-    tang_table(V, Ww, lam, fc.N, tg);
-    T dw0[3][5], w0[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      w0[i] = 0.0;
-      dw0[0][i] = dw0[1][i] = dw0[2][i] = 0.0;
-    }
-    sym_mv<0, 0, 0, 3, true>(Uh, tg, a, dw0, w0);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      x1[i] = rho * w0[i];  // W0 part (R13)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) x1[5 + 5 * d + i] = rho * dw0[d][i];  // dW0 part (R14)
-    }
-  }
-  x1[20] = p;
+  const T sv = 0.5 / lam;  // variance 1/(2 lam)
+  const T ip = ok ? T(1.0) / p : T(1.0);
+  const T Uv[3] = {U, V, Ww};
   // Euler time derivative of this side (R23): dW/dt = rho <A psi> = -sum_al DF_al(W) dW_al (full
-  // moments, compatibility R16), as Jacobian-vector products
+  // moments, compatibility R16) as Jacobian-vector products
+  T dtw[5] = {0, 0, 0, 0, 0};
   {
-    const T Uv[3] = {U, V, Ww};
-    const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
-    T dtw[5] = {0, 0, 0, 0, 0};
     const Dprim<T> q0 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[0]);
     jvp_flux<0>(rho, Uv, p, W[4], dW[0], q0, -1.0, dtw);
     const Dprim<T> q1 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[1]);
     jvp_flux<1>(rho, Uv, p, W[4], dW[1], q1, -1.0, dtw);
     const Dprim<T> q2 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[2]);
     jvp_flux<2>(rho, Uv, p, W[4], dW[2], q2, -1.0, dtw);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) park.put(15 + i, dtw[i]);
   }
-  // park what the own-side phase A2 needs (a, dW/dt): frees registers during the equilibrium phase
+  // x1: 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3 = rho <u psi>, 25-29 MF4 = rho <u (a.u) psi>,
+  // 30-34 MF5 = rho <u A psi>, 35-39 MQ4 = rho <(a.u) psi>, 40-44 MQ5 = rho <A psi>, 45 p (half ranges)
+  T x1[46];
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
+  for (int i = 0; i < 45; ++i) x1[i] = 0.0;
+  x1[45] = p;
+  {
+    T M[7];
+    half_moments(U, lam, sgn, M);  // H(u) or 1-H(u)
+    Tg<T> tg;
+    tg_value(V, Ww, sv, fc.N, tg);
+    col_value<0, 0, 0>(M, tg, rho, x1 + 0);
+    col_value<1, 0, 0>(M, tg, rho, x1 + 20);
+    // directional derivatives along dW_n, dW_t1, dW_t2 (micro-slopes a_al) and dW/dt (A)
 #pragma unroll
-    for (int i = 0; i < 5; ++i) park.put(5 * d + i, a[d][i]);
+    for (int dir = 0; dir < 4; ++dir) {
+      const T* d = dir < 3 ? dW[dir] : dtw;
+      const Dprim<T> q = dprim(ir, Uv, uu2s, fc.gamma - 1.0, d);
+      const T dlam = lam * (q.dr * ir - q.dp * ip);
+      const T ds = -2.0 * sv * sv * dlam;
+      T dM[5];
+      moments_deriv(M, U, lam, sv, q.du[0], dlam, dM);
+      Tg<T> dt;
+      tg_deriv(V, Ww, sv, fc.N, q.du[1], q.du[2], ds, dt);
+      if (dir == 0) {
+        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 5);
+        col_deriv<1, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 35);
+        col_deriv<2, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+      } else if (dir == 1) {
+        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 10);
+        col_deriv<0, 1, 0>(M, dM, tg, dt, rho, q.dr, x1 + 35);
+        col_deriv<1, 1, 0>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+      } else if (dir == 2) {
+        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 15);
+        col_deriv<0, 0, 1>(M, dM, tg, dt, rho, q.dr, x1 + 35);
+        col_deriv<1, 0, 1>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+      } else {
+        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 40);
+        col_deriv<1, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 30);
+      }
+    }
+  }
   // ---- exchange 1: W0, dW0 = sum of the two half-range contributions
   const bool ok_other = xchg.flag(ok);
   T other_p;
   {
 #pragma unroll
-    for (int i = 0; i < 21; ++i) {
+    for (int i = 0; i < 46; ++i) {
       const T y = xchg(x1[i]);
-      if (i < 20)
+      if (i < 45)
         x1[i] += y;
       else
         other_p = y;
     }
+  }
+  // park the summed half-range terms and this side's W, dW/dt until the final phase
+#pragma unroll
+  for (int i = 0; i < 25; ++i) park.put(i, x1[20 + i]);
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    park.put(25 + i, dtw[i]);
+    park.put(30 + i, W[i]);
   }
   bool good = ok && ok_other;
   park.mark(1);  // start of the equilibrium phase (identical in both lanes)
@@ -436,73 +448,33 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   park.mark(2);
   park.mark(3);
   park.mark(4);
-  // ---- (A2) own side: compatibility coefficients A (R16), Euler time derivative (R23),
-  // half-range flux and state terms of this side
-  T sacc[22];
-  T dtW[5];
+  // ---- half-range terms of both sides (summed by the exchange): k = 3, 4, 5 of Eq. (flux)
+  T dtW[5], Wown[5];
   {
-    T a2[3][5];
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) a2[d][i] = park.get(5 * d + i);
-    Tang<T> tg;
-    tang_table(V, Ww, lam, fc.N, tg);
-    T A[1][5];
-    {
-      T b[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        dtW[i] = park.get(15 + i);
-        b[i] = dtW[i] * ir;
-      }
-      micro_slope(U, V, Ww, lam, fc.N, b, A[0]);  // A = M^{-1}(-<(a.u) psi>) (R16)
-    }
-    T Uh[7];
-    half_moments(U, lam, sgn, Uh);
-    // MF3 = <u psi>, MF5 = <u A psi>, MQ4 = <(a.u) psi>, MF4 = <u (a.u) psi>, MQ5 = <A psi> (x rho)
-    T MF3[5], MF5[1][5], MQ4[1][5], MF4[1][5], MQ5[1][5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) MF3[i] = MF5[0][i] = MQ4[0][i] = MF4[0][i] = MQ5[0][i] = 0.0;
-    {
-      T vv[2][5], oo[2][5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        vv[0][i] = A[0][i];
-        vv[1][i] = a2[0][i];
-        oo[0][i] = oo[1][i] = 0.0;
-      }
-      sym_mv<1, 0, 0, 2, true>(Uh, tg, vv, oo, MF3);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        MF5[0][i] = oo[0][i];
-        MQ4[0][i] = oo[1][i];
-      }
-    }
-    sym_mv<0, 1, 0, 1, false>(Uh, tg, &a2[1], MQ4, (T*)nullptr);
-    sym_mv<0, 0, 1, 1, false>(Uh, tg, &a2[2], MQ4, (T*)nullptr);
-    sym_mv<2, 0, 0, 1, false>(Uh, tg, &a2[0], MF4, (T*)nullptr);
-    sym_mv<1, 1, 0, 1, false>(Uh, tg, &a2[1], MF4, (T*)nullptr);
-    sym_mv<1, 0, 1, 1, false>(Uh, tg, &a2[2], MF4, (T*)nullptr);
-    sym_mv<0, 0, 0, 1, false>(Uh, tg, A, MQ5, (T*)nullptr);
-    const T s3 = rho * qF(MF3, U0, V0, Ww0, uu2);
-    const T s4 = rho * (qF(MF4[0], U0, V0, Ww0, uu2) - U0 * qF(MQ4[0], U0, V0, Ww0, uu2));
-    const T s5 = rho * (qF(MF5[0], U0, V0, Ww0, uu2) - U0 * qF(MQ5[0], U0, V0, Ww0, uu2));
+    T v3[5], v4[5], v5[5], q4[5], q5[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      const T mf3 = rho * MF3[i], mf4 = rho * MF4[0][i], mf5 = rho * MF5[0][i];
-      const T mq4 = rho * MQ4[0][i], mq5 = rho * MQ5[0][i];
-      sacc[i] = al[3] * mf3 + al[4] * mf4 + al[5] * mf5;
-      sacc[5 + i] = be[3] * mf3 + be[4] * mf4 + be[5] * mf5;
-      sacc[10 + i] = al[4] * mq4 + al[5] * mq5;
-      sacc[15 + i] = be[4] * mq4 + be[5] * mq5;
+      v3[i] = park.get(i);
+      v4[i] = park.get(5 + i);
+      v5[i] = park.get(10 + i);
+      q4[i] = park.get(15 + i);
+      q5[i] = park.get(20 + i);
+      dtW[i] = park.get(25 + i);
+      Wown[i] = park.get(30 + i);
     }
-    sacc[20] = al[3] * s3 + al[4] * s4 + al[5] * s5;
-    sacc[21] = be[3] * s3 + be[4] * s4 + be[5] * s5;
-  }
-  // ---- exchange 2: add the other side's half-range terms
+    const T s3 = qF(v3, U0, V0, Ww0, uu2);
+    const T s4 = qF(v4, U0, V0, Ww0, uu2) - U0 * qF(q4, U0, V0, Ww0, uu2);
+    const T s5 = qF(v5, U0, V0, Ww0, uu2) - U0 * qF(q5, U0, V0, Ww0, uu2);
 #pragma unroll
-  for (int i = 0; i < 22; ++i) acc[i] += sacc[i] + xchg(sacc[i]);
+    for (int i = 0; i < 5; ++i) {
+      acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
+      acc[5 + i] += be[3] * v3[i] + be[4] * v4[i] + be[5] * v5[i];
+      acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
+      acc[15 + i] += be[4] * q4[i] + be[5] * q5[i];
+    }
+    acc[20] += al[3] * s3 + al[4] * s4 + al[5] * s5;
+    acc[21] += be[3] * s3 + be[4] * s4 + be[5] * s5;
+  }
   // ---- Prandtl fix (R20) and outputs
   if (fc.Pr != 1.0) {
     const double pf = 1.0 / fc.Pr - 1.0;
@@ -521,7 +493,7 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     const T w = 1.0 - ee;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      o.QLn[i] = w * acc[10 + i] + ee * W[i];
+      o.QLn[i] = w * acc[10 + i] + ee * Wown[i];
       o.QLt[i] = w * acc[15 + i] + ee * dtW[i];
     }
   }

@@ -357,9 +357,9 @@ struct FluxTile {
   static constexpr int NQ = DIM + 1;                         // value + DIM derivatives
   static constexpr int TS = NB + 1;                          // padded per-(side, quantity) row (no bank conflicts)
   static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
-  static constexpr size_t smem_bytes() {
-    return sizeof(double) * ((size_t)NFLD * NT + TAB + 20 * 128);
-  }
+  // the tile region is reused for parking slots 20..39 after the evaluation
+  static constexpr int TILE = NFLD * NT > 20 * 128 ? NFLD * NT : 20 * 128;
+  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128); }
 };
 
 template <int DIM, int AX, bool COMPACT, bool BOX>
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   constexpr int NR = COMPACT ? 20 : 10;  // values each lane reduces over the Gauss points
   extern __shared__ double smem[];
   double* tile = smem;                            // [NFLD][NT]: reconstruction fields, then Q
-  double* tab = smem + FT::NFLD * NT;             // [side][gp][val, d0, d1, d2][NB]
+  double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
   double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
   if (err->code) return;
   const int fn0 = c_geo.fn[AX][0];
@@ -518,8 +518,11 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       dn[d][4] = dW[pp[d]][4];
     }
   }
+  // the tile is dead from here on: its space (with the scratch) holds the per-lane parking slots
+  __syncthreads();
   GPOut o;
-  const bool ok = gks_flux_side<COMPACT>(side, wn, dn, dt, c_fc, XchgDev(), ParkDev{scratch + lane}, o);
+  const bool ok =
+      gks_flux_side<COMPACT>(side, wn, dn, dt, c_fc, XchgDev(), ParkDev{scratch + lane, smem + lane}, o);
   if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
   // back to the global frame, weight 1/NG; side 0: Fn Ft (QLn QLt), side 1: QRn QRt
   double out[NR];
