@@ -344,13 +344,18 @@ struct XchgDev {
 #define CGKS_FLUX_MINB 3
 #endif
 
-// flux kernel geometry: 128 threads = FPB faces along x of one (j, k) row, 2*NG lanes per face
+// flux kernel geometry: 128 threads = FPB faces, 2*NG lanes per face.  x-faces: a run of FPB
+// faces along x (tile: FPB + 1 cells of one row).  y-/z-faces: a patch of FX faces along x by
+// FY faces along the normal axis (tile: FX x (FY + 1) cells, 32-byte x-runs), so each staged
+// cell serves FY / (FY + 1) faces instead of 1/2.
 template <int DIM, int AX, bool COMPACT>
 struct FluxTile {
   static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
   static constexpr int LPF = 2 * NG;                         // lanes per face
   static constexpr int FPB = 128 / LPF;                      // faces per block
-  static constexpr int NT = AX == 0 ? FPB + 1 : 2 * FPB;     // tile cells
+  static constexpr int FY = AX == 0 ? 1 : 4;                 // faces along the normal axis
+  static constexpr int FX = FPB / FY;                        // faces along x
+  static constexpr int NT = AX == 0 ? FPB + 1 : FX * (FY + 1);  // tile cells
   static constexpr int NB = Sten<DIM>::NB;
   static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
   static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
@@ -377,26 +382,37 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
   double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
   if (err->code) return;
+  constexpr int FX = FT::FX, FY = FT::FY;
   const int fn0 = c_geo.fn[AX][0];
-  const int i0 = blockIdx.x * FPB, j = blockIdx.y, k = blockIdx.z;
-  // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous rows).
+  // block origin: face (i0, j0, k0); y-/z-faces cover FY faces along their normal axis
+  const int i0 = blockIdx.x * FX;
+  const int j0 = AX == 1 ? blockIdx.y * FY : blockIdx.y;
+  const int k0 = AX == 2 ? blockIdx.z * FY : blockIdx.z;
+  // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous runs).
   // Each thread serves one tile cell (index math once) and a strided subset of its fields.
   {
     constexpr int TPC = 128 / NT;  // threads per cell
     const int c = threadIdx.x % NT, fsub = threadIdx.x / NT;
     if (fsub < TPC) {
-      int ci, cj = j, ck = k;
+      int ci, cj = j0, ck = k0;
       if (AX == 0) {
         ci = i0 - 1 + c;
       } else {
-        ci = i0 + (c < FPB ? c : c - FPB);
-        if (c < FPB) {
-          if (AX == 1) cj -= 1;
-          if (AX == 2) ck -= 1;
-        }
+        ci = i0 + c % FX;
+        if (AX == 1) cj += c / FX - 1;
+        if (AX == 2) ck += c / FX - 1;
       }
-      const int imax = c_geo.n[0] - 1 + (c_geo.bounded[0] ? 1 : 0);  // clamp the ragged row tail
+      // clamp the ragged tails (those cells only feed faces that are not stored)
+      const int imax = c_geo.n[0] - 1 + (c_geo.bounded[0] ? 1 : 0);
       if (ci > imax) ci = imax;
+      if (AX == 1) {
+        const int jmax = c_geo.n[1] - 1 + (c_geo.bounded[1] ? 1 : 0);
+        if (cj > jmax) cj = jmax;
+      }
+      if (AX == 2) {
+        const int kmax = c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0);
+        if (ck > kmax) ck = kmax;
+      }
       const double* rb = rec + eidx(FT::NREC, 0, ci, cj, ck);
       const long long st = c_geo.eplane;
       // asynchronous global -> shared copies (LDGSTS): all in flight at once
@@ -419,10 +435,11 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const int side = lane & 1;
   const int gp = (lane >> 1) % NG;
   const int fl = lane / FT::LPF;  // face within the block
-  const int i = i0 + fl;
-  const bool valid = i < fn0;
+  const int fx = fl % FX, fy = fl / FX;
+  const int i = i0 + fx, j = AX == 1 ? j0 + fy : j0, k = AX == 2 ? k0 + fy : k0;
+  const bool valid = i < fn0 && (AX != 1 || j < c_geo.fn[1][1]) && (AX != 2 || k < c_geo.fn[2][2]);
   // tile column of this lane's cell
-  const int c = AX == 0 ? fl + side : (side ? FPB + fl : fl);
+  const int c = AX == 0 ? fl + side : (fy + side) * FX + fx;
   const double* tc = tile + c;
 
   // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)

@@ -86,7 +86,9 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
     attr = true;
   }
-  const dim3 grid((unsigned)((a.fn[AX][0] + FT::FPB - 1) / FT::FPB), (unsigned)a.fn[AX][1], (unsigned)a.fn[AX][2]);
+  const unsigned gy = (unsigned)(AX == 1 ? (a.fn[AX][1] + FT::FY - 1) / FT::FY : a.fn[AX][1]);
+  const unsigned gz = (unsigned)(AX == 2 ? (a.fn[AX][2] + FT::FY - 1) / FT::FY : a.fn[AX][2]);
+  const dim3 grid((unsigned)((a.fn[AX][0] + FT::FX - 1) / FT::FX), gy, gz);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (env.prof) {
     cudaEventCreate(&e0);
