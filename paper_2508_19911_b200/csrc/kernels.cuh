@@ -150,7 +150,8 @@ struct ReconTile {
   static constexpr int HX = TX + 2, HY = DIM >= 2 ? TY + 2 : 1, HZ = DIM == 3 ? TZ + 2 : 1;
   static constexpr int HALO = HX * HY * HZ;
   static constexpr int NFS = 1 + DIM;  // staged fields per component: Q_v, dQ_v/dx_a
-  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO; }
+  // two component buffers + the staging offset table (ReconStageMap)
+  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO + sizeof(unsigned) * NFS * HALO; }
 };
 
 template <int DIM>
@@ -168,21 +169,43 @@ struct Recon5TileLoader {
   }
 };
 
+// Halo-tile staging of the reconstruction.  Each tile element's global offset for component
+// v = 0 (index arithmetic, periodic wrap) is computed once per block into a shared table, so
+// staging component v is one shared load, one add and one cp.async per element: field f of
+// component v sits at offset(f, v = 0) + v * plane in the [z][field][y][x] layout.
+template <int DIM>
+struct ReconStageMap {
+  using RT = ReconTile<DIM>;
+  static constexpr int NEL = RT::NFS * RT::HALO;
+  unsigned* off;  // [NEL] in shared memory
+  __device__ __forceinline__ void init(int x0, int y0, int z0) const {
+    for (int idx = threadIdx.x; idx < NEL; idx += RT::NTH) {
+      const int f = idx / RT::HALO, h = idx % RT::HALO;
+      const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
+      const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
+      const int fld = f == 0 ? 0 : 5 + (f - 1) * 5;
+      off[idx] = (unsigned)sidx(20, fld, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk));
+    }
+  }
+};
+
 // stage fields (Q_v, G_{a,v}) of the block's halo tile into buf
 template <int DIM, bool BOX>
 __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double* buf, int v, int x0, int y0,
-                                            int z0) {
+                                            int z0, const ReconStageMap<DIM>& map) {
   using RT = ReconTile<DIM>;
-  for (int idx = threadIdx.x; idx < RT::NFS * RT::HALO; idx += RT::NTH) {
-    const int f = idx / RT::HALO, h = idx % RT::HALO;
-    const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
-    const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
-    const int fld = f == 0 ? v : 5 + (f - 1) * 5 + v;
-    if (BOX) {
+  if (BOX) {
+    for (int idx = threadIdx.x; idx < RT::NFS * RT::HALO; idx += RT::NTH) {
+      const int f = idx / RT::HALO, h = idx % RT::HALO;
+      const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
+      const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
+      const int fld = f == 0 ? v : 5 + (f - 1) * 5 + v;
       buf[idx] = ld_state<true>(U, 20, fld, i, j, kk);
-    } else {
-      cp_async8(buf + idx, U + sidx(20, fld, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk)));
     }
+  } else {
+    const double* Uv = U + (long long)v * c_geo.plane;
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < ReconStageMap<DIM>::NEL; idx += RT::NTH) cp_async8(buf + idx, Uv + map.off[idx]);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -205,12 +228,20 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
   const bool valid = (i < c_geo.elo[0] + c_geo.en[0]) && (j < c_geo.elo[1] + c_geo.en[1]) &&
                      (k < c_geo.elo[2] + c_geo.en[2]);
   const int own = (DIM == 3 ? (tz + 1) * RT::HX * RT::HY : 0) + (DIM >= 2 ? (ty + 1) * RT::HX : 0) + tx + 1;
-  recon_stage<DIM, BOX>(U, rsm, 0, x0, y0, z0);
+  const ReconStageMap<DIM> map{reinterpret_cast<unsigned*>(rsm + 2 * RT::NFS * RT::HALO)};
+  if (!BOX) {
+    map.init(x0, y0, z0);
+    __syncthreads();
+  }
+  // coefficient q of component v at cb[(q * 5 + v) * eplane]
+  double* cb = coef + (valid ? eidx(NCO, 0, i, j, k) : 0);
+  const long long ep = c_geo.eplane;
+  recon_stage<DIM, BOX>(U, rsm, 0, x0, y0, z0, map);
 #pragma unroll 1
   for (int v = 0; v < 5; ++v) {
     double* cur = rsm + (v & 1) * RT::NFS * RT::HALO;
     if (v < 4) {
-      recon_stage<DIM, BOX>(U, rsm + ((v + 1) & 1) * RT::NFS * RT::HALO, v + 1, x0, y0, z0);
+      recon_stage<DIM, BOX>(U, rsm + ((v + 1) & 1) * RT::NFS * RT::HALO, v + 1, x0, y0, z0, map);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -271,8 +302,12 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
       for (int a = 0; a < DIM; ++a) acc[a] = fma(1.0 - chi, lin[a], acc[a]);
     }
     if (valid) {
+      double* cv = cb + v * ep;
 #pragma unroll
-      for (int q = 0; q < S::NB; ++q) coef[eidx(NCO, q * 5 + v, i, j, k)] = acc[q];
+      for (int q = 0; q < S::NB; ++q) {
+        *cv = acc[q];  // running pointer: no per-coefficient index arithmetic
+        cv += 5 * ep;
+      }
     }
     __syncthreads();  // this buffer is refilled by the prefetch two components ahead
   }
