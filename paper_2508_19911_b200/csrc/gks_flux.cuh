@@ -124,36 +124,62 @@ HD void tg_pick(const Tg<T>& t, T& g000, T& g100, T& g010, T& g001, bool deriv) 
   }
 }
 
-// c += s * c_X (value)
-template <int p, int q, int r, typename T, typename S>
-HD void col_value(const T* M, const Tg<T>& t, S s, T* c) {
+// rho-weighted transverse factors of one pick (q, r): value G_j = rho g_j, derivative
+// H_j = rho h_j + drho g_j (j = 000, 100, 010, 001), with the halves of the 000 and 001 entries
+// that enter the energy component (psi_4 = (u^2 + eta) / 2)
+template <typename T>
+struct RW {
+  T x0, x1, x2, x3, x0h, x3h;
+};
+
+template <int q, int r, typename T>
+HD RW<T> rw_value(const Tg<T>& t, T rho) {
   T g000, g100, g010, g001;
   tg_pick<q, r>(t, g000, g100, g010, g001, false);
-  c[0] += s * (M[p] * g000);
-  c[1] += s * (M[p + 1] * g000);
-  c[2] += s * (M[p] * g100);
-  c[3] += s * (M[p] * g010);
-  c[4] += s * (0.5 * (M[p + 2] * g000 + M[p] * g001));
+  RW<T> w;
+  w.x0 = (q == 0 && r == 0) ? rho : rho * g000;
+  w.x1 = rho * g100;
+  w.x2 = rho * g010;
+  w.x3 = rho * g001;
+  w.x0h = 0.5 * w.x0;
+  w.x3h = 0.5 * w.x3;
+  return w;
 }
 
-// c += rho dc_X + drho c_X: directional derivative of rho c_X
-template <int p, int q, int r, typename T>
-HD void col_deriv(const T* M, const T* dM, const Tg<T>& t, const Tg<T>& dt, T rho, T drho, T* c) {
+template <int q, int r, typename T>
+HD RW<T> rw_deriv(const Tg<T>& t, const Tg<T>& dt, T rho, T drho) {
   T g000, g100, g010, g001, h000, h100, h010, h001;
   tg_pick<q, r>(t, g000, g100, g010, g001, false);
   tg_pick<q, r>(dt, h000, h100, h010, h001, true);
-  const T v0 = M[p] * g000, v1 = M[p + 1] * g000, v2 = M[p] * g100, v3 = M[p] * g010;
-  const T v4 = 0.5 * (M[p + 2] * g000 + M[p] * g001);
-  const T d0 = dM[p] * g000 + M[p] * h000;
-  const T d1 = dM[p + 1] * g000 + M[p + 1] * h000;
-  const T d2 = dM[p] * g100 + M[p] * h100;
-  const T d3 = dM[p] * g010 + M[p] * h010;
-  const T d4 = 0.5 * (dM[p + 2] * g000 + M[p + 2] * h000 + dM[p] * g001 + M[p] * h001);
-  c[0] += rho * d0 + drho * v0;
-  c[1] += rho * d1 + drho * v1;
-  c[2] += rho * d2 + drho * v2;
-  c[3] += rho * d3 + drho * v3;
-  c[4] += rho * d4 + drho * v4;
+  RW<T> w;
+  w.x0 = (q == 0 && r == 0) ? drho : rho * h000 + drho * g000;
+  w.x1 = rho * h100 + drho * g100;
+  w.x2 = rho * h010 + drho * g010;
+  w.x3 = rho * h001 + drho * g001;
+  w.x0h = 0.5 * w.x0;
+  w.x3h = 0.5 * w.x3;
+  return w;
+}
+
+// c += rho c_X (value), X = u^p v^q w^r with G = rw_value<q, r>
+template <int p, typename T>
+HD void col_value(const T* M, const RW<T>& G, T* c) {
+  c[0] += M[p] * G.x0;
+  c[1] += M[p + 1] * G.x0;
+  c[2] += M[p] * G.x1;
+  c[3] += M[p] * G.x2;
+  c[4] += M[p + 2] * G.x0h + M[p] * G.x3h;
+}
+
+// c += D[rho c_X] = rho dc_X + drho c_X: directional derivative, with the normal moments' derivative
+// dM and the pick's rho-weighted value G and derivative H
+template <int p, typename T>
+HD void col_deriv(const T* M, const T* dM, const RW<T>& G, const RW<T>& H, T* c) {
+  c[0] += dM[p] * G.x0 + M[p] * H.x0;
+  c[1] += dM[p + 1] * G.x0 + M[p + 1] * H.x0;
+  c[2] += dM[p] * G.x1 + M[p] * H.x1;
+  c[3] += dM[p] * G.x2 + M[p] * H.x2;
+  c[4] += dM[p + 2] * G.x0h + M[p + 2] * H.x0h + dM[p] * G.x3h + M[p] * H.x3h;
 }
 
 // derivative of the normal moments M_0..M_4 along (dU, dlam):
@@ -297,8 +323,9 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
     half_moments(U, lam, sgn, M);  // H(u) or 1-H(u)
     Tg<T> tg;
     tg_value(V, Ww, sv, fc.N, tg);
-    col_value<0, 0, 0>(M, tg, rho, x1 + 0);
-    col_value<1, 0, 0>(M, tg, rho, x1 + 20);
+    const RW<T> G00 = rw_value<0, 0>(tg, rho), G10 = rw_value<1, 0>(tg, rho), G01 = rw_value<0, 1>(tg, rho);
+    col_value<0>(M, G00, x1 + 0);
+    col_value<1>(M, G00, x1 + 20);
     // directional derivatives along dW_n, dW_t1, dW_t2 (micro-slopes a_al) and dW/dt (A)
 #pragma unroll
     for (int dir = 0; dir < 4; ++dir) {
@@ -310,21 +337,24 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
       moments_deriv(M, U, lam, sv, q.du[0], dlam, dM);
       Tg<T> dt;
       tg_deriv(V, Ww, sv, fc.N, q.du[1], q.du[2], ds, dt);
+      const RW<T> H00 = rw_deriv<0, 0>(tg, dt, rho, q.dr);
       if (dir == 0) {
-        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 5);
-        col_deriv<1, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 35);
-        col_deriv<2, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+        col_deriv<0>(M, dM, G00, H00, x1 + 5);
+        col_deriv<1>(M, dM, G00, H00, x1 + 35);
+        col_deriv<2>(M, dM, G00, H00, x1 + 25);
       } else if (dir == 1) {
-        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 10);
-        col_deriv<0, 1, 0>(M, dM, tg, dt, rho, q.dr, x1 + 35);
-        col_deriv<1, 1, 0>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+        const RW<T> H10 = rw_deriv<1, 0>(tg, dt, rho, q.dr);
+        col_deriv<0>(M, dM, G00, H00, x1 + 10);
+        col_deriv<0>(M, dM, G10, H10, x1 + 35);
+        col_deriv<1>(M, dM, G10, H10, x1 + 25);
       } else if (dir == 2) {
-        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 15);
-        col_deriv<0, 0, 1>(M, dM, tg, dt, rho, q.dr, x1 + 35);
-        col_deriv<1, 0, 1>(M, dM, tg, dt, rho, q.dr, x1 + 25);
+        const RW<T> H01 = rw_deriv<0, 1>(tg, dt, rho, q.dr);
+        col_deriv<0>(M, dM, G00, H00, x1 + 15);
+        col_deriv<0>(M, dM, G01, H01, x1 + 35);
+        col_deriv<1>(M, dM, G01, H01, x1 + 25);
       } else {
-        col_deriv<0, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 40);
-        col_deriv<1, 0, 0>(M, dM, tg, dt, rho, q.dr, x1 + 30);
+        col_deriv<0>(M, dM, G00, H00, x1 + 40);
+        col_deriv<1>(M, dM, G00, H00, x1 + 30);
       }
     }
   }
