@@ -388,6 +388,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   ctx->fc.N = (5.0 - 3.0 * gamma) / (gamma - 1.0);
   ctx->fc.mu = mu;
   ctx->fc.Pr = Pr;
+  ctx->fc.pfix = 1.0 / Pr - 1.0;  // Prandtl fix factor (R20)
   ctx->fc.tau_eps = scheme->tau_eps;
   ctx->fc.tau_C = scheme->tau_C;
   ctx->fc.relax_C = scheme->relax_C;

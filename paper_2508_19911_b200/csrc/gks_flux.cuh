@@ -30,21 +30,12 @@ HD double rsqrt_(double x) {
 
 struct FluxConst {
   double gamma, N, mu, Pr, tau_eps, tau_C, relax_C;
+  double pfix;  // 1/Pr - 1
 };
-
-template <typename T>
-HD void full_moments(T U, T lam, T* M) {
-  const T r = 0.5 / lam;
-  M[0] = 1.0;
-  M[1] = U;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) M[k + 2] = U * M[k + 1] + (k + 1) * r * M[k];
-}
 
 // half-range moments over u>0 (side=+1) or u<0 (side=-1)
 template <typename T>
-HD void half_moments(T U, T lam, double side, T* M) {
-  const T r = 0.5 / lam;
+HD void half_moments(T U, T lam, T r, double side, T* M) {  // r = 1/(2 lam)
   const T sl = sqrt(lam);
   const T g = 0.5 * exp(-lam * U * U) * rsqrt_(lam * 3.14159265358979323846);
   M[0] = 0.5 * erfc(-side * sl * U);
@@ -297,9 +288,9 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
   const T p = gm1 * (W[4] - rho * uu2s);
   const bool ok = (rho > 0.0) && (p > 0.0);
-  const T lam = ok ? T(0.5) * rho / p : T(1.0);
-  const T sv = 0.5 / lam;  // variance 1/(2 lam)
   const T ip = ok ? T(1.0) / p : T(1.0);
+  const T lam = ok ? T(0.5) * rho * ip : T(1.0);
+  const T sv = ok ? p * ir : T(0.5);  // variance 1/(2 lam)
   const T Uv[3] = {U, V, Ww};
   // Euler time derivative of this side (R23): dW/dt = rho <A psi> = -sum_al DF_al(W) dW_al (full
   // moments, compatibility R16) as Jacobian-vector products
@@ -320,7 +311,7 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   x1[45] = p;
   {
     T M[7];
-    half_moments(U, lam, sgn, M);  // H(u) or 1-H(u)
+    half_moments(U, lam, sv, sgn, M);  // H(u) or 1-H(u)
     Tg<T> tg;
     tg_value(V, Ww, sv, fc.N, tg);
     const RW<T> G00 = rw_value<0, 0>(tg, rho), G10 = rw_value<1, 0>(tg, rho), G01 = rw_value<0, 1>(tg, rho);
@@ -396,8 +387,8 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   T al[6], be[6];
   {
     const T idt = 1.0 / dt;
-    const T E2 = exp(-0.5 * dt / tau);
-    const T m2 = -expm1(-0.5 * dt / tau);
+    const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation
+    const T E2 = 1.0 - m2;
     const T c3 = tau * m2 * (3.0 - E2) * idt;
     const T qq = 4.0 * tau * m2 * m2 * idt * idt;
     al[0] = 1.0 - c3;
@@ -507,7 +498,7 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   }
   // ---- Prandtl fix (R20) and outputs
   if (fc.Pr != 1.0) {
-    const double pf = 1.0 / fc.Pr - 1.0;
+    const double pf = fc.pfix;
     acc[4] += pf * acc[20];
     acc[9] += pf * acc[21];
   }
