@@ -896,9 +896,9 @@ static double flux_point_flops(const FluxConst& f, bool compact) {
     double marks[5] = {0, 0, 0, 0, 0};
     fc::tally() = fc::Tally();
     if (compact)
-      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots, marks}, o);
+      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
     else
-      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), f, XchgMirror(), ParkHost{slots, marks}, o);
+      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
     total += fc::tally().flops - (side == 1 ? (marks[2] - marks[1]) + (marks[4] - marks[3]) : 0.0);
   }
   return total;

@@ -36,8 +36,9 @@ struct FluxConst {
 // half-range moments over u>0 (side=+1) or u<0 (side=-1)
 template <typename T>
 HD void half_moments(T U, T lam, T r, double side, T* M) {  // r = 1/(2 lam)
-  const T sl = sqrt(lam);
-  const T g = 0.5 * exp(-lam * U * U) * rsqrt_(lam * 3.14159265358979323846);
+  const T rl = rsqrt_(lam);
+  const T sl = lam * rl;  // sqrt(lam)
+  const T g = (0.5 * 0.56418958354775628695) * exp(-lam * U * U) * rl;  // exp(-lam U^2) / (2 sqrt(pi lam))
   M[0] = 0.5 * erfc(-side * sl * U);
   M[1] = U * M[0] + side * g;
 #pragma unroll
@@ -278,7 +279,7 @@ struct ParkDev {
 // (own, other, or the equilibrium) is not positive.
 // ---------------------------------------------------------------------------
 template <bool COMPACT, typename T, typename X, typename P>
-HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxConst& fc, const X& xchg,
+HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const FluxConst& fc, const X& xchg,
                       const P& park, GPOutT<T>& o) {
   const T gm1 = fc.gamma - 1.0;
   const double sgn = side == 0 ? 1.0 : -1.0;
@@ -382,11 +383,12 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, const FluxCo
   const T l0 = good ? T(0.5) * r0 / p0 : T(1.0);
   // collision time (R17) and combined time coefficients:
   // F^n = sum alpha_k MF_k, F_t^n = sum beta_k MF_k (E2 = e^{-dt/(2tau)}, tau = 0 -> Euler limit)
-  const T jump = fabs((pL - pR) / (pL + pR));
-  const T tau = (fc.mu > 0.0) ? (fc.mu / p0 + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
+  // one reciprocal serves 1/p0 and 1/(pL + pR)
+  const T rpp = 1.0 / (p0 * (pL + pR));
+  const T jump = fabs(pL - pR) * (p0 * rpp);
+  const T tau = (fc.mu > 0.0) ? (fc.mu * ((pL + pR) * rpp) + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
   T al[6], be[6];
   {
-    const T idt = 1.0 / dt;
     const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation
     const T E2 = 1.0 - m2;
     const T c3 = tau * m2 * (3.0 - E2) * idt;

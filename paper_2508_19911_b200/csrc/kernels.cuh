@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   __syncthreads();
   GPOut o;
   const bool ok =
-      gks_flux_side<COMPACT>(side, wn, dn, dt, c_fc, XchgDev(), ParkDev{scratch + lane, smem + lane}, o);
+      gks_flux_side<COMPACT>(side, wn, dn, dt, ts->idt, c_fc, XchgDev(), ParkDev{scratch + lane, smem + lane}, o);
   if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
   // back to the global frame, weight 1/NG; side 0: Fn Ft (QLn QLt), side 1: QRn QRt
   double out[NR];
@@ -769,7 +769,9 @@ __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV
 static __global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
   if (err->code) return;
   const double m = __longlong_as_double((long long)ts->dtmin_bits);
-  ts->dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
+  const double dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
+  ts->dt = dt;
+  ts->idt = 1.0 / dt;
   ts->dtmin_bits = (unsigned long long)__double_as_longlong(1e300);
 }
 

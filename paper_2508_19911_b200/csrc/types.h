@@ -41,6 +41,7 @@ struct TimeState {
   double dt;
   unsigned long long dtmin_bits;
   int pad;
+  double idt;  // 1/dt, written with dt
 };
 
 }  // namespace cgks
