@@ -465,7 +465,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
     return fail(CGKS_ERR_CUDA);
   }
-  // face evaluation tables per axis: [side][quantity][nb] (quantity 0 value, 1 d/dn, 2 d/dtA, 3 d/dtB);
+  // face evaluation tables per axis: [side][quantity][nb + 1] (quantity 0 value, 1 d/dn, 2 d/dtA, 3 d/dtB);
   // entry = (+-1/2)^{d_n} s^{d_tA + d_tB} / d! with one exponent lowered for derivatives, minus the
   // own-cell average of delta^d/d! for the value; the Gauss-point signs are applied in the kernel.
   if (ctx->scheme_id == CGKS_CGKS5) {
@@ -479,7 +479,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     for (int a = 0; a < dim; ++a) {
       const int tA = dim == 3 ? (a + 1) % 3 : (dim == 2 ? 1 - a : -1);
       const int tB = dim == 3 ? (a + 2) % 3 : -1;
-      std::vector<double> tab((size_t)2 * nq * nb, 0.0);
+      const int ts = nb + 1;  // padded row (FluxTile::TS): bank-conflict-free per-quantity rows
+      std::vector<double> tab((size_t)2 * nq * ts, 0.0);
       for (int side = 0; side < 2; ++side) {
         const double dn = side == 0 ? 0.5 : -0.5;
         for (int q = 0; q < nq; ++q)
@@ -492,7 +493,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
               val = f(dn, e[a]) * (tA >= 0 ? f(sg, e[tA]) : 1.0) * (tB >= 0 ? f(sg, e[tB]) : 1.0);
               if (q == 0) val -= ctx->cls.avg0[kk];
             }
-            tab[((size_t)side * nq + q) * nb + kk] = val;
+            tab[((size_t)side * nq + q) * ts + kk] = val;
           }
       }
       if (!alloc(&ctx->gtab[a], (long long)tab.size()) ||

@@ -121,6 +121,9 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_s
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async8s(unsigned smem_addr, const double* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr), "l"(gmem_src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
                                                const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                int stage) {
   using FT = FluxTile<DIM, AX, COMPACT>;
-  constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT, FPB = FT::FPB;
+  constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT;
   constexpr int NV = COMPACT ? 20 : 5;
   constexpr int NF = COMPACT ? 30 : 10;
   constexpr int NR = COMPACT ? 20 : 10;  // values each lane reduces over the Gauss points
@@ -448,10 +451,16 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
         const int kmax = c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0);
         if (ck > kmax) ck = kmax;
       }
-      const double* rb = rec + eidx(FT::NREC, 0, ci, cj, ck);
       const long long st = c_geo.eplane;
-      // asynchronous global -> shared copies (LDGSTS): all in flight at once
-      for (int fld = fsub; fld < FT::NREC; fld += TPC) cp_async8(tile + fld * NT + c, rb + fld * st);
+      // asynchronous global -> shared copies (LDGSTS): all in flight at once; running addresses
+      const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
+      unsigned dst = (unsigned)__cvta_generic_to_shared(tile + fsub * NT + c);
+#pragma unroll 4
+      for (int fld = fsub; fld < FT::NREC; fld += TPC) {
+        cp_async8s(dst, src);
+        src += TPC * st;
+        dst += TPC * NT * (unsigned)sizeof(double);
+      }
       if (BOX) {
         for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
       } else {
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     }
   }
   if (COMPACT)
-    for (int q = threadIdx.x; q < 2 * FT::NQ * NB; q += blockDim.x) cp_async8(tab + (q / NB) * FT::TS + q % NB, gtab + q);
+    for (int q = threadIdx.x; q < 2 * FT::NQ * FT::TS; q += blockDim.x) cp_async8(tab + q, gtab + q);  // padded rows
   cp_async_wait_all();
   __syncthreads();
 
@@ -576,41 +585,55 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const bool ok =
       gks_flux_side<COMPACT>(side, wn, dn, dt, ts->idt, c_fc, XchgDev(), ParkDev{scratch + lane, smem + lane}, o);
   if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
-  // back to the global frame, weight 1/NG; side 0: Fn Ft (QLn QLt), side 1: QRn QRt
-  double out[NR];
+  const int fn1 = c_geo.fn[AX][1];
+  const long long fpl = (long long)fn0 * fn1;
+  const long long base = (long long)k * NF * fpl + (long long)j * fn0 + i;
   const double wgt = 1.0 / NG;
+  // back to the global frame with weight 1/NG: y[0..9] = Fn, Ft (equal in both lanes), y[10..19] =
+  // this side's Qn, Qt (QL on side 0, QR on side 1)
+  double y[NR];
 #pragma unroll
   for (int s = 0; s < NR / 5; ++s) {
-    double x[5];
 #pragma unroll
     for (int cc = 0; cc < 5; ++cc) {
-      const double a0 = s == 0 ? o.Fn[cc] : (s == 1 ? o.Ft[cc] : (s == 2 ? o.QLn[cc] : o.QLt[cc]));
-      const double a1 = (s % 2 == 0) ? o.QLn[cc] : o.QLt[cc];
-      x[cc] = side == 0 ? a0 : a1;
-    }
-    out[s * 5 + 0] = wgt * x[0];
-    out[s * 5 + 1 + P0] = wgt * x[1];
-    out[s * 5 + 1 + P1] = wgt * x[2];
-    out[s * 5 + 1 + P2] = wgt * x[3];
-    out[s * 5 + 4] = wgt * x[4];
-  }
-  if (NG > 1) {
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-#pragma unroll
-      for (int m = 2; m < 2 * NG; m <<= 1) out[q] += __shfl_xor_sync(0xffffffffu, out[q], m);
+      const double a = s == 0 ? o.Fn[cc] : (s == 1 ? o.Ft[cc] : (s == 2 ? o.QLn[cc] : o.QLt[cc]));
+      const int g = cc == 0 ? 0 : (cc == 4 ? 4 : 1 + (cc == 1 ? P0 : (cc == 2 ? P1 : P2)));
+      y[s * 5 + g] = wgt * a;
     }
   }
-  if (valid && gp == 0) {
-    const int fn1 = c_geo.fn[AX][1];
-    const long long fpl = (long long)fn0 * fn1;
-    const long long base = (long long)k * NF * fpl + (long long)j * fn0 + i;
-    if (side == 0) {
+  if constexpr (NG == 1) {
+    if (valid && side == 0) {
 #pragma unroll
-      for (int q = 0; q < NR; ++q) face[base + q * fpl] = out[q];
-    } else if (COMPACT) {
+      for (int q = 0; q < NR; ++q) face[base + q * fpl] = y[q];
+    } else if (valid && COMPACT) {
 #pragma unroll
-      for (int q = 0; q < 10; ++q) face[base + (20 + q) * fpl] = out[q];
+      for (int q = 10; q < NR; ++q) face[base + (q + 10) * fpl] = y[q];
+    }
+  } else {
+    // Gauss-point sum through shared memory: every lane writes its NR values into its warp's own
+    // scratch columns (row q, column skewed by q: conflict-free, and no other warp touches these
+    // columns, so a warp barrier suffices), then the LPF lanes of a face each sum a strided
+    // subset of the NF face outputs over the NG Gauss points in a fixed order and store them.
+    __syncwarp();
+    const int wb = lane & ~31, lw = lane & 31;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) scratch[q * 128 + wb + ((lw + q) & 31)] = y[q];
+    __syncwarp();
+    constexpr int LPF = FT::LPF;
+    const int r = lane & (LPF - 1);
+    const int m0 = lw - r;  // first lane of this face within the warp
+#pragma unroll
+    for (int it = 0; it < (NF + LPF - 1) / LPF; ++it) {
+      const int oo = r + it * LPF;
+      if (oo < NF) {
+        // outputs 0..19 from the side-0 lanes (Fn Ft QLn QLt), 20..29 from the side-1 lanes (QRn QRt)
+        const int sd = oo < 20 ? 0 : 1, slot = oo < 20 ? oo : oo - 10;
+        const double* row = scratch + slot * 128 + wb;
+        const int m = m0 + sd + slot;
+        double sum = row[m & 31] + row[(m + 2) & 31];
+        if (NG > 2) sum += row[(m + 4) & 31] + row[(m + 6) & 31];
+        if (valid) face[base + oo * fpl] = sum;
+      }
     }
   }
 }
