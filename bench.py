@@ -271,8 +271,20 @@ def run_ours(args, rank, ws, lr):
     except Exception:
         pass
     achieved = flops.get(dom, 0.0) / (dom_ms * 1e-3) / 1e12
+    # measured DRAM traffic per launch of the dominant kernel from the committed ncu --set full
+    # capture of this workload (tools/ncu_summary.py traffic), else null
+    traffic, traffic_src = None, None
+    wl = f"{case.name} {case.n[0]}x{case.n[1]}x{case.n[2]} {args.scheme}" + ("-geno" if case.nonlinear else "-linear")
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if tj.get("workload") == wl and ws == 1:
+            traffic = tj["per_launch_bytes"].get(dom)
+            traffic_src = "profiles/ncu_traffic.json (" + tj.get("source", "?") + ")"
+    except Exception:
+        pass
     roof = {"bound": "alu", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
-            "frac": achieved / peak64 if peak64 else None, "traffic": None,
+            "frac": achieved / peak64 if peak64 else None, "traffic": traffic, "traffic_unit": "bytes/launch",
+            "traffic_source": traffic_src,
             "kernel": dom, "kernel_ms": dom_ms, "kernel_share": prof[dom][0] / total_prof,
             "algorithmic_flops_per_launch": flops.get(dom, 0.0),
             "peak_source": "measured FP64 DFMA probe (cgks_fp64_peak) in this run; MEASURED_PEAKS.json has no FP64",

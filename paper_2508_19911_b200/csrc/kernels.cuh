@@ -424,8 +424,10 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const int fn0 = c_geo.fn[AX][0];
   // block origin: face (i0, j0, k0); y-/z-faces cover FY faces along their normal axis
   const int i0 = blockIdx.x * FX;
-  const int j0 = AX == 1 ? blockIdx.y * FY : blockIdx.y;
-  const int k0 = AX == 2 ? blockIdx.z * FY : blockIdx.z;
+  // (z-faces: grid (x, z, y), so the blocks sharing a tile plane run close together and the
+  // shared plane is still in L2)
+  const int j0 = AX == 1 ? blockIdx.y * FY : (AX == 2 ? blockIdx.z : blockIdx.y);
+  const int k0 = AX == 2 ? blockIdx.y * FY : blockIdx.z;
   // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous runs).
   // Each thread serves one tile cell (index math once) and a strided subset of its fields.
   {

@@ -88,7 +88,8 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
   }
   const unsigned gy = (unsigned)(AX == 1 ? (a.fn[AX][1] + FT::FY - 1) / FT::FY : a.fn[AX][1]);
   const unsigned gz = (unsigned)(AX == 2 ? (a.fn[AX][2] + FT::FY - 1) / FT::FY : a.fn[AX][2]);
-  const dim3 grid((unsigned)((a.fn[AX][0] + FT::FX - 1) / FT::FX), gy, gz);
+  const unsigned gx = (unsigned)((a.fn[AX][0] + FT::FX - 1) / FT::FX);
+  const dim3 grid = AX == 2 ? dim3(gx, gz, gy) : dim3(gx, gy, gz);  // z-faces: (x, z, y) order
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (env.prof) {
     cudaEventCreate(&e0);

@@ -3,7 +3,14 @@
 
   python tools/ncu_summary.py launches gpurun_out/launches.csv
   python tools/ncu_summary.py full gpurun_out/prof_flux.ncu-rep
+  python tools/ncu_summary.py traffic gpurun_out/full.ncu-rep "tgv 128x128x128 cgks5-linear" > profiles/ncu_traffic.json
+
+The traffic mode writes the measured DRAM bytes (read + write) per launch of each library kernel
+of a --set full capture, keyed by the bench's kernel names; bench.py reports it as roofline.traffic
+for the dominant kernel when the workload matches.
 """
+import json
+import re
 import collections
 import csv
 import io
@@ -83,6 +90,40 @@ def full(path):
     return "\n".join(out)
 
 
+BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def bench_name(kernel):
+    m = re.search(r"k_flux<(\d+), (\d+),", kernel)
+    if m:
+        return "flux_" + "xyz"[int(m.group(2))]
+    for k in ("recon5", "recon2", "update", "dt_finalize", "dt", "step_end", "pack", "unpack"):
+        if "k_" + k + "<" in kernel or kernel.startswith("k_" + k) or "::k_" + k in kernel:
+            return k
+    return None
+
+
+def traffic(path, workload):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
+    per = {}
+    for vals in rows[2:]:
+        d = dict(zip(hdr, vals))
+        name = bench_name(d.get("Kernel Name", ""))
+        if name is None:
+            continue
+        b = sum(float(d[k].replace(",", "")) * BYTES.get(units.get(k, "byte"), 1.0)
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        per.setdefault(name, []).append(b)
+    return json.dumps({"workload": workload, "source": path.split("/")[-1],
+                       "metric": "dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)",
+                       "per_launch_bytes": {k: sum(v) / len(v) for k, v in per.items()}}, indent=1)
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    print(launches(path) if mode == "launches" else full(path))
+    if mode == "traffic":
+        print(traffic(path, sys.argv[3]))
+    else:
+        print(launches(path) if mode == "launches" else full(path))
