@@ -74,6 +74,8 @@ inline CD special_(double r) {
 inline CD exp(const CD& a) { return a.k ? CD(std::exp(a.v)) : special_(std::exp(a.v)); }
 inline CD expm1(const CD& a) { return a.k ? CD(std::expm1(a.v)) : special_(std::expm1(a.v)); }
 inline CD erfc(const CD& a) { return a.k ? CD(std::erfc(a.v)) : special_(std::erfc(a.v)); }
+// erfc with the shared exp(-z^2) (gks_flux.cuh: erfc_e) counts as one special function
+inline CD erfc_e(const CD& z, const CD& e) { return z.k ? CD(std::erfc(z.v)) : special_(std::erfc(z.v)); }
 inline CD rsqrt_(const CD& a) { return a.k ? CD(1.0 / std::sqrt(a.v)) : special_(1.0 / std::sqrt(a.v)); }
 inline CD sqrt(const CD& a) {
   if (a.k) return CD(std::sqrt(a.v));
