@@ -282,17 +282,20 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
         ismin = fmin(ismin, IS[m]);
       }
       double lin[3] = {0.0, 0.0, 0.0};
+      // omega_m = (IS_m + eps)^-5 / sum_k (IS_k + eps)^-5 (R9): with eps = 1e-15 every term is
+      // at most 1e75, so the normalised form cannot overflow (6 reciprocals, no ratio table)
+      double w5[S::NFACE], s5 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < S::NFACE; ++kk) {
+        const double iv = 1.0 / (IS[kk] + eps);
+        const double i2 = iv * iv;
+        w5[kk] = i2 * i2 * iv;
+        s5 += w5[kk];
+      }
+      const double is5 = 1.0 / s5;
 #pragma unroll
       for (int m = 0; m < S::NFACE; ++m) {
-        double den = 0.0;
-        const double num = IS[m] + eps;
-#pragma unroll
-        for (int kk = 0; kk < S::NFACE; ++kk) {
-          const double r = num / (IS[kk] + eps);
-          const double r2 = r * r;
-          den += r2 * r2 * r;
-        }
-        const double w = 1.0 / den;
+        const double w = w5[m] * is5;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) lin[a] = fma(w, bm[m][a], lin[a]);
       }
