@@ -5,8 +5,8 @@ averages Q and exact cell-averaged gradients grad Q of analytic or seeded random
 fields (R26 of DESIGN.md), in the user-facing layout
 ``Q[5][nz][ny][nx]`` and ``G[3][5][nz][ny][nx]`` (x fastest).
 """
-from .cases import (Case, tgv, vortex, vortex_exact, random_smooth, uniform, double_sod, shock_vortex, hit,
-                    CASES, make_case)
+from .cases import (Case, tgv, tgv_supersonic, vortex, vortex_exact, random_smooth, uniform, double_sod,
+                    shock_vortex, hit, CASES, make_case)
 
-__all__ = ["Case", "tgv", "vortex", "vortex_exact", "random_smooth", "uniform", "double_sod", "shock_vortex",
+__all__ = ["Case", "tgv", "tgv_supersonic", "vortex", "vortex_exact", "random_smooth", "uniform", "double_sod", "shock_vortex",
            "hit", "CASES", "make_case"]

@@ -37,6 +37,7 @@ class Case:
     relax_C: float = 10.0
     steps: int = 10
     note: str = ""
+    sutherland_S: float = 0.0  # 0: constant mu; 0.4042: Sutherland law
 
     @property
     def ncell(self) -> int:
@@ -50,7 +51,8 @@ class Case:
         """Physical and scheme parameters as keyword arguments (shared by both arms)."""
         return dict(n=tuple(self.n), lo=tuple(self.lo), hi=tuple(self.hi), gamma=self.gamma, mu=self.mu,
                     Pr=self.Pr, bc=self.bc, bc_state=np.array(self.bc_state), cfl=self.cfl,
-                    nonlinear=self.nonlinear, tau_eps=self.tau_eps, tau_C=self.tau_C, relax_C=self.relax_C)
+                    nonlinear=self.nonlinear, tau_eps=self.tau_eps, tau_C=self.tau_C, relax_C=self.relax_C,
+                    sutherland_S=self.sutherland_S)
 
 
 def prim_to_cons(rho, u, v, w, p, gamma):
@@ -204,6 +206,35 @@ def tgv(n: int = 64, Ma: float = 0.1, Re: float = 1600.0, Pr: float = 0.72, gamm
     mu = 1.0 / Re  # rho0 U0 L / Re
     return Case("tgv", nn, lo, hi, Q, G, gamma=gamma, mu=mu, Pr=Pr, cfl=0.3, nonlinear=0, steps=100,
                 note=f"TGV Ma={Ma} Re={Re} rho=1 (BASELINE configs[1]); exact separable averages")
+
+
+def _tgv_supersonic_prim(Ma, gamma):
+    U0 = math.sqrt(gamma) * Ma  # U0 = sqrt(gamma) Ma, rho0 = p0 = T0 = 1
+
+    def f(x, y, z):
+        s = 1.0 + (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
+        u = U0 * np.sin(x) * np.cos(y) * np.cos(z)
+        v = -U0 * np.cos(x) * np.sin(y) * np.cos(z)
+        return s, u, v, np.zeros_like(u), s  # rho = rho0 s, p = p0 s: T = p / rho = 1
+    return f
+
+
+def tgv_supersonic(n: int = 116, Ma: float = 2.0, Re: float = 1600.0, Pr: float = 0.7, gamma: float = 1.4,
+                   nq: int = 6) -> Case:
+    """High-speed Taylor-Green vortex: periodic [-pi, pi]^3 (L = 1),
+    U = U0 sin x cos y cos z, V = -U0 cos x sin y cos z, W = 0, rho = p = 1 + (cos 2x + cos 2y)(cos 2z + 2)/16,
+    U0 = sqrt(gamma) Ma, Re = 1600, Pr = 0.7, Sutherland viscosity mu(T) = mu0 1.4042 T^1.5 / (T + 0.4042),
+    mu0 = rho0 U0 L / Re.  Cell averages and averaged gradients by nq-point Gauss-Legendre per axis
+    (trigonometric data of frequency <= 4: nq = 6 is exact to rounding at the paper's 116^3).  Nonlinear
+    schemes (GENO / Venkatakrishnan) as in the paper."""
+    nn = (n, n, n)
+    lo, hi = (-PI, -PI, -PI), (PI, PI, PI)
+    Q, G = gl_average(_tgv_supersonic_prim(Ma, gamma), nn, lo, hi, gamma, nq=nq)
+    U0 = math.sqrt(gamma) * Ma
+    c = Case("tgv_ss", nn, lo, hi, Q, G, gamma=gamma, mu=U0 / Re, Pr=Pr, cfl=0.3, nonlinear=1, steps=100,
+             note=f"high-speed TGV Ma={Ma} Re={Re} Sutherland (P:455-474)")
+    c.sutherland_S = 0.4042
+    return c
 
 
 # ---------------------------------------------------------------------------
@@ -397,7 +428,7 @@ def random_smooth(n=(12, 10, 8), seed: int = 7, amp: float = 0.2, gamma: float =
     return Case("random_smooth", nn, lo, hi, Q, G, gamma=gamma, mu=mu, Pr=Pr, cfl=0.4)
 
 
-CASES = {"vortex": vortex, "tgv": tgv, "hit": hit, "shock_vortex": shock_vortex, "double_sod": double_sod,
+CASES = {"vortex": vortex, "tgv": tgv, "tgv_supersonic": tgv_supersonic, "hit": hit, "shock_vortex": shock_vortex, "double_sod": double_sod,
          "uniform": uniform, "random_smooth": random_smooth}
 
 

@@ -49,6 +49,7 @@ class OrcParams(ctypes.Structure):
         ("relax_C", ctypes.c_double),
         ("k_venkat", ctypes.c_double),
         ("chi_c", ctypes.c_double),
+        ("sutherland_S", ctypes.c_double),
     ]
 
 
@@ -108,6 +109,7 @@ class Problem:
     relax_C: float = 10.0
     k_venkat: float = 0.3
     chi_c: float = 0.01
+    sutherland_S: float = 0.0  # 0: constant mu; 0.4042: the paper's Sutherland law
     bc: tuple = ((0, 0), (0, 0), (0, 0))
     bc_state: np.ndarray = field(default_factory=lambda: np.zeros((3, 2, 5)))
 
@@ -126,6 +128,7 @@ class Problem:
         p.cfl, p.fixed_dt = self.cfl, self.fixed_dt
         p.tau_eps, p.tau_C, p.relax_C = self.tau_eps, self.tau_C, self.relax_C
         p.k_venkat, p.chi_c = self.k_venkat, self.chi_c
+        p.sutherland_S = self.sutherland_S
         return p
 
 
@@ -168,13 +171,13 @@ def time_integrals(T: float, tau: float) -> np.ndarray:
 
 
 def flux_point(WL, dWL, WR, dWR, gamma, dt, mu=0.0, Pr=1.0, tau_eps=0.05, tau_C=10.0, relax_C=10.0,
-               compact=1):
+               compact=1, sutherland_S=0.0):
     """Interface flux at one Gauss point (normal frame). Returns a dict of outputs."""
     WL = np.ascontiguousarray(WL, dtype=np.float64)
     WR = np.ascontiguousarray(WR, dtype=np.float64)
     dWL = np.ascontiguousarray(dWL, dtype=np.float64).reshape(15)
     dWR = np.ascontiguousarray(dWR, dtype=np.float64).reshape(15)
-    fpar = np.array([dt, mu, Pr, tau_eps, tau_C, relax_C, compact], dtype=np.float64)
+    fpar = np.array([dt, mu, Pr, tau_eps, tau_C, relax_C, compact, sutherland_S], dtype=np.float64)
     out = np.zeros(64)
     sl = np.zeros(60)
     rc = lib().orc_flux_point(_ptr(WL), _ptr(dWL), _ptr(WR), _ptr(dWR), gamma, _ptr(fpar), _ptr(out), _ptr(sl))

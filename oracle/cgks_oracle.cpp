@@ -46,6 +46,7 @@ typedef struct {
   double relax_C;           // tau0 constant (R23)
   double k_venkat;          // Venkatakrishnan K (R11)
   double chi_c;             // GENO chi constant (R8)
+  double sutherland_S;      // 0: constant mu; > 0: Sutherland law mu(T) = mu (1+S) T^{3/2} / (T+S), T = p/rho
 } orc_params;
 
 }  // extern "C"
@@ -295,7 +296,16 @@ void micro_slope(const MomMat& mm, const double b[5], double a[5]) {
 struct FluxParams {
   double dt, mu, Pr, tau_eps, tau_C, relax_C;
   int compact;  // 1: CGKS-5th (interface values and side relaxation wanted)
+  double sutherland_S;  // 0: constant mu
 };
+
+// Dynamic viscosity (high-speed TGV): the Sutherland law
+//   mu(T) = mu_0 * 1.4042 T^{3/2} / (T + 0.4042),  T = p / rho (R = 1),
+// written with S = 0.4042 as mu_0 (1 + S) T^{3/2} / (T + S); S = 0 gives the constant mu_0 (R19).
+double viscosity(double mu0, double S, double T) {
+  if (S <= 0.0) return mu0;
+  return mu0 * (1.0 + S) * std::pow(T, 1.5) / (T + S);
+}
 
 struct FluxOut {
   double Fn[5], Ft[5];          // F^n, F_t^n
@@ -404,7 +414,7 @@ int gks_flux(const double WL[5], const double dWL[3][5], const double WR[5], con
   double jump = std::fabs((pL.p - pR.p) / (pL.p + pR.p));
   double tau;
   if (fp.mu > 0.0)
-    tau = fp.mu / p0.p + fp.tau_C * jump * fp.dt;
+    tau = viscosity(fp.mu, fp.sutherland_S, p0.p / p0.rho) / p0.p + fp.tau_C * jump * fp.dt;  // mu(T0), T0 = p0/rho0
   else
     tau = fp.tau_eps * fp.dt + fp.tau_C * jump * fp.dt;
   o.tau = tau;
@@ -1003,7 +1013,7 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
 
   // (2) face fluxes: Gauss points (R27); K = 4 on a 3-D face, 2 on a 2-D edge, 1 in 1-D; midpoint for GKS-2nd
   double gq = 0.5 / std::sqrt(3.0);
-  FluxParams fp{dt, S.P.mu, S.P.Pr, S.P.tau_eps, S.P.tau_C, S.P.relax_C, S.P.scheme == 1 ? 1 : 0};
+  FluxParams fp{dt, S.P.mu, S.P.Pr, S.P.tau_eps, S.P.tau_C, S.P.relax_C, S.P.scheme == 1 ? 1 : 0, S.P.sutherland_S};
   long nc = S.ncell();
   std::vector<std::vector<FaceAvg>> faces(S.dim);
   std::vector<int> face_err(S.dim, 0);
@@ -1159,7 +1169,8 @@ double compute_dt(const Solver& S, const std::vector<CellState>& F, int* err) {
     double cs = std::sqrt(S.gas.gamma * w.p / w.rho);
     for (int a = 0; a < S.dim; ++a) {
       double d = S.h[a] / (std::fabs(w.U[a]) + cs);
-      if (S.P.mu > 0.0) d = std::min(d, S.h[a] * S.h[a] / (3.0 * S.P.mu / w.rho));
+      if (S.P.mu > 0.0)  // nu = mu(T) / rho (R25)
+        d = std::min(d, S.h[a] * S.h[a] / (3.0 * viscosity(S.P.mu, S.P.sutherland_S, w.p / w.rho) / w.rho));
       dtmin = std::min(dtmin, d);
     }
   }
@@ -1315,13 +1326,14 @@ void orc_micro_slope(const double* prim, double gamma, const double* b, double* 
 // time-integral coefficients C_1..C_6 (Appendix A.1 of SURVEY)
 void orc_time_integrals(double T, double tau, double* C6) { time_integrals(T, tau, C6); }
 
-// flux at one Gauss point in the normal frame.  fparams = (dt, mu, Pr, tau_eps, tau_C, relax_C, compact)
+// flux at one Gauss point in the normal frame.  fparams = (dt, mu, Pr, tau_eps, tau_C, relax_C, compact,
+// sutherland_S)
 // out (length 64): Fn[5] Ft[5] Qn[5] Qt[5] QLn[5] QLt[5] QRn[5] QRt[5] Fbar_dt[5] Fbar_half[5] tau tau0 W0[5]
 // slopes (length 60): aL[15] aR[15] abar[15] AL[5] AR[5] Abar[5]
 int orc_flux_point(const double* WL, const double* dWL, const double* WR, const double* dWR, double gamma,
                    const double* fparams, double* out, double* slopes) {
   Gas gas(gamma);
-  FluxParams fp{fparams[0], fparams[1], fparams[2], fparams[3], fparams[4], fparams[5], (int)fparams[6]};
+  FluxParams fp{fparams[0], fparams[1], fparams[2], fparams[3], fparams[4], fparams[5], (int)fparams[6], fparams[7]};
   double dl[3][5], dr[3][5];
   for (int a = 0; a < 3; ++a)
     for (int v = 0; v < 5; ++v) {

@@ -250,6 +250,31 @@ def test_navier_stokes_limit(Pr):
     assert abs(d["Fn"][1] - 1.0) < 1e-12  # pressure unchanged to first order
 
 
+def _sutherland(mu0, T):
+    # mu(T) = mu_0 1.4042 T^{3/2} / (T + 0.4042)
+    return mu0 * 1.4042 * T ** 1.5 / (T + 0.4042)
+
+
+@pytest.mark.parametrize("rho", [1.0, 0.5, 2.5])
+def test_navier_stokes_limit_sutherland(rho):
+    """High-speed TGV viscosity: with the Sutherland law the Chapman-Enskog shear
+    stress of the BGK flux is mu(T) dv/dx with T = p/rho of the local state (here T = 1/rho), and
+    mu(1) = mu_0."""
+    mu0, dt, s = 1e-6, 1e-2, 0.1
+    W = _ns_state(rho=rho, p=1.0)
+    dW = np.zeros((3, 5))
+    dW[0, 2] = rho * s  # v = s x
+    d = oracle.flux_point(W, dW, W, dW, GAMMA, dt=dt, mu=mu0, Pr=1.0, tau_C=0.0, sutherland_S=0.4042)
+    mu = _sutherland(mu0, 1.0 / rho)
+    assert abs(d["Fn"][2] - (-mu * s)) < 1e-3 * mu * s
+    if rho == 1.0:
+        assert abs(mu - mu0) < 1e-22
+    # collision time in a smooth region: tau = mu(T0) / p0 (P:352-354)
+    z = np.zeros((3, 5))
+    d = oracle.flux_point(W, z, W, z, GAMMA, dt=dt, mu=mu0, sutherland_S=0.4042)
+    assert abs(d["tau"] - mu / 1.0) < 1e-15 * mu
+
+
 def test_prandtl_fix_vanishes_in_euler_limit():
     # tau = 0: f = g0 + t Abar g0 is pure equilibrium, so the Pr fix must add nothing (R20 pitfall)
     rng = np.random.default_rng(11)

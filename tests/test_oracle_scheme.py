@@ -127,6 +127,14 @@ def test_dt_examples():
     c = uniform((4, 4, 4), state=(1.0, 0.0, 0.0, 0.0, 1e-14), L=0.4)
     p = _prob(c, cfl=0.3, mu=0.01)
     assert abs(oracle.dt(p, c.Q) - 0.1) < 1e-14
+    # Sutherland viscosity (R25: nu = mu(T)/rho): rho = 0.25, p = 1 -> T = 4,
+    # mu = 0.01 * 1.4042 * 8 / 4.4042; dt = 0.3 h^2 / (3 nu) with h = 0.1, sound speed bound inactive
+    c = uniform((4, 4, 4), state=(0.25, 0.0, 0.0, 0.0, 1.0), L=0.4)  # primitive (rho, u, v, w, p)
+    p = _prob(c, cfl=0.3, mu=0.01)
+    p.sutherland_S = 0.4042
+    nu = 0.01 * 1.4042 * 8.0 / 4.4042 / 0.25
+    want = 0.3 * min(0.1 / math.sqrt(1.4 * 4.0), 0.01 / (3.0 * nu))
+    assert abs(oracle.dt(p, c.Q) - want) < 1e-15 * want
 
 
 def test_positivity_error_code():
@@ -153,3 +161,31 @@ def test_tgv_initial_energy_decay():
     assert rc == 0
     rate = (ek(Q) - ek(c.Q)) / t
     assert abs(rate / (-0.75 / 1600.0) - 1.0) < 0.08, rate
+
+
+def test_supersonic_tgv_initial_condition():
+    """High-speed TGV: rho = p pointwise (T = 1), mean rho = 1, zero mean momentum and
+    <rho E> = p0/(gamma-1) + rho0 U0^2 / 8 exactly (the (cos 2x + cos 2y) correlation averages out), i.e.
+    the normalised kinetic energy starts at E_k = 1/8."""
+    from cgks_inputs import tgv_supersonic
+    c = tgv_supersonic(12)
+    U0sq = 1.4 * 4.0
+    assert abs(c.Q[0].mean() - 1.0) < 1e-14
+    assert np.abs(c.Q[1:4].mean(axis=(1, 2, 3))).max() < 1e-14
+    assert abs(c.Q[4].mean() - (1.0 / 0.4 + U0sq / 8.0)) < 1e-13
+    assert c.sutherland_S == 0.4042 and abs(c.mu - math.sqrt(1.4) * 2.0 / 1600.0) < 1e-18
+
+
+def test_supersonic_tgv_runs_nonlinear():
+    """The nonlinear schemes advance the Ma = 2 TGV with Sutherland viscosity: positive, conservative,
+    kinetic energy non-increasing over a few steps."""
+    from cgks_inputs import tgv_supersonic
+    c = tgv_supersonic(12)
+    for scheme, ts in ((1, 2), (0, 1)):
+        p = _prob(c, scheme=scheme, time_scheme=ts, nonlinear=1)
+        Q, G, t, dt, rc = oracle.run(p, c.Q, c.G if scheme == 1 else None, 4)
+        assert rc == 0 and t > 0
+        assert np.allclose(Q.sum(axis=(1, 2, 3)), c.Q.sum(axis=(1, 2, 3)), rtol=1e-13, atol=1e-11)
+        ek0 = (0.5 * (c.Q[1] ** 2 + c.Q[2] ** 2 + c.Q[3] ** 2) / c.Q[0]).sum()
+        ek1 = (0.5 * (Q[1] ** 2 + Q[2] ** 2 + Q[3] ** 2) / Q[0]).sum()
+        assert ek1 < ek0
