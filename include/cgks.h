@@ -76,6 +76,9 @@ typedef struct {
   double relax_C;   /* tau0 jump constant of the side-state relaxation (R23), 10       */
   double k_venkat;  /* Venkatakrishnan K (R11), 0.3                                               */
   double chi_c;     /* GENO chi constant (R8), 0.01                                               */
+  double sutherland_S; /* viscosity law: 0 = constant mu (R19, default); S > 0 = Sutherland law       */
+                       /* mu(T) = mu (1 + S) T^{3/2} / (T + S), T = p / rho, with mu the value at T = 1 */
+                       /* (S = 0.4042); used in the collision time and the viscous dt bound */
 } cgks_scheme;
 
 /* Fill a cgks_scheme with the paper defaults for scheme id (CGKS_GKS2 / CGKS_CGKS5). */

@@ -45,6 +45,7 @@ class cgks_scheme(ctypes.Structure):
         ("relax_C", ctypes.c_double),
         ("k_venkat", ctypes.c_double),
         ("chi_c", ctypes.c_double),
+        ("sutherland_S", ctypes.c_double),
     ]
 
 
@@ -161,7 +162,8 @@ class Solver:
 
     def __init__(self, n, lo, hi, gamma=1.4, mu=0.0, Pr=1.0, scheme=CGKS_CGKS5, nonlinear=0,
                  time_scheme=CGKS_TIME_DEFAULT, cfl=None, fixed_dt=0.0, tau_eps=0.05, tau_C=10.0, relax_C=10.0,
-                 k_venkat=0.3, chi_c=0.01, bc=((0, 0), (0, 0), (0, 0)), bc_state=None, stream=None,
+                 k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
+                 stream=None,
                  nproc=(1, 1, 1), rank=0, nccl_id=None):
         L = load()
         g = cgks_grid()
@@ -188,6 +190,7 @@ class Solver:
         sc.fixed_dt = float(fixed_dt)
         sc.tau_eps, sc.tau_C, sc.relax_C = float(tau_eps), float(tau_C), float(relax_C)
         sc.k_venkat, sc.chi_c = float(k_venkat), float(chi_c)
+        sc.sutherland_S = float(sutherland_S)
         ctx = ctypes.c_void_p()
         rc = L.cgks_create(ctypes.byref(g), float(gamma), float(mu), float(Pr), ctypes.byref(sc), ctypes.byref(ctx))
         if rc != CGKS_OK:
@@ -284,6 +287,6 @@ class Solver:
     def from_case(cls, case, scheme=CGKS_CGKS5, **kw):
         d = dict(gamma=case.gamma, mu=case.mu, Pr=case.Pr, nonlinear=case.nonlinear, cfl=case.cfl,
                  tau_eps=case.tau_eps, tau_C=case.tau_C, relax_C=case.relax_C, bc=case.bc,
-                 bc_state=case.bc_state)
+                 bc_state=case.bc_state, sutherland_S=getattr(case, "sutherland_S", 0.0))
         d.update(kw)
         return cls(case.n, case.lo, case.hi, scheme=scheme, **d)

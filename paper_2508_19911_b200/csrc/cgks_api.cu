@@ -281,6 +281,7 @@ void cgks_scheme_defaults(int id, cgks_scheme* s) {
   s->relax_C = 10.0;
   s->k_venkat = 0.3;
   s->chi_c = 0.01;
+  s->sutherland_S = 0.0;
 }
 
 int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const cgks_scheme* scheme,
@@ -302,6 +303,10 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     }
   if (!(gamma > 1.0 && gamma <= 5.0 / 3.0 + 1e-12) || !(mu >= 0.0) || !(Pr > 0.0)) {
     set_msg(ctx, "invalid gas parameters gamma=%g mu=%g Pr=%g", gamma, mu, Pr);
+    return fail(CGKS_ERR_CONFIG);
+  }
+  if (!(scheme->sutherland_S >= 0.0)) {
+    set_msg(ctx, "invalid Sutherland constant %g", scheme->sutherland_S);
     return fail(CGKS_ERR_CONFIG);
   }
   if (scheme->id != CGKS_GKS2 && scheme->id != CGKS_CGKS5) {
@@ -380,6 +385,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   g.gamma = gamma;
   g.k_venkat = scheme->k_venkat;
   g.chi_c = scheme->chi_c;
+  g.suth = scheme->sutherland_S;
   double hg = 1.0;
   for (int a = 0; a < dim; ++a) hg *= g.h[a];
   hg = std::pow(hg, 1.0 / dim);
@@ -392,6 +398,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   ctx->fc.tau_eps = scheme->tau_eps;
   ctx->fc.tau_C = scheme->tau_C;
   ctx->fc.relax_C = scheme->relax_C;
+  ctx->fc.suth = scheme->sutherland_S;
   ctx->ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   ctx->necell = (long long)g.en[0] * g.en[1] * g.en[2];
 

@@ -31,6 +31,7 @@ HD double rsqrt_(double x) {
 struct FluxConst {
   double gamma, N, mu, Pr, tau_eps, tau_C, relax_C;
   double pfix;  // 1/Pr - 1
+  double suth;  // Sutherland constant S: mu(T) = mu (1 + S) T^{3/2} / (T + S); 0 = constant mu
 };
 
 // Complementary error function given e = exp(-z^2), which the caller shares with the half-range
@@ -420,7 +421,13 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const
   // one reciprocal serves 1/p0 and 1/(pL + pR)
   const T rpp = 1.0 / (p0 * (pL + pR));
   const T jump = fabs(pL - pR) * (p0 * rpp);
-  const T tau = (fc.mu > 0.0) ? (fc.mu * ((pL + pR) * rpp) + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
+  // mu / p0 with mu = mu(T0), T0 = p0 / rho0 (Sutherland): mu(T0) / p0 = mu (1+S) sqrt(T0) / (rho0 (T0+S))
+  T mu_p0 = fc.mu * ((pL + pR) * rpp);
+  if (fc.suth > 0.0) {
+    const T T0 = p0 * i0;
+    mu_p0 = fc.mu * (1.0 + fc.suth) * sqrt(T0) * i0 / (T0 + fc.suth);
+  }
+  const T tau = (fc.mu > 0.0) ? (mu_p0 + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
   T al[6], be[6];
   {
     const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation

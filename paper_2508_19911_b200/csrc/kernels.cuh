@@ -772,10 +772,15 @@ __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV
       flag_error(err, 3, 3, 0, ts->steps, i, j, k);
     } else {
       const double c = sqrt(c_geo.gamma * p * ir);
+      double mu_T = c_geo.mu;
+      if (c_geo.suth > 0.0) {  // Sutherland law, T = p / rho
+        const double Tc = p * ir;
+        mu_T = c_geo.mu * (1.0 + c_geo.suth) * Tc * sqrt(Tc) / (Tc + c_geo.suth);
+      }
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
         double d = c_geo.h[a] / (fabs(u[a]) + c);
-        if (c_geo.mu > 0.0) d = fmin(d, c_geo.h[a] * c_geo.h[a] / (3.0 * c_geo.mu * ir));
+        if (c_geo.mu > 0.0) d = fmin(d, c_geo.h[a] * c_geo.h[a] / (3.0 * mu_T * ir));  // nu = mu(T) / rho (R25)
         cand = fmin(cand, d);
       }
       if (!(cand == cand)) flag_error(err, 4, 3, 0, ts->steps, i, j, k);

@@ -25,6 +25,7 @@ struct Geo {
   double bc_state[3][2][5];
   double cfl, fixed_dt, mu, gamma;
   double k_venkat, chi_c, eps_venkat2;
+  double suth;  // Sutherland constant S (0: constant mu)
 };
 
 struct ErrState {

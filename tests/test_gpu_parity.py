@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
-from cgks_inputs import double_sod, hit, random_smooth, shock_vortex, tgv, uniform, vortex
+from cgks_inputs import double_sod, hit, random_smooth, shock_vortex, tgv, tgv_supersonic, uniform, vortex
 from parity_util import floors, rel_linf, worst
 
 pytestmark = pytest.mark.gpu
@@ -248,3 +248,24 @@ def test_parity_shock_vortex_config4_100_steps():
     sens = worst(rel_linf(Qs, Qo, Gs, Go, _L(case)))[1]
     err = worst(rel_linf(Qg, Qo, Gg, Go, _L(case)))
     assert err[1] <= max(1e-8, 20.0 * sens), (err, sens)
+
+
+# ---- high-speed TGV (Ma 2) with Sutherland viscosity, nonlinear schemes ----
+def test_parity_supersonic_tgv_geno_10_steps():
+    # P:455-474 at 20^3: nonlinear CGKS-5th (GENO), mu(T) by the Sutherland law, 10 S2O4 steps
+    case = tgv_supersonic(20)
+    Qg, Gg, Qo, Go = _run_both(case, 1, 10)
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+
+
+def test_parity_supersonic_tgv_gks2_venkat_10_steps():
+    # the paper's GKS-2nd comparison run: Venkatakrishnan-limited GKS-2nd, S1O2, Sutherland viscosity
+    case = tgv_supersonic(20)
+    Qg, Gg, Qo, Go = _run_both(case, 0, 10)
+    _check(Qg, Gg, Qo, Go, 0, 1e-10, _L(case))
+
+
+def test_full_size_supersonic_tgv116_sampled():
+    # the paper's CGKS-5th mesh (116^3, nonlinear), one step on the full grid, sampled against the oracle
+    e = _sampled_one_step(tgv_supersonic(116), 1, samples=8)
+    assert e <= 1e-10, e
