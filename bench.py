@@ -3,7 +3,7 @@
 cell-updates/s and the fraction of the FP64/HBM roofline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload tgv128|tgv64|hit128|shock_vortex|vortex40] [--scheme cgks5|gks2]
+                  [--workload tgv128|tgv64|hit128|shock_vortex|vortex40|tgv_ss116] [--scheme cgks5|gks2]
 
 A step is one full S2O4 time step of CGKS-5th (dt min-reduction + two stages of
 reconstruction, fluxes and update) over the whole grid.  Default workload: the
@@ -35,7 +35,9 @@ METRIC = "CGKS-5th FP64 cell-updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline
 
 
 def make_case(name):
-    from cgks_inputs import hit, shock_vortex, tgv, vortex
+    from cgks_inputs import hit, shock_vortex, tgv, tgv_supersonic, vortex
+    if name == "tgv_ss116":  # high-speed TGV, the paper's CGKS-5th mesh (NEXT-2), nonlinear
+        return tgv_supersonic(116)
     if name == "tgv128":
         return tgv(128)
     if name == "tgv64":
@@ -130,7 +132,11 @@ def cpu_baseline(case_name, scheme, budget_s=20.0):
     import oracle
     from cgks_inputs import tgv
     oracle.build()
-    c = tgv(32) if case_name.startswith("tgv") else make_case(case_name)
+    if case_name.startswith("tgv_ss"):
+        from cgks_inputs import tgv_supersonic
+        c = tgv_supersonic(32)
+    else:
+        c = tgv(32) if case_name.startswith("tgv") else make_case(case_name)
     if case_name in ("hit128",):
         from cgks_inputs import hit
         c = hit(32)
@@ -158,7 +164,11 @@ def run_reference(args, rank, ws):
     # the reference arm: W untimed + K timed oracle steps on the bounded sample
     import oracle
     from cgks_inputs import tgv
-    c = tgv(24) if args.workload.startswith("tgv") else make_case(args.workload)
+    if args.workload.startswith("tgv_ss"):
+        from cgks_inputs import tgv_supersonic
+        c = tgv_supersonic(24)
+    else:
+        c = tgv(24) if args.workload.startswith("tgv") else make_case(args.workload)
     prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if args.scheme == "cgks5" else 0,
                           time_scheme=2 if args.scheme == "cgks5" else 1)
     Q, G = c.Q, c.G
