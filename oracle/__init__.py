@@ -79,6 +79,8 @@ def lib():
         L.orc_recon_eval.restype = ctypes.c_int
         L.orc_stage_residual.argtypes = [pp, dp, dp, ctypes.c_double, dp, dp, dp, dp]
         L.orc_stage_residual.restype = ctypes.c_int
+        L.orc_diagnostics.argtypes = [pp, dp, dp, dp]
+        L.orc_diagnostics.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -223,6 +225,19 @@ def recon_eval(prob: Problem, Q, G, ijk, x):
     if rc:
         raise ValueError(f"recon_eval rc={rc}")
     return out[:, :5], out[:, 5:].reshape(-1, 3, 5), chi
+
+
+def diagnostics(prob: Problem, Q, G=None):
+    """Quadrature of the reconstructed state (orc_diagnostics): returns
+    (int 1/2 rho|U|^2 dV, int mu|curl U|^2 dV, int 4/3 mu (div U)^2 dV, int rho dV)."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    G = np.zeros((3,) + Q.shape) if G is None else np.ascontiguousarray(G, dtype=np.float64)
+    out = np.zeros(4)
+    p = prob.to_c()
+    rc = lib().orc_diagnostics(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
+    if rc:
+        raise ValueError(f"oracle diagnostics failed rc={rc}")
+    return out
 
 
 def stage_residual(prob: Problem, Q, G, dt: float):

@@ -1415,6 +1415,72 @@ int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i,
   return 0;
 }
 
+// Flow diagnostics of a state:
+//   out[0] = int 1/2 rho |U|^2 dV              kinetic energy (E_k times rho0 U0^2 |Omega|)
+//   out[1] = int mu(T) |curl U|^2 dV          solenoidal dissipation (eps_S times rho0 U0^2 |Omega|)
+//   out[2] = int 4/3 mu(T) (div U)^2 dV       dilatational dissipation (eps_D times rho0 U0^2 |Omega|)
+//   out[3] = int rho dV                        mass
+// "calculated by numerical quadrature, and the velocity derivative values at quadrature points are
+// obtained by the compact reconstruction": each cell's own reconstruction (CGKS-5th
+// quartic, blended with the GENO linears when nonlinear; GKS-2nd limited linear) is evaluated at the
+// 3-point Gauss-Legendre nodes of every active axis (reading R35), weights times the cell volume.
+// U = (rho U)/rho, dU = (d(rho U) - U d rho)/rho, T = p/rho, mu(T) by viscosity() (R19 / P:469-473).
+int orc_diagnostics(const orc_params* p, const double* Q, const double* G, double* out) {
+  Solver S(*p);
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
+  load_state(S, Q, G);
+  const double gx[3] = {-0.5 * std::sqrt(0.6), 0.0, 0.5 * std::sqrt(0.6)};  // nodes on [-1/2, 1/2]
+  const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};                // weights, sum 1
+  const int nq[3] = {S.dim >= 1 ? 3 : 1, S.dim >= 2 ? 3 : 1, S.dim >= 3 ? 3 : 1};
+  const double vol = S.h[0] * S.h[1] * S.h[2];
+  const long nc = S.ncell();
+  std::vector<double> part((size_t)nc * 4, 0.0);
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (long c = 0; c < nc; ++c) {
+    const int i = (int)(c % S.P.n[0]), j = (int)((c / S.P.n[0]) % S.P.n[1]), k = (int)(c / ((long)S.P.n[0] * S.P.n[1]));
+    CellRecon cr;
+    if (S.P.scheme == 1)
+      recon5_cell(S, S.U, i, j, k, cr);
+    else
+      recon2_cell(S, S.U, i, j, k, cr);
+    for (int qz = 0; qz < nq[2]; ++qz)
+      for (int qy = 0; qy < nq[1]; ++qy)
+        for (int qx = 0; qx < nq[0]; ++qx) {
+          const double x[3] = {nq[0] == 3 ? gx[qx] : 0.0, nq[1] == 3 ? gx[qy] : 0.0, nq[2] == 3 ? gx[qz] : 0.0};
+          const double w = (nq[0] == 3 ? gw[qx] : 1.0) * (nq[1] == 3 ? gw[qy] : 1.0) * (nq[2] == 3 ? gw[qz] : 1.0) * vol;
+          double W[5], dW[3][5];
+          if (S.P.scheme == 1)
+            recon5_eval(S, cr, basis_at(S.rc, x), W, dW);
+          else
+            recon2_eval(S, cr, x, W, dW);
+          const double rho = W[0];
+          if (!(rho > 0.0)) {
+            bad = 1;
+            continue;
+          }
+          double U[3], dU[3][3];  // dU[a][i] = d U_i / d x_a
+          for (int a = 0; a < 3; ++a) U[a] = W[1 + a] / rho;
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) dU[a][b] = (dW[a][1 + b] - U[b] * dW[a][0]) / rho;
+          const double ke = 0.5 * rho * (U[0] * U[0] + U[1] * U[1] + U[2] * U[2]);
+          const double pr = (S.gas.gamma - 1.0) * (W[4] - ke);
+          const double mu = viscosity(S.P.mu, S.P.sutherland_S, pr / rho);
+          const double om[3] = {dU[1][2] - dU[2][1], dU[2][0] - dU[0][2], dU[0][1] - dU[1][0]};
+          const double dv = dU[0][0] + dU[1][1] + dU[2][2];
+          part[(size_t)c * 4 + 0] += w * ke;
+          part[(size_t)c * 4 + 1] += w * mu * (om[0] * om[0] + om[1] * om[1] + om[2] * om[2]);
+          part[(size_t)c * 4 + 2] += w * (4.0 / 3.0) * mu * dv * dv;
+          part[(size_t)c * 4 + 3] += w * rho;
+        }
+  }
+  long double acc[4] = {0, 0, 0, 0};
+  for (long c = 0; c < nc; ++c)
+    for (int q = 0; q < 4; ++q) acc[q] += part[(size_t)c * 4 + q];
+  for (int q = 0; q < 4; ++q) out[q] = (double)acc[q];
+  return bad ? 3 : 0;
+}
+
 // One stage's residual L, dL/dt and Gauss-theorem gradients for a given dt (for unit tests).
 // L, Lt: [5][ncell]; Gn, Gt: [3][5][ncell]
 int orc_stage_residual(const orc_params* p, const double* Q, const double* G, double dt, double* L, double* Lt,
