@@ -133,6 +133,19 @@ int cgks_get_state(const cgks_ctx* ctx, double* Q, double* gradQ);
 /* Simulated time, completed steps, and the last time step used. */
 int cgks_get_time(const cgks_ctx* ctx, double* t, int64_t* steps, double* last_dt);
 
+/* Flow diagnostics of the current state (DESIGN R35):
+ *   out[0] = int 1/2 rho |U|^2 dV            (kinetic energy)
+ *   out[1] = int mu(T) |curl U|^2 dV        (solenoidal / enstrophy dissipation)
+ *   out[2] = int 4/3 mu(T) (div U)^2 dV     (dilatational dissipation)
+ *   out[3] = int rho dV                      (mass)
+ * over the domain, by 3-point Gauss-Legendre quadrature per active axis of every cell's own
+ * reconstruction (CGKS-5th quartic with GENO when nonlinear; GKS-2nd limited linear), mu(T) by the
+ * context's viscosity law.  Unnormalised: divide by rho0 U0^2 |Omega| for the paper's E_k and eps.
+ * out: host array of 4 doubles, caller-owned.  Synchronous; does not change the state.  Reuses the
+ * reconstruction buffer.  CGKS_ERR_CONFIG for decomposed contexts (nproc > 1) in this version;
+ * CGKS_ERR_NUMERICAL if a result is not finite. */
+int cgks_diagnostics(cgks_ctx* ctx, double out[4]);
+
 /* Message of the last error (includes cell (i,j,k) and stage for positivity failures). */
 const char* cgks_last_error(const cgks_ctx* ctx);
 

@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
     L.cgks_step.argtypes = [vp, ctypes.c_int]
     L.cgks_get_state.argtypes = [vp, vp, vp]
     L.cgks_get_time.argtypes = [vp, dp, ctypes.POINTER(ctypes.c_int64), dp]
+    L.cgks_diagnostics.argtypes = [vp, dp]
     L.cgks_last_error.argtypes = [vp]
     L.cgks_last_error.restype = ctypes.c_char_p
     L.cgks_launches_per_step.argtypes = [vp]
@@ -238,6 +239,13 @@ class Solver:
         d = ctypes.c_double()
         self._check(self._L.cgks_get_time(self.ctx, ctypes.byref(t), ctypes.byref(s), ctypes.byref(d)))
         return t.value, s.value, d.value
+
+    def diagnostics(self):
+        """cgks_diagnostics: (int 1/2 rho|U|^2 dV, int mu|curl U|^2 dV, int 4/3 mu (div U)^2 dV,
+        int rho dV) of the current state, by quadrature of the reconstruction (unnormalised)."""
+        out = np.zeros(4)
+        self._check(self._L.cgks_diagnostics(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
 
     def last_error(self):
         return self._L.cgks_last_error(self.ctx).decode()

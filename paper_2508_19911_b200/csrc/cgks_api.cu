@@ -97,6 +97,9 @@ struct cgks_ctx {
   double* rec = nullptr;
   double* face[3] = {nullptr, nullptr, nullptr};
   double* gtab[3] = {nullptr, nullptr, nullptr};
+  double* dtab = nullptr;   // diagnostics quadrature weights [node][value, d/dxi_a][nb] (CGKS-5th)
+  double* dpart = nullptr;  // diagnostics block partials
+  long long dpart_n = 0;
   double* staging = nullptr;
   TimeState* ts = nullptr;
   ErrState* err = nullptr;
@@ -159,7 +162,7 @@ static LaunchEnv env_of(cgks_ctx* ctx) {
   return e;
 }
 
-static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   StageArgs a;
   a.Uin = Uin;
   a.Uout = Uout;
@@ -179,6 +182,11 @@ static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
   a.box = ctx->box;
+  return a;
+}
+
+static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+  StageArgs a = stage_args(ctx, Uin, Uout);
   LaunchEnv env = env_of(ctx);
   int rc = ctx->ops->stage(env, a, mode, stage);
   return rc ? CGKS_ERR_CUDA : CGKS_OK;
@@ -510,6 +518,27 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       }
     }
   }
+  // diagnostics quadrature (NEXT-3, R35): basis values and reference derivatives at the 3-point
+  // Gauss-Legendre nodes of every active axis, node order x fastest (k_diag)
+  if (ctx->scheme_id == CGKS_CGKS5) {
+    const int nb = ctx->cls.nb;
+    const int np = dim == 3 ? 27 : (dim == 2 ? 9 : 3);
+    const double gx[3] = {-0.5 * std::sqrt(0.6), 0.0, 0.5 * std::sqrt(0.6)};
+    std::vector<double> w((size_t)np * 4 * nb, 0.0), val(nb), der(3 * nb);
+    for (int pnode = 0; pnode < np; ++pnode) {
+      const double x[3] = {gx[pnode % 3], dim >= 2 ? gx[(pnode / 3) % 3] : 0.0, dim >= 3 ? gx[pnode / 9] : 0.0};
+      basis_at(ctx->cls, x, val.data(), der.data());
+      for (int kk = 0; kk < nb; ++kk) {
+        w[((size_t)pnode * 4 + 0) * nb + kk] = val[kk];
+        for (int a = 0; a < 3; ++a) w[((size_t)pnode * 4 + 1 + a) * nb + kk] = der[a * nb + kk];
+      }
+    }
+    if (!alloc(&ctx->dtab, (long long)w.size()) ||
+        cudaMemcpy(ctx->dtab, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_msg(ctx, "diagnostics table upload failed");
+      return fail(CGKS_ERR_CUDA);
+    }
+  }
   cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
   // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
   // group stepped by cgks_step_group (halo copies on one device)
@@ -828,6 +857,46 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
   return CGKS_OK;
 }
 
+int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
+  if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (ctx->nranks > 1 || ctx->comm_mode == 2) {
+    set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
+    return CGKS_ERR_CONFIG;
+  }
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  StageArgs a = stage_args(ctx, ctx->U[ctx->cur], nullptr);
+  const int np = ctx->dim == 3 ? 27 : (ctx->dim == 2 ? 9 : 3);
+  const long long need = 4 * ((ctx->ncell * np + 255) / 256);
+  if (need > ctx->dpart_n) {
+    if (ctx->dpart) cudaFree(ctx->dpart);
+    ctx->dpart = nullptr;
+    if (cudaMalloc((void**)&ctx->dpart, sizeof(double) * need) != cudaSuccess) {
+      ctx->dpart = nullptr;
+      set_msg(ctx, "cgks_diagnostics: out of device memory");
+      return CGKS_ERR_CUDA;
+    }
+    ctx->dpart_n = need;
+  }
+  LaunchEnv env = env_of(ctx);
+  env.prof = false;
+  long long nblk = 0;
+  if (ctx->ops->diag(env, a, ctx->dtab, ctx->dpart, &nblk)) return CGKS_ERR_CUDA;
+  std::vector<double> h((size_t)nblk * 4);
+  CK(cudaMemcpyAsync(h.data(), ctx->dpart, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  long double acc[4] = {0, 0, 0, 0};  // fixed order: deterministic
+  for (long long b = 0; b < nblk; ++b)
+    for (int q = 0; q < 4; ++q) acc[q] += h[(size_t)b * 4 + q];
+  for (int q = 0; q < 4; ++q) out[q] = (double)acc[q];
+  for (int q = 0; q < 4; ++q)
+    if (!(out[q] == out[q])) {
+      set_msg(ctx, "cgks_diagnostics: non-finite result (non-positive reconstructed density?)");
+      return CGKS_ERR_NUMERICAL;
+    }
+  return CGKS_OK;
+}
+
 const char* cgks_last_error(const cgks_ctx* ctx) { return ctx ? ctx->msg : "null context"; }
 
 int cgks_launches_per_step(const cgks_ctx* ctx) { return ctx ? ctx->launches_per_step : 0; }
@@ -1021,8 +1090,8 @@ void cgks_destroy(cgks_ctx* ctx) {
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
   if (g_const_owner == ctx) g_const_owner = nullptr;
-  double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us, ctx->carry, ctx->rec, ctx->staging,
-                    ctx->face[0], ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2]};
+  double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
+                    ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);

@@ -48,6 +48,8 @@ struct DimOps {
   int (*step_end)(LaunchEnv& env, TimeState* ts, ErrState* err);
   int (*pack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
+  // flow diagnostics of a.Uin (reconstruction + quadrature); *nblk = number of 4-double block partials
+  int (*diag)(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk);
 };
 
 extern const DimOps kOps1, kOps2, kOps3;

@@ -837,4 +837,114 @@ static __global__ void k_unpack(const double* __restrict__ src, double* __restri
   dst[t] = src[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.plane + r];
 }
 
+// ---------------------------------------------------------------------------
+// Flow diagnostics (reading R35): quadrature of each cell's
+// reconstruction at the 3-point Gauss-Legendre nodes per active axis.  One thread per (cell, node);
+// per block: sums of 1/2 rho |U|^2, mu(T) |curl U|^2, 4/3 mu(T) (div U)^2, rho (times weight and cell
+// volume) in a fixed shuffle / shared-memory order, written to part[block][4].
+// wtab (CGKS-5th): [node][value, d/dxi_0, d/dxi_1, d/dxi_2][NB] basis weights in reference units.
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct DiagQuad {
+  static constexpr int NP = DIM == 3 ? 27 : (DIM == 2 ? 9 : 3);
+  static constexpr int BLOCK = 256;
+};
+
+template <int DIM, bool COMPACT>
+__global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, const double* __restrict__ rec,
+                                               const double* __restrict__ wtab, double* __restrict__ part) {
+  constexpr int NP = DiagQuad<DIM>::NP;
+  constexpr int NB = Sten<DIM>::NB;
+  constexpr int NV = COMPACT ? 20 : 5;
+  constexpr int NW = COMPACT ? NP * 4 * NB : 1;
+  __shared__ double wt[NW];
+  __shared__ double red[8][4];
+  if (COMPACT)
+    for (int q = threadIdx.x; q < NW; q += blockDim.x) wt[q] = wtab[q];
+  __syncthreads();
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long cell = t / NP;
+  const int p = (int)(t % NP);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (cell < nc) {
+    const int i = (int)(cell % c_geo.n[0]);
+    const int j = (int)((cell / c_geo.n[0]) % c_geo.n[1]);
+    const int k = (int)(cell / c_geo.plane);
+    // Gauss-Legendre node of this thread (3 per active axis on [-1/2, 1/2]) and its weight
+    const double gx[3] = {-0.38729833462074168852, 0.0, 0.38729833462074168852};  // sqrt(3/5)/2
+    const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    const int pi = p % 3, pj = (p / 3) % 3, pk = p / 9;
+    const double xi[3] = {gx[pi], DIM >= 2 ? gx[pj] : 0.0, DIM >= 3 ? gx[pk] : 0.0};
+    const double w = gw[pi] * (DIM >= 2 ? gw[pj] : 1.0) * (DIM >= 3 ? gw[pk] : 1.0) * c_geo.h[0] * c_geo.h[1] * c_geo.h[2];
+    double W[5], dW[3][5];
+    if (COMPACT) {
+      const double* cb = rec + eidx(NB * 5, 0, i, j, k);
+      const long long ep = c_geo.eplane;
+      const double* wv = wt + p * 4 * NB;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        double val = __ldg(U + sidx(NV, v, i, j, k)), d0 = 0.0, d1 = 0.0, d2 = 0.0;
+        for (int kk = 0; kk < NB; ++kk) {
+          const double c = __ldg(cb + (long long)(kk * 5 + v) * ep);
+          val = fma(c, wv[kk], val);
+          d0 = fma(c, wv[NB + kk], d0);
+          d1 = fma(c, wv[2 * NB + kk], d1);
+          d2 = fma(c, wv[3 * NB + kk], d2);
+        }
+        W[v] = val;
+        dW[0][v] = d0 * c_geo.ih[0];
+        dW[1][v] = d1 * c_geo.ih[1];
+        dW[2][v] = d2 * c_geo.ih[2];
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        W[v] = __ldg(U + sidx(NV, v, i, j, k));
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double sl = __ldg(rec + eidx(15, a * 5 + v, i, j, k));  // limited slope, reference units
+          W[v] = fma(sl, xi[a], W[v]);
+          dW[a][v] = sl * c_geo.ih[a];
+        }
+      }
+    }
+    const double ir = 1.0 / W[0];
+    double Uv[3], dU[3][3];  // dU[a][b] = d U_b / d x_a
+#pragma unroll
+    for (int b = 0; b < 3; ++b) Uv[b] = W[1 + b] * ir;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) dU[a][b] = (dW[a][1 + b] - Uv[b] * dW[a][0]) * ir;
+    const double ke = 0.5 * W[0] * (Uv[0] * Uv[0] + Uv[1] * Uv[1] + Uv[2] * Uv[2]);
+    const double pr = (c_geo.gamma - 1.0) * (W[4] - ke);
+    double mu = c_geo.mu;
+    if (c_geo.suth > 0.0) {  // Sutherland law
+      const double T = pr * ir;
+      mu = c_geo.mu * (1.0 + c_geo.suth) * T * sqrt(T) / (T + c_geo.suth);
+    }
+    const double o0 = dU[1][2] - dU[2][1], o1 = dU[2][0] - dU[0][2], o2 = dU[0][1] - dU[1][0];
+    const double dv = dU[0][0] + dU[1][1] + dU[2][2];
+    acc[0] = w * ke;
+    acc[1] = w * mu * (o0 * o0 + o1 * o1 + o2 * o2);
+    acc[2] = w * (4.0 / 3.0) * mu * dv * dv;
+    acc[3] = w * W[0];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
+  const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[wp][q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double sum = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sum += red[q][threadIdx.x];
+    part[(long long)blockIdx.x * 4 + threadIdx.x] = sum;
+  }
+}
+
 }  // namespace cgks

@@ -147,6 +147,34 @@ int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   return stage_t<false, true, true>(env, a, mode, stage);
 }
 
+// diagnostics: reconstruction of the state a.Uin, then quadrature per (cell, node); returns the number of
+// block partials written to part (4 doubles each)
+template <bool COMPACT, bool NONLIN, bool BOX>
+int diag_t(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk) {
+  if (COMPACT) {
+    int rc = recon5_launch<NONLIN, BOX>(env, a);
+    if (rc) return rc;
+  } else {
+    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  }
+  constexpr int NP = DiagQuad<D>::NP;
+  *nblk = (a.ncell * NP + 255) / 256;
+  LAUNCH("diag", (k_diag<D, COMPACT>), a.ncell * NP, 256, (const double*)a.Uin, (const double*)a.rec, wtab, part);
+  return 0;
+}
+
+int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk) {
+  const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
+  if (c && !nl && !b) return diag_t<true, false, false>(env, a, wtab, part, nblk);
+  if (c && nl && !b) return diag_t<true, true, false>(env, a, wtab, part, nblk);
+  if (c && !nl && b) return diag_t<true, false, true>(env, a, wtab, part, nblk);
+  if (c && nl && b) return diag_t<true, true, true>(env, a, wtab, part, nblk);
+  if (!c && !nl && !b) return diag_t<false, false, false>(env, a, wtab, part, nblk);
+  if (!c && nl && !b) return diag_t<false, true, false>(env, a, wtab, part, nblk);
+  if (!c && !nl && b) return diag_t<false, false, true>(env, a, wtab, part, nblk);
+  return diag_t<false, true, true>(env, a, wtab, part, nblk);
+}
+
 int upload_fn(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s) {
   if (cudaMemcpyToSymbolAsync(c_geo, &g, sizeof(Geo), 0, cudaMemcpyHostToDevice, s) != cudaSuccess) return 5;
   if (cudaMemcpyToSymbolAsync(c_fc, &fc, sizeof(FluxConst), 0, cudaMemcpyHostToDevice, s) != cudaSuccess) return 5;

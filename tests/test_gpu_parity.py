@@ -269,3 +269,36 @@ def test_full_size_supersonic_tgv116_sampled():
     # the paper's CGKS-5th mesh (116^3, nonlinear), one step on the full grid, sampled against the oracle
     e = _sampled_one_step(tgv_supersonic(116), 1, samples=8)
     assert e <= 1e-10, e
+
+
+# ---- flow diagnostics (E_k, solenoidal / dilatational dissipation, mass) -----
+@pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 0), (0, 1)])
+def test_diagnostics_parity(scheme, nl):
+    """cgks_diagnostics against the oracle's quadrature of the reconstructed state, before and after
+    5 steps, on the high-speed TGV (Sutherland mu) at 20^3: relative difference <= 1e-12 (only the
+    summation order differs)."""
+    case = tgv_supersonic(20)
+    d = case.problem_kwargs()
+    d["nonlinear"] = nl
+    prob = oracle.Problem(**d, scheme=scheme, time_scheme=2 if scheme == 1 else 1)
+    S = _gpu().from_case(case, scheme=scheme, nonlinear=nl)
+    S.set_state(case.Q, case.G)
+    for steps in (0, 5):
+        S.step(steps)
+        Qg, Gg = S.get_state()
+        dg = S.diagnostics()
+        do = oracle.diagnostics(prob, Qg, Gg if scheme == 1 else None)
+        assert np.all(np.abs(dg - do) <= 1e-12 * np.abs(do) + 1e-300), (steps, dg, do)
+    S.close()
+
+
+def test_diagnostics_tgv128_value():
+    # bench-size TGV at t = 0: E_k / |Omega| = 1/8 (rho = 1, U0 = 1) to the reconstruction's accuracy
+    case = tgv(128)
+    S = _gpu().from_case(case, scheme=1)
+    S.set_state(case.Q, case.G)
+    d = S.diagnostics()
+    S.close()
+    V = (2 * np.pi) ** 3
+    assert abs(d[0] / V - 0.125) < 1e-9 and abs(d[3] / V - 1.0) < 1e-12
+    assert abs(d[1] / (case.mu * V) - 0.75) < 1e-6
