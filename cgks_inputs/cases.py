@@ -208,31 +208,91 @@ def tgv(n: int = 64, Ma: float = 0.1, Re: float = 1600.0, Pr: float = 0.72, gamm
                 note=f"TGV Ma={Ma} Re={Re} rho=1 (BASELINE configs[1]); exact separable averages")
 
 
-def _tgv_supersonic_prim(Ma, gamma):
-    U0 = math.sqrt(gamma) * Ma  # U0 = sqrt(gamma) Ma, rho0 = p0 = T0 = 1
+# 1-D trigonometric polynomials {("c"|"s", k): coef} (cos kx / sin kx), for exact separable cell averages
+def _tp_mul(p, q):
+    out = {}
+    for (ta, ka), ca in p.items():
+        for (tb, kb), cb in q.items():
+            c = 0.5 * ca * cb
+            if ta == "c" and tb == "c":
+                terms = [("c", ka - kb, c), ("c", ka + kb, c)]
+            elif ta == "s" and tb == "s":
+                terms = [("c", ka - kb, c), ("c", ka + kb, -c)]
+            elif ta == "s":  # sin a cos b
+                terms = [("s", ka + kb, c), ("s", ka - kb, c)]
+            else:  # cos a sin b
+                terms = [("s", ka + kb, c), ("s", kb - ka, c)]
+            for t, k, cc in terms:
+                if k < 0:  # cos(-k x) = cos(k x), sin(-k x) = -sin(k x)
+                    k, cc = -k, (cc if t == "c" else -cc)
+                if t == "s" and k == 0:
+                    continue
+                out[(t, k)] = out.get((t, k), 0.0) + cc
+    return out
 
-    def f(x, y, z):
-        s = 1.0 + (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
-        u = U0 * np.sin(x) * np.cos(y) * np.cos(z)
-        v = -U0 * np.cos(x) * np.sin(y) * np.cos(z)
-        return s, u, v, np.zeros_like(u), s  # rho = rho0 s, p = p0 s: T = p / rho = 1
-    return f
+
+def _tp_avg(p, a, b):
+    h = b - a
+    r = np.zeros_like(a)
+    for (t, k), c in p.items():
+        if k == 0:
+            r = r + c
+        elif t == "c":
+            r = r + c * (np.sin(k * b) - np.sin(k * a)) / (k * h)
+        else:
+            r = r + c * (np.cos(k * a) - np.cos(k * b)) / (k * h)
+    return r
 
 
-def tgv_supersonic(n: int = 116, Ma: float = 2.0, Re: float = 1600.0, Pr: float = 0.7, gamma: float = 1.4,
-                   nq: int = 6) -> Case:
+def _tp_pt(p, x):
+    r = np.zeros_like(x)
+    for (t, k), c in p.items():
+        r = r + c * (np.cos(k * x) if t == "c" else np.sin(k * x))
+    return r
+
+
+def tgv_supersonic(n: int = 116, Ma: float = 2.0, Re: float = 1600.0, Pr: float = 0.7, gamma: float = 1.4) -> Case:
     """High-speed Taylor-Green vortex: periodic [-pi, pi]^3 (L = 1),
     U = U0 sin x cos y cos z, V = -U0 cos x sin y cos z, W = 0, rho = p = 1 + (cos 2x + cos 2y)(cos 2z + 2)/16,
     U0 = sqrt(gamma) Ma, Re = 1600, Pr = 0.7, Sutherland viscosity mu(T) = mu0 1.4042 T^1.5 / (T + 0.4042),
-    mu0 = rho0 U0 L / Re.  Cell averages and averaged gradients by nq-point Gauss-Legendre per axis
-    (trigonometric data of frequency <= 4: nq = 6 is exact to rounding at the paper's 116^3).  Nonlinear
-    schemes (GENO / Venkatakrishnan) as in the paper."""
+    mu0 = rho0 U0 L / Re.  Every conservative field is a sum of separable trigonometric products, so the
+    cell averages and averaged gradients (Gauss theorem) are exact.  Nonlinear schemes (GENO /
+    Venkatakrishnan) as in the paper."""
     nn = (n, n, n)
     lo, hi = (-PI, -PI, -PI), (PI, PI, PI)
-    Q, G = gl_average(_tgv_supersonic_prim(Ma, gamma), nn, lo, hi, gamma, nq=nq)
     U0 = math.sqrt(gamma) * Ma
+    one, c1, s1, c2 = {("c", 0): 1.0}, {("c", 1): 1.0}, {("s", 1): 1.0}, {("c", 2): 1.0}
+    # s = rho / rho0 = p / p0 = 1 + (c2x c2z + 2 c2x + c2y c2z + 2 c2y) / 16, as (coef, fx, fy, fz)
+    sfac = [(1.0, one, one, one), (1 / 16, c2, one, c2), (2 / 16, c2, one, one), (1 / 16, one, c2, c2),
+            (2 / 16, one, c2, one)]
+
+    def times(terms, c, fx, fy, fz):
+        return [(c * t[0], _tp_mul(t[1], fx), _tp_mul(t[2], fy), _tp_mul(t[3], fz)) for t in terms]
+
+    fields = {
+        0: sfac,
+        1: times(sfac, U0, s1, c1, c1),
+        2: times(sfac, -U0, c1, s1, c1),
+        3: [],
+        4: [(t[0] / (gamma - 1.0),) + t[1:] for t in sfac]
+        + times(sfac, 0.5 * U0 * U0, _tp_mul(s1, s1), _tp_mul(c1, c1), _tp_mul(c1, c1))
+        + times(sfac, 0.5 * U0 * U0, _tp_mul(c1, c1), _tp_mul(s1, s1), _tp_mul(c1, c1)),
+    }
+    h = 2 * PI / n
+    e = -PI + h * np.arange(n + 1)
+    a, b = e[:-1], e[1:]
+    Q = np.zeros((5, n, n, n))
+    G = np.zeros((3, 5, n, n, n))
+    for v, tl in fields.items():
+        for (c, fx, fy, fz) in tl:
+            Ax, Ay, Az = _tp_avg(fx, a, b), _tp_avg(fy, a, b), _tp_avg(fz, a, b)
+            Dx, Dy, Dz = [(_tp_pt(f, b) - _tp_pt(f, a)) / h for f in (fx, fy, fz)]
+            Q[v] += c * Az[:, None, None] * Ay[None, :, None] * Ax[None, None, :]
+            G[0, v] += c * Az[:, None, None] * Ay[None, :, None] * Dx[None, None, :]
+            G[1, v] += c * Az[:, None, None] * Dy[None, :, None] * Ax[None, None, :]
+            G[2, v] += c * Dz[:, None, None] * Ay[None, :, None] * Ax[None, None, :]
     c = Case("tgv_ss", nn, lo, hi, Q, G, gamma=gamma, mu=U0 / Re, Pr=Pr, cfl=0.3, nonlinear=1, steps=100,
-             note=f"high-speed TGV Ma={Ma} Re={Re} Sutherland (P:455-474)")
+             note=f"high-speed TGV Ma={Ma} Re={Re} Sutherland (P:455-474); exact separable averages")
     c.sutherland_S = 0.4042
     return c
 
