@@ -39,17 +39,19 @@ struct FluxConst {
 // K = 3.75, 25 terms (Shepherd-Laframboise form; coefficients computed by tools/erfc_fit.py),
 // erfc(-a) = 2 - erfc(a).  Branch-free; one reciprocal.  Max relative error (tools/erfc_fit.py):
 // 1.2e-15 for |z| <= 3, 6e-14 at |z| = 26 (the rounding of z^2 inside exp).
+// Chebyshev coefficients of erfc_e (tools/erfc_fit.py); on the device a __constant__ table, so the
+// FMAs take them as constant-bank operands instead of materialising 64-bit immediates
+#define CGKS_ERFC_COEFS 2.3551578691348034, -0.004590054580646478, -0.08424913336651792, 0.05920993999819189, -0.026658668435305753, 0.009074997670705265, -0.002413163540417608, 0.0004907758365258086, -6.916973302501207e-05, 4.13902798607301e-06, 7.74038306619849e-07, -2.1886401049234397e-07, 1.076499946567091e-08, 4.521959811218287e-09, -7.754400208831351e-10, -6.318088340886684e-11, 2.86879501093067e-11, 1.9455868545777347e-13, -9.65469674843344e-13, 3.25254814814874e-14, 3.3478119482868056e-14, -1.864562880419313e-15, -1.2507950530688648e-15, 7.418235256624044e-17, 5.0681489047961116e-17
+static __constant__ double c_erfc[25] = {CGKS_ERFC_COEFS};
+
 template <typename T>
 HD T erfc_e(T z, T e) {
   constexpr double K = 3.75;
-  constexpr double C[25] = {
-      2.3551578691348034, -0.004590054580646478, -0.08424913336651792, 0.05920993999819189,
-      -0.026658668435305753, 0.009074997670705265, -0.002413163540417608, 0.0004907758365258086,
-      -6.916973302501207e-05, 4.13902798607301e-06, 7.74038306619849e-07, -2.1886401049234397e-07,
-      1.076499946567091e-08, 4.521959811218287e-09, -7.754400208831351e-10, -6.318088340886684e-11,
-      2.86879501093067e-11, 1.9455868545777347e-13, -9.65469674843344e-13, 3.25254814814874e-14,
-      3.3478119482868056e-14, -1.864562880419313e-15, -1.2507950530688648e-15, 7.418235256624044e-17,
-      5.0681489047961116e-17};
+#ifdef __CUDA_ARCH__
+  const double* C = c_erfc;
+#else
+  constexpr double C[25] = {CGKS_ERFC_COEFS};
+#endif
   const T a = fabs(z);
   const T q = 1.0 + 2.0 * a;
   const T r = 1.0 / ((a + K) * q);

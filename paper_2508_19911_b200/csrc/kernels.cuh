@@ -615,30 +615,41 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       for (int q = 10; q < NR; ++q) face[base + (q + 10) * fpl] = y[q];
     }
   } else {
-    // Gauss-point sum through shared memory: every lane writes its NR values into its warp's own
-    // scratch columns (row q, column skewed by q: conflict-free, and no other warp touches these
-    // columns, so a warp barrier suffices), then the LPF lanes of a face each sum a strided
-    // subset of the NF face outputs over the NG Gauss points in a fixed order and store them.
-    __syncwarp();
-    const int wb = lane & ~31, lw = lane & 31;
+    // Gauss-point sum by a reduce-scatter over the face's lanes (lane = 2 gp + side): round 1 with
+    // partner gp^1 halves the 20 values (even gp keeps y[0..9] = Fn Ft, odd gp keeps y[10..19] = this
+    // side's Qn Qt), round 2 with partner gp^2 halves again (NG = 4); each lane then holds NR / NG
+    // fully summed outputs ((g0 + g1) + (g2 + g3) in every lane: deterministic) and stores them; the
+    // side-1 lanes skip the duplicate Fn Ft.
+    constexpr int H = NR / 2;
+    constexpr int NOUT = NR / NG;
+    const bool up = gp & 1;
+    double z[H];
 #pragma unroll
-    for (int q = 0; q < NR; ++q) scratch[q * 128 + wb + ((lw + q) & 31)] = y[q];
-    __syncwarp();
-    constexpr int LPF = FT::LPF;
-    const int r = lane & (LPF - 1);
-    const int m0 = lw - r;  // first lane of this face within the warp
+    for (int q = 0; q < H; ++q) {
+      const double send = up ? y[q] : y[H + q];
+      const double keep = up ? y[H + q] : y[q];
+      z[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    int o0 = up ? H : 0;  // first of this lane's outputs among the side's NR values
+    double zz[NOUT];
+    if constexpr (NG > 2) {
+      const bool up2 = gp & 2;
 #pragma unroll
-    for (int it = 0; it < (NF + LPF - 1) / LPF; ++it) {
-      const int oo = r + it * LPF;
-      if (oo < NF) {
-        // outputs 0..19 from the side-0 lanes (Fn Ft QLn QLt), 20..29 from the side-1 lanes (QRn QRt)
-        const int sd = oo < 20 ? 0 : 1, slot = oo < 20 ? oo : oo - 10;
-        const double* row = scratch + slot * 128 + wb;
-        const int m = m0 + sd + slot;
-        double sum = row[m & 31] + row[(m + 2) & 31];
-        if (NG > 2) sum += row[(m + 4) & 31] + row[(m + 6) & 31];
-        if (valid) face[base + oo * fpl] = sum;
+      for (int q = 0; q < H / 2; ++q) {
+        const double send = up2 ? z[q] : z[H / 2 + q];
+        const double keep = up2 ? z[H / 2 + q] : z[q];
+        zz[q] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
       }
+      o0 += up2 ? H / 2 : 0;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) zz[q] = z[q];
+    }
+    // face slots: 0..9 Fn Ft, 10..19 QLn QLt (side 0), 20..29 QRn QRt (side 1)
+    if (valid && (o0 >= 10 || side == 0)) {
+      double* dst = face + base + (long long)(o0 + (o0 >= 10 && side ? 10 : 0)) * fpl;
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) dst[q * fpl] = zz[q];
     }
   }
 }
