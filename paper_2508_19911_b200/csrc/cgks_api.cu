@@ -1,10 +1,13 @@
 // cgks_api.cu -- host side of the C ABI declared in include/cgks.h: context,
 // device memory, the S2O4 / S1O2 stage driver and per-kernel profiling.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -98,6 +101,11 @@ struct cgks_ctx {
   double* face[3] = {nullptr, nullptr, nullptr};
   double* gtab[3] = {nullptr, nullptr, nullptr};
   double* dtab = nullptr;   // diagnostics quadrature weights [node][value, d/dxi_a][nb] (CGKS-5th)
+  // TMA descriptors of the flux tiles per normal axis: reconstruction fields, and the cell averages
+  // of each stage input buffer (0 = U[0], 1 = U[1], 2 = Us)
+  CUtensorMap tm_rec[3];
+  CUtensorMap tm_U[3][3];
+  bool use_tma = false;
   double* dpart = nullptr;  // diagnostics block partials
   long long dpart_n = 0;
   double* staging = nullptr;
@@ -182,6 +190,14 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
   a.box = ctx->box;
+  if (ctx->use_tma) {
+    const int b = Uin == ctx->U[0] ? 0 : (Uin == ctx->U[1] ? 1 : (Uin == ctx->Us ? 2 : -1));
+    if (b >= 0) {
+      a.tm_rec = ctx->tm_rec;
+      a.tm_U = ctx->tm_U[b];
+      a.use_tma = 1;
+    }
+  }
   return a;
 }
 
@@ -479,6 +495,44 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       cudaMalloc((void**)&ctx->err, sizeof(ErrState)) != cudaSuccess) {
     set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
     return fail(CGKS_ERR_CUDA);
+  }
+  // TMA descriptors (3-D CGKS-5th, periodic or z-decomposed, even x extent so that rows are
+  // multiples of 16 bytes): 4-D views [z][field][y][x] of the reconstruction fields and of each
+  // state buffer, boxes = the flux tiles of each normal axis; CGKS_NO_TMA=1 disables
+  if (ctx->scheme_id == CGKS_CGKS5 && dim == 3 && !ctx->box && g.en[0] % 2 == 0 && g.n[0] % 2 == 0 &&
+      std::getenv("CGKS_NO_TMA") == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+        q == cudaDriverEntryPointSuccess) {
+      auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      const cuuint32_t es[4] = {1, 1, 1, 1};
+      bool good = true;
+      for (int a = 0; a < 3 && good; ++a) {
+        int tx = 0, tn = 0;
+        ctx->ops->flux_tile(a, &tx, &tn);
+        const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
+        {
+          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)g.en[1], (cuuint64_t)nrec, (cuuint64_t)g.en[2]};
+          const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.eplane * 8, (cuuint64_t)g.eplane * nrec * 8};
+          const cuuint32_t box[4] = {(cuuint32_t)tx, by, (cuuint32_t)nrec, bz};
+          good = good && encode(&ctx->tm_rec[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->rec, dims, str, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        double* bufs[3] = {ctx->U[0], ctx->U[1], ctx->Us};
+        for (int b = 0; b < 3 && good; ++b) {
+          const cuuint64_t dims[4] = {(cuuint64_t)g.n[0], (cuuint64_t)g.n[1], (cuuint64_t)NV,
+                                      (cuuint64_t)(g.n[2] + 2 * g.zoff)};
+          const cuuint64_t str[3] = {(cuuint64_t)g.n[0] * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.plane * NV * 8};
+          const cuuint32_t box[4] = {(cuuint32_t)tx, by, 5, bz};
+          good = encode(&ctx->tm_U[b][a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[b], dims, str, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+      }
+      ctx->use_tma = good;
+    }
   }
   // face evaluation tables per axis: [side][quantity][nb + 1] (quantity 0 value, 1 d/dn, 2 d/dtA, 3 d/dtB);
   // entry = (+-1/2)^{d_n} s^{d_tA + d_tB} / d! with one exponent lowered for derivatives, minus the

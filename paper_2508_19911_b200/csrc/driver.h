@@ -3,6 +3,7 @@
 // Each dimension is compiled separately (parallel builds); each owns its constant memory,
 // so the ABI uploads the context's parameters through every unit it uses.
 #pragma once
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 
 #include <string>
@@ -37,6 +38,10 @@ struct StageArgs {
   int scheme;     // 0 GKS-2nd, 1 CGKS-5th
   int nonlinear;
   int box;
+  // TMA descriptors of the flux tiles per normal axis (reconstruction fields; cell averages of Uin)
+  const CUtensorMap* tm_rec = nullptr;
+  const CUtensorMap* tm_U = nullptr;
+  int use_tma = 0;
 };
 
 struct DimOps {
@@ -50,6 +55,8 @@ struct DimOps {
   int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   // flow diagnostics of a.Uin (reconstruction + quadrature); *nblk = number of 4-double block partials
   int (*diag)(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk);
+  // flux tile extent (cells along x, cells along the normal axis) for the TMA boxes, CGKS-5th
+  void (*flux_tile)(int ax, int* tx, int* tn);
 };
 
 extern const DimOps kOps1, kOps2, kOps3;

@@ -11,6 +11,7 @@
 //
 // Layout of every cell field: [z][field][y][x], x fastest (coalesced along x).
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors; no driver-API calls on the device)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -125,6 +126,39 @@ __device__ __forceinline__ void cp_async8s(unsigned smem_addr, const double* gme
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// TMA (cp.async.bulk.tensor) tile load completing on an mbarrier, and the mbarrier primitives
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(b)
+      : "memory");
+}
 
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
                                            int j, int k) {
@@ -396,32 +430,46 @@ struct FluxTile {
   static constexpr int FPB = 128 / LPF;                      // faces per block
   static constexpr int FY = AX == 0 ? 1 : 4;                 // faces along the normal axis
   static constexpr int FX = FPB / FY;                        // faces along x
-  static constexpr int NT = AX == 0 ? FPB + 1 : FX * (FY + 1);  // tile cells
+  // tile cells (x-faces: cells i0 - 2 .. i0 + FPB - 1, of which the first feeds no face: TMA rows
+  // start at an even cell and span a multiple of 16 bytes)
+  static constexpr int NT = AX == 0 ? FPB + 2 : FX * (FY + 1);
+  static constexpr int TX = AX == 0 ? NT : FX;               // cells of the tile along x
+  static constexpr int TN = AX == 0 ? 1 : FY + 1;            // cells of the tile along the normal axis
   static constexpr int NB = Sten<DIM>::NB;
   static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
   static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
   static constexpr int NQ = DIM + 1;                         // value + DIM derivatives
   static constexpr int TS = NB + 1;                          // padded per-(side, quantity) row (no bank conflicts)
   static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
+  // Tile layout = the TMA box layout of the [z][field][y][x] arrays: reconstruction fields, then the
+  // cell averages.  x- and y-faces: [field][cell] (field stride NT); z-faces: [cz][field][cx]
+  // (field stride FX).  cbase(c) = offset of cell c = (normal index) * TX + x index.
+  static constexpr int FS = AX == 2 ? FX : NT;
+  __host__ __device__ static constexpr int cbase(int c, int nfield) {
+    return AX == 2 ? (c / FX) * nfield * FX + c % FX : c;
+  }
+  static constexpr int STILE = (NREC * NT + 15) / 16 * 16;   // start of the cell-average tile (128-byte aligned)
   // the tile region is reused for parking slots 20..39 after the evaluation
-  static constexpr int TILE = NFLD * NT > 20 * 128 ? NFLD * NT : 20 * 128;
-  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128); }
+  static constexpr int TILE = STILE + 5 * NT > 20 * 128 ? STILE + 5 * NT : 20 * 128;
+  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128) + 16; }
 };
 
 template <int DIM, int AX, bool COMPACT, bool BOX>
 __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
                                                const double* __restrict__ gtab, double* __restrict__ face,
                                                const TimeState* __restrict__ ts, ErrState* __restrict__ err,
-                                               int stage) {
+                                               int stage, const __grid_constant__ CUtensorMap tm_rec,
+                                               const __grid_constant__ CUtensorMap tm_U, int use_tma) {
   using FT = FluxTile<DIM, AX, COMPACT>;
   constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT;
   constexpr int NV = COMPACT ? 20 : 5;
   constexpr int NF = COMPACT ? 30 : 10;
   constexpr int NR = COMPACT ? 20 : 10;  // values each lane reduces over the Gauss points
-  extern __shared__ double smem[];
-  double* tile = smem;                            // [NFLD][NT]: reconstruction fields, then Q
+  extern __shared__ __align__(128) double smem[];
+  double* tile = smem;                            // reconstruction fields, then Q (TMA box layout)
   double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
   double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
+  uint64_t* bar = reinterpret_cast<uint64_t*>(scratch + 20 * 128);  // TMA completion barrier
   if (err->code) return;
   constexpr int FX = FT::FX, FY = FT::FY;
   const int fn0 = c_geo.fn[AX][0];
@@ -432,14 +480,30 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const int j0 = AX == 1 ? blockIdx.y * FY : (AX == 2 ? blockIdx.z : blockIdx.y);
   const int k0 = AX == 2 ? blockIdx.y * FY : blockIdx.z;
   // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous runs).
-  // Each thread serves one tile cell (index math once) and a strided subset of its fields.
-  {
+  // TMA: one 4-D box per array (reconstruction fields, cell averages) issued by one thread, landing
+  // on an mbarrier -- used when the tile needs no periodic wrap (all blocks but the first along a
+  // periodic normal axis); otherwise cp.async per element into the same layout.
+  // (the innermost TMA coordinate must be 16-byte aligned: x-tiles start at the even cell i0 - 2)
+  const int x0 = AX == 0 ? i0 - 2 : i0, y0 = AX == 1 ? j0 - 1 : j0, z0 = AX == 2 ? k0 - 1 : k0;
+  const bool wraps = (AX == 0 && x0 < 0 && !c_geo.bounded[0]) || (AX == 1 && y0 < 0 && !c_geo.bounded[1]) ||
+                     (AX == 2 && z0 < 0 && !c_geo.bounded[2]);
+  const bool tma = !BOX && use_tma && !wraps;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_expect_tx(bar, (unsigned)(sizeof(double) * (FT::NREC + 5) * NT));
+      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], y0 - c_geo.elo[1], 0, z0 - c_geo.elo[2]);
+      tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
+    }
+  } else {
+    // Each thread serves one tile cell (index math once) and a strided subset of its fields.
     constexpr int TPC = 128 / NT;  // threads per cell
     const int c = threadIdx.x % NT, fsub = threadIdx.x / NT;
     if (fsub < TPC) {
       int ci, cj = j0, ck = k0;
       if (AX == 0) {
-        ci = i0 - 1 + c;
+        ci = i0 - 2 + c;
+        if (c_geo.bounded[0] && ci < -1) ci = -1;  // column 0 feeds no face
       } else {
         ci = i0 + c % FX;
         if (AX == 1) cj += c / FX - 1;
@@ -459,24 +523,29 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       const long long st = c_geo.eplane;
       // asynchronous global -> shared copies (LDGSTS): all in flight at once; running addresses
       const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
-      unsigned dst = (unsigned)__cvta_generic_to_shared(tile + fsub * NT + c);
+      unsigned dst = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NREC) + fsub * FT::FS);
 #pragma unroll 4
       for (int fld = fsub; fld < FT::NREC; fld += TPC) {
         cp_async8s(dst, src);
         src += TPC * st;
-        dst += TPC * NT * (unsigned)sizeof(double);
+        dst += TPC * FT::FS * (unsigned)sizeof(double);
       }
+      double* sdst = tile + FT::STILE + FT::cbase(c, 5);
       if (BOX) {
-        for (int v = fsub; v < 5; v += TPC) tile[(FT::NREC + v) * NT + c] = ld_state<BOX>(U, NV, v, ci, cj, ck);
+        for (int v = fsub; v < 5; v += TPC) sdst[v * FT::FS] = ld_state<BOX>(U, NV, v, ci, cj, ck);
       } else {
         const double* ub = U + sidx(NV, 0, wrap_ax(0, ci), wrap_ax(1, cj), wrap_ax(2, ck));
-        for (int v = fsub; v < 5; v += TPC) cp_async8(tile + (FT::NREC + v) * NT + c, ub + v * c_geo.plane);
+        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FS, ub + v * c_geo.plane);
       }
     }
   }
   if (COMPACT)
     for (int q = threadIdx.x; q < 2 * FT::NQ * FT::TS; q += blockDim.x) cp_async8(tab + q, gtab + q);  // padded rows
   cp_async_wait_all();
+  if (tma) {
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(bar, 0);
+  }
   __syncthreads();
 
   const double dt = ts->dt;
@@ -488,8 +557,9 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   const int i = i0 + fx, j = AX == 1 ? j0 + fy : j0, k = AX == 2 ? k0 + fy : k0;
   const bool valid = i < fn0 && (AX != 1 || j < c_geo.fn[1][1]) && (AX != 2 || k < c_geo.fn[2][2]);
   // tile column of this lane's cell
-  const int c = AX == 0 ? fl + side : (fy + side) * FX + fx;
-  const double* tc = tile + c;
+  const int c = AX == 0 ? fl + side + 1 : (fy + side) * FX + fx;
+  const double* tc = tile + FT::cbase(c, FT::NREC);           // field f at tc[f * FS]
+  const double* sc = tile + FT::STILE + FT::cbase(c, 5);      // cell average v at sc[v * FS]
 
   // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)
   constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
@@ -518,7 +588,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
                                  : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
         const double t = T[kk];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * NT], t, S[v][cls]);
+        for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * FT::FS], t, S[v][cls]);
       }
       const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);  // derivative along tA / tB flips that parity
 #pragma unroll
@@ -539,7 +609,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     double W[5], dW[NQ][5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      W[v] = tc[(FT::NREC + v) * NT] + xs[v * 128 + lane];
+      W[v] = sc[v * FT::FS] + xs[v * 128 + lane];
 #pragma unroll
       for (int q = 1; q < NQ; ++q) dW[q][v] = xs[(q * 5 + v) * 128 + lane];
     }
@@ -568,10 +638,10 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     const double hs = side ? -0.5 : 0.5;
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      const double q = tc[(FT::NREC + v) * NT];
-      W[v] = q + hs * tc[(AX * 5 + v) * NT];
+      const double q = sc[v * FT::FS];
+      W[v] = q + hs * tc[(AX * 5 + v) * FT::FS];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * NT] * c_geo.ih[a];
+      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * FT::FS] * c_geo.ih[a];
     }
     wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
     const int pp[3] = {P0, P1, P2};

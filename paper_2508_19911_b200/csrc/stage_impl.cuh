@@ -96,7 +96,10 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
     cudaEventCreate(&e1);
     cudaEventRecord(e0, env.stream);
   }
-  kern<<<grid, 128, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage);
+  static const CUtensorMap none{};
+  kern<<<grid, 128, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage,
+                                        a.use_tma ? a.tm_rec[AX] : none, a.use_tma ? a.tm_U[AX] : none,
+                                        a.use_tma && COMPACT && !BOX ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
@@ -173,6 +176,19 @@ int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part
   if (!c && nl && !b) return diag_t<false, true, false>(env, a, wtab, part, nblk);
   if (!c && !nl && b) return diag_t<false, false, true>(env, a, wtab, part, nblk);
   return diag_t<false, true, true>(env, a, wtab, part, nblk);
+}
+
+void flux_tile_fn(int ax, int* tx, int* tn) {
+  if (ax == 0) {
+    *tx = FluxTile<D, 0, true>::TX;
+    *tn = FluxTile<D, 0, true>::TN;
+  } else if (ax == 1) {
+    *tx = FluxTile<D, (D > 1 ? 1 : 0), true>::TX;
+    *tn = FluxTile<D, (D > 1 ? 1 : 0), true>::TN;
+  } else {
+    *tx = FluxTile<D, (D > 2 ? 2 : 0), true>::TX;
+    *tn = FluxTile<D, (D > 2 ? 2 : 0), true>::TN;
+  }
 }
 
 int upload_fn(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s) {
