@@ -106,11 +106,6 @@ struct cgks_ctx {
   CUtensorMap tm_rec[3];
   CUtensorMap tm_U[3][3];
   bool use_tma = false;
-  // the same for the warp-specialised flux kernel (k_flux_ws, 8-face tiles)
-  CUtensorMap tm_rec_ws[3];
-  CUtensorMap tm_U_ws[3][3];
-  bool use_ws = false;
-  int nsm = 148;
   double* dpart = nullptr;  // diagnostics block partials
   long long dpart_n = 0;
   double* staging = nullptr;
@@ -195,18 +190,12 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
   a.box = ctx->box;
-  a.nsm = ctx->nsm;
   if (ctx->use_tma) {
     const int b = Uin == ctx->U[0] ? 0 : (Uin == ctx->U[1] ? 1 : (Uin == ctx->Us ? 2 : -1));
     if (b >= 0) {
       a.tm_rec = ctx->tm_rec;
       a.tm_U = ctx->tm_U[b];
       a.use_tma = 1;
-      if (ctx->use_ws) {
-        a.tm_rec_ws = ctx->tm_rec_ws;
-        a.tm_U_ws = ctx->tm_U_ws[b];
-        a.use_ws = 1;
-      }
     }
   }
   return a;
@@ -381,7 +370,6 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     ctx->time_scheme = scheme->id == CGKS_CGKS5 ? CGKS_TIME_S2O4 : CGKS_TIME_S1O2;
   ctx->NV = scheme->id == CGKS_CGKS5 ? 20 : 5;
   cudaGetDevice(&ctx->device);
-  cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, ctx->device);
 
   // ---- geometry constants
   Geo& g = ctx->geo;
@@ -520,38 +508,29 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
       const cuuint32_t es[4] = {1, 1, 1, 1};
       bool good = true;
-      // ws = 0: the generic kernel's tiles; ws = 1: the warp-specialised kernel's tiles
-      for (int ws = 0; ws < 2 && good; ++ws)
-        for (int a = 0; a < 3 && good; ++a) {
-          int tx = 0, tn = 0;
-          ctx->ops->flux_tile(a, ws, &tx, &tn);
-          const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
-          {
-            const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)g.en[1], (cuuint64_t)nrec,
-                                        (cuuint64_t)g.en[2]};
-            const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.eplane * 8,
-                                       (cuuint64_t)g.eplane * nrec * 8};
-            const cuuint32_t box[4] = {(cuuint32_t)tx, by, (cuuint32_t)nrec, bz};
-            CUtensorMap* m = ws ? &ctx->tm_rec_ws[a] : &ctx->tm_rec[a];
-            good = good && encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->rec, dims, str, box, es,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-          }
-          double* bufs[3] = {ctx->U[0], ctx->U[1], ctx->Us};
-          for (int b = 0; b < 3 && good; ++b) {
-            const cuuint64_t dims[4] = {(cuuint64_t)g.n[0], (cuuint64_t)g.n[1], (cuuint64_t)NV,
-                                        (cuuint64_t)(g.n[2] + 2 * g.zoff)};
-            const cuuint64_t str[3] = {(cuuint64_t)g.n[0] * 8, (cuuint64_t)g.plane * 8,
-                                       (cuuint64_t)g.plane * NV * 8};
-            const cuuint32_t box[4] = {(cuuint32_t)tx, by, 5, bz};
-            CUtensorMap* m = ws ? &ctx->tm_U_ws[b][a] : &ctx->tm_U[b][a];
-            good = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[b], dims, str, box, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-          }
+      for (int a = 0; a < 3 && good; ++a) {
+        int tx = 0, tn = 0;
+        ctx->ops->flux_tile(a, &tx, &tn);
+        const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
+        {
+          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)g.en[1], (cuuint64_t)nrec, (cuuint64_t)g.en[2]};
+          const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.eplane * 8, (cuuint64_t)g.eplane * nrec * 8};
+          const cuuint32_t box[4] = {(cuuint32_t)tx, by, (cuuint32_t)nrec, bz};
+          good = good && encode(&ctx->tm_rec[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->rec, dims, str, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
         }
-      // opt-in (CGKS_WS=1): correct, but measured slower than k_flux on B200
-      ctx->use_ws = good && std::getenv("CGKS_WS") != nullptr;
+        double* bufs[3] = {ctx->U[0], ctx->U[1], ctx->Us};
+        for (int b = 0; b < 3 && good; ++b) {
+          const cuuint64_t dims[4] = {(cuuint64_t)g.n[0], (cuuint64_t)g.n[1], (cuuint64_t)NV,
+                                      (cuuint64_t)(g.n[2] + 2 * g.zoff)};
+          const cuuint64_t str[3] = {(cuuint64_t)g.n[0] * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.plane * NV * 8};
+          const cuuint32_t box[4] = {(cuuint32_t)tx, by, 5, bz};
+          good = encode(&ctx->tm_U[b][a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[b], dims, str, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+      }
       ctx->use_tma = good;
     }
   }
@@ -1015,20 +994,21 @@ int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_
 // Algorithmic FP64 operations per launch of each kernel (counting rules in flop_count.h).
 // The flux point is counted by running the device formulation with the counting type.
 // host "exchange" for counting: the other lane's value is mirrored (counts do not depend on it)
-struct NoParkHost {
-  void mark(int) const {}
+struct XchgMirror {
+  fc::CD operator()(const fc::CD& x) const { return x; }
+  bool flag(bool b) const { return b; }
 };
-struct SumSV {  // the summed side vectors x1[20..44]; W and dW/dt of side r
-  const fc::CD* s;
-  const fc::CD (*W)[5];
-  const fc::CD (*dtw)[5];
-  fc::CD operator()(int i) const { return s[20 + i]; }
-  fc::CD rel(int r, int i) const { return i < 5 ? W[r][i] : dtw[r][i - 5]; }
+struct ParkHost {
+  fc::CD* slots;
+  double* marks;
+  void put(int s, const fc::CD& v) const { slots[s] = v; }
+  fc::CD get(int s) const { return slots[s]; }
+  void mark(int m) const { marks[m] = fc::tally().flops; }
 };
 
-// flops of one Gauss point: the half-range terms of both sides, their sum, the interface part once,
-// and the relaxation of both sides (CGKS-5th); work that lanes duplicate to stay convergent is not
-// algorithmic and is not counted
+// flops of one Gauss point: both cooperating lanes, with the part both lanes compute identically to
+// stay convergent (the exchange sums and the whole interface phase up to the side relaxation, marks
+// 1 to 5) counted once
 static double flux_point_flops(const FluxConst& f, bool compact) {
   using fc::CD;
   CD W[2][5], dW[2][3][5];
@@ -1041,20 +1021,19 @@ static double flux_point_flops(const FluxConst& f, bool compact) {
       dW[1][d][i] = CD::run(-0.02 * (i + 1) + 0.01 * d);
     }
   }
-  fc::tally() = fc::Tally();
-  CD x1[2][46], dtw[2][5], sum[45];
-  side_terms(0, W[0], dW[0], f, x1[0], dtw[0]);
-  side_terms(1, W[1], dW[1], f, x1[1], dtw[1]);
-  for (int i = 0; i < 45; ++i) sum[i] = x1[0][i] + x1[1][i];
-  const SumSV sv{sum, W, dtw};
-  if (compact) {
-    IfaceOut<CD, 2> io;  // both sides relaxed
-    interface_terms(sum, sv, x1[0][45], x1[1][45], CD::run(1e-3), CD::run(1e3), f, NoParkHost{}, io);
-  } else {
-    IfaceOut<CD, 0> io;
-    interface_terms(sum, sv, x1[0][45], x1[1][45], CD::run(1e-3), CD::run(1e3), f, NoParkHost{}, io);
+  double total = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    GPOutT<CD> o;
+    CD slots[40];
+    double marks[6] = {0, 0, 0, 0, 0, 0};
+    fc::tally() = fc::Tally();
+    if (compact)
+      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
+    else
+      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
+    total += fc::tally().flops - (side == 1 ? marks[5] - marks[1] : 0.0);
   }
-  return fc::tally().flops;
+  return total;
 }
 
 extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names, double* flops_per_launch,

@@ -42,11 +42,6 @@ struct StageArgs {
   const CUtensorMap* tm_rec = nullptr;
   const CUtensorMap* tm_U = nullptr;
   int use_tma = 0;
-  // warp-specialised flux kernel (3-D CGKS-5th, TMA): its own descriptors (smaller tiles)
-  const CUtensorMap* tm_rec_ws = nullptr;
-  const CUtensorMap* tm_U_ws = nullptr;
-  int use_ws = 0;
-  int nsm = 148;
 };
 
 struct DimOps {
@@ -60,9 +55,8 @@ struct DimOps {
   int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   // flow diagnostics of a.Uin (reconstruction + quadrature); *nblk = number of 4-double block partials
   int (*diag)(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk);
-  // flux tile extent (cells along x, cells along the normal axis) for the TMA boxes, CGKS-5th;
-  // ws = 1: the warp-specialised kernel's tiles
-  void (*flux_tile)(int ax, int ws, int* tx, int* tn);
+  // flux tile extent (cells along x, cells along the normal axis) for the TMA boxes, CGKS-5th
+  void (*flux_tile)(int ax, int* tx, int* tn);
 };
 
 extern const DimOps kOps1, kOps2, kOps3;

@@ -302,19 +302,25 @@ struct ParkDev {
 };
 
 // ---------------------------------------------------------------------------
-// (S) One side of the interface solver at one Gauss point: primitives, half-range moments and
-// all half-range terms of Eq. (flux) of this side (side 0 = left state restricted to u > 0,
-// side 1 = right state restricted to u < 0), as values and directional derivatives of
-// half-range moment vectors.  Inputs in the normal frame: W (5) conservative state of this side,
-// dW[dir][var] physical derivatives (dir 0 = normal).  Outputs: x1[0..4] W0 part (R13), 5-19 dW0
-// parts (R14), 20-24 MF3 = rho <u psi>, 25-29 MF4 = rho <u (a.u) psi>, 30-34 MF5 = rho <u A psi>,
-// 35-39 MQ4 = rho <(a.u) psi>, 40-44 MQ5 = rho <A psi> (half ranges), x1[45] = p; dtw = the side's
-// Euler time derivative dW/dt (R23).  Returns false if the state is not positive.
+// One side of the interface solver at one Gauss point (two cooperating lanes per Gauss
+// point: side 0 = left state restricted to u > 0, side 1 = right state restricted to u < 0).
+// Phases: (S) all half-range terms of this side (W0 and dW0 parts, MF3..MF5, MQ4, MQ5), as
+// values and directional derivatives of half-range moment vectors -> one exchange (lane xor 1)
+// sums the two sides -> (G) interface equilibrium g0, collision time and combined time
+// coefficients, equilibrium terms as Jacobian-vector products, everything folded into F^n,
+// F_t^n, Q^n, Q_t^n and the heat-flux scalars -> Prandtl fix and own side relaxation.
+// Both lanes run the same instruction stream.
+// Inputs in the normal frame: W (5) conservative state of this side, dW[dir][var] physical
+// derivatives (dir 0 = normal).  Outputs (normal frame): side 0 holds Fn, Ft, QLn, QLt;
+// side 1 holds Fn, Ft and its QRn, QRt in the QLn/QLt slots.  Returns false if a state
+// (own, other, or the equilibrium) is not positive.
 // ---------------------------------------------------------------------------
-template <typename T>
-HD bool side_terms(int side, const T* W, const T (*dW)[5], const FluxConst& fc, T* x1, T* dtw) {
+template <bool COMPACT, typename T, typename X, typename P>
+HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const FluxConst& fc, const X& xchg,
+                      const P& park, GPOutT<T>& o) {
   const T gm1 = fc.gamma - 1.0;
   const double sgn = side == 0 ? 1.0 : -1.0;
+  // ---- (S) this side: primitives, half-range moments, and all half-range terms of Eq. (flux)
   const T rho = W[0], ir = 1.0 / rho;
   const T U = W[1] * ir, V = W[2] * ir, Ww = W[3] * ir;
   const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
@@ -326,8 +332,7 @@ HD bool side_terms(int side, const T* W, const T (*dW)[5], const FluxConst& fc, 
   const T Uv[3] = {U, V, Ww};
   // Euler time derivative of this side (R23): dW/dt = rho <A psi> = -sum_al DF_al(W) dW_al (full
   // moments, compatibility R16) as Jacobian-vector products
-#pragma unroll
-  for (int i = 0; i < 5; ++i) dtw[i] = 0.0;
+  T dtw[5] = {0, 0, 0, 0, 0};
   {
     const Dprim<T> q0 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[0]);
     jvp_flux<0>(rho, Uv, p, W[4], dW[0], q0, -1.0, dtw);
@@ -336,6 +341,9 @@ HD bool side_terms(int side, const T* W, const T (*dW)[5], const FluxConst& fc, 
     const Dprim<T> q2 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[2]);
     jvp_flux<2>(rho, Uv, p, W[4], dW[2], q2, -1.0, dtw);
   }
+  // x1: 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3 = rho <u psi>, 25-29 MF4 = rho <u (a.u) psi>,
+  // 30-34 MF5 = rho <u A psi>, 35-39 MQ4 = rho <(a.u) psi>, 40-44 MQ5 = rho <A psi>, 45 p (half ranges)
+  T x1[46];
 #pragma unroll
   for (int i = 0; i < 45; ++i) x1[i] = 0.0;
   x1[45] = p;
@@ -379,35 +387,37 @@ HD bool side_terms(int side, const T* W, const T (*dW)[5], const FluxConst& fc, 
       }
     }
   }
-  return ok;
-}
-
-// outputs of the interface phase (normal frame): F^n, F_t^n, the interface values Q^n, Q_t^n
-// before the side relaxation, and the relaxation weights (Q^s = w Q + ee W_s, R23)
-template <typename T, int NRS>
-struct IfaceOut {
-  T Fn[5], Ft[5];
-  T Qs[NRS > 0 ? NRS : 1][10];  // relaxed interface values of the NRS requested sides: Q^n (5), Q_t^n (5)
-};
-
-// ---------------------------------------------------------------------------
-// (G) The interface part at one Gauss point, from the two sides' summed half-range terms:
-// equilibrium g0 (R13, R14), collision time, combined time coefficients, equilibrium terms as
-// Jacobian-vector products, the summed half-range terms (k = 3, 4, 5 of Eq. (flux)) folded into
-// F^n, F_t^n, Q^n, Q_t^n and the heat-flux scalars, and the Prandtl fix.
-// x1[0..19]: summed W0 and dW0 parts; sv(i), i = 0..24: summed MF3, MF4, MF5, MQ4, MQ5 (read late,
-// so they can live in shared memory); pL, pR the side pressures.  Returns false if g0 is not positive.
-// ---------------------------------------------------------------------------
-template <int NRS, typename T, typename SV, typename P>
-HD bool interface_terms(const T* x1, const SV& sv, T pL, T pR, T dt, T idt, const FluxConst& fc, const P& park,
-                        IfaceOut<T, NRS>& o) {
-  const T gm1 = fc.gamma - 1.0;
-  park.mark(1);  // start of the equilibrium phase
+  // ---- exchange 1: W0, dW0 = sum of the two half-range contributions
+  park.mark(1);  // from here to mark 5 both lanes compute the same values (counted once)
+  const bool ok_other = xchg.flag(ok);
+  T other_p;
+  {
+#pragma unroll
+    for (int i = 0; i < 46; ++i) {
+      const T y = xchg(x1[i]);
+      if (i < 45)
+        x1[i] += y;
+      else
+        other_p = y;
+    }
+  }
+  // park the summed half-range terms and this side's W, dW/dt until the final phase
+#pragma unroll
+  for (int i = 0; i < 25; ++i) park.put(i, x1[20 + i]);
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    park.put(25 + i, dtw[i]);
+    park.put(30 + i, W[i]);
+  }
+  bool good = ok && ok_other;
+  const T pL = side == 0 ? p : other_p, pR = side == 0 ? other_p : p;
+  // ---- (G) interface equilibrium g0 (R13, R14)
   const T r0 = x1[0], i0 = 1.0 / r0;
   const T U0 = x1[1] * i0, V0 = x1[2] * i0, Ww0 = x1[3] * i0;
   const T uu2 = 0.5 * (U0 * U0 + V0 * V0 + Ww0 * Ww0);
   const T p0 = gm1 * (x1[4] - r0 * uu2);
-  const bool good = (r0 > 0.0) && (p0 > 0.0);
+  good = good && (r0 > 0.0) && (p0 > 0.0);
+  const T l0 = good ? T(0.5) * r0 / p0 : T(1.0);
   // collision time (R17) and combined time coefficients:
   // F^n = sum alpha_k MF_k, F_t^n = sum beta_k MF_k (E2 = e^{-dt/(2tau)}, tau = 0 -> Euler limit)
   // one reciprocal serves 1/p0 and 1/(pL + pR)
@@ -500,25 +510,19 @@ HD bool interface_terms(const T* x1, const SV& sv, T pL, T pR, T dt, T idt, cons
     acc[20] += (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) + al[2] * (sMF2 + U0 * sMQa);
     acc[21] += be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
   }
-  park.mark(2);
-  park.mark(3);
-  park.mark(4);
-  // ---- half-range terms of both sides (summed): k = 3, 4, 5 of Eq. (flux)
-  T rel[NRS > 0 ? NRS : 1][10];  // W_s and dW_s/dt of the sides to relax (read with the side vectors)
+  // ---- half-range terms of both sides (summed by the exchange): k = 3, 4, 5 of Eq. (flux)
+  T dtW[5], Wown[5];
   {
     T v3[5], v4[5], v5[5], q4[5], q5[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      v3[i] = sv(i);
-      v4[i] = sv(5 + i);
-      v5[i] = sv(10 + i);
-      q4[i] = sv(15 + i);
-      q5[i] = sv(20 + i);
-#pragma unroll
-      for (int r = 0; r < NRS; ++r) {
-        rel[r][5 + i] = sv.rel(r, 5 + i);
-        rel[r][i] = sv.rel(r, i);
-      }
+      v3[i] = park.get(i);
+      v4[i] = park.get(5 + i);
+      v5[i] = park.get(10 + i);
+      q4[i] = park.get(15 + i);
+      q5[i] = park.get(20 + i);
+      dtW[i] = park.get(25 + i);
+      Wown[i] = park.get(30 + i);
     }
     const T s3 = qF(v3, U0, V0, Ww0, uu2);
     const T s4 = qF(v4, U0, V0, Ww0, uu2) - U0 * qF(q4, U0, V0, Ww0, uu2);
@@ -533,7 +537,7 @@ HD bool interface_terms(const T* x1, const SV& sv, T pL, T pR, T dt, T idt, cons
     acc[20] += al[3] * s3 + al[4] * s4 + al[5] * s5;
     acc[21] += be[3] * s3 + be[4] * s4 + be[5] * s5;
   }
-  // ---- Prandtl fix (R20)
+  // ---- Prandtl fix (R20) and outputs
   if (fc.Pr != 1.0) {
     const double pf = fc.pfix;
     acc[4] += pf * acc[20];
@@ -544,74 +548,16 @@ HD bool interface_terms(const T* x1, const SV& sv, T pL, T pR, T dt, T idt, cons
     o.Fn[i] = acc[i];
     o.Ft[i] = acc[5 + i];
   }
-  if (NRS > 0) {
-    // side-state relaxation (R23): Q^s = w Q + ee W_s, Q_t^s = w Q_t + ee dW_s/dt
+  park.mark(5);  // end of the part both lanes compute identically
+  if (COMPACT) {
+    // side-state relaxation of this side (R23)
     const T tau0 = fc.relax_C * jump * dt;
     const T ee = (tau0 > 0.0) ? exp(-dt / tau0) : T(0.0);
     const T w = 1.0 - ee;
 #pragma unroll
-    for (int r = 0; r < NRS; ++r)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        o.Qs[r][i] = w * acc[10 + i] + ee * rel[r][i];
-        o.Qs[r][5 + i] = w * acc[15 + i] + ee * rel[r][5 + i];
-      }
-  }
-  return good;
-}
-
-// the summed side vectors (slots 0..24) and this side's dW/dt (25..29) and W (30..34) from the parking
-template <typename P>
-struct ParkSV {
-  const P& park;
-  HD auto operator()(int i) const { return park.get(i); }
-  HD auto rel(int, int i) const { return park.get(i < 5 ? 30 + i : 20 + i); }
-};
-
-// ---------------------------------------------------------------------------
-// Two-lane form used by the generic flux kernel: side terms of this lane's side, one exchange
-// (lane xor 1) sums the two sides, the summed side vectors and this side's W, dW/dt are parked,
-// then both lanes run the interface part (identical) and relax their own side.
-// Outputs (normal frame): side 0 holds Fn, Ft, QLn, QLt; side 1 holds Fn, Ft and its QRn, QRt in the
-// QLn/QLt slots.  Returns false if a state (own, other, or the equilibrium) is not positive.
-// ---------------------------------------------------------------------------
-template <bool COMPACT, typename T, typename X, typename P>
-HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const FluxConst& fc, const X& xchg,
-                      const P& park, GPOutT<T>& o) {
-  T x1[46], dtw[5];
-  const bool ok = side_terms(side, W, dW, fc, x1, dtw);
-  // ---- exchange: W0, dW0 and the side vectors = sum of the two half-range contributions
-  const bool ok_other = xchg.flag(ok);
-  T other_p;
-#pragma unroll
-  for (int i = 0; i < 46; ++i) {
-    const T y = xchg(x1[i]);
-    if (i < 45)
-      x1[i] += y;
-    else
-      other_p = y;
-  }
-  // park the summed half-range terms and this side's W, dW/dt until the final phase
-#pragma unroll
-  for (int i = 0; i < 25; ++i) park.put(i, x1[20 + i]);
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    park.put(25 + i, dtw[i]);
-    park.put(30 + i, W[i]);
-  }
-  const T pL = side == 0 ? x1[45] : other_p, pR = side == 0 ? other_p : x1[45];
-  IfaceOut<T, COMPACT ? 1 : 0> io;
-  const bool good = interface_terms(x1, ParkSV<P>{park}, pL, pR, dt, idt, fc, park, io) && ok && ok_other;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    o.Fn[i] = io.Fn[i];
-    o.Ft[i] = io.Ft[i];
-  }
-  if constexpr (COMPACT) {
-#pragma unroll
     for (int i = 0; i < 5; ++i) {
-      o.QLn[i] = io.Qs[0][i];
-      o.QLt[i] = io.Qs[0][5 + i];
+      o.QLn[i] = w * acc[10 + i] + ee * Wown[i];
+      o.QLt[i] = w * acc[15 + i] + ee * dtW[i];
     }
   }
   return good;

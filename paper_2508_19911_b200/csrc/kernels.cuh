@@ -1029,5 +1029,3 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
 }
 
 }  // namespace cgks
-
-#include "flux_ws.cuh"

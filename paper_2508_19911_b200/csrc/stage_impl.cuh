@@ -4,7 +4,6 @@
 #ifndef CGKS_DIM
 #error "define CGKS_DIM before including stage_impl.cuh"
 #endif
-#include <algorithm>
 #include <cstdio>
 
 #include "driver.h"
@@ -77,50 +76,8 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 }
 
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
-// warp-specialised flux kernel: persistent blocks of 96 threads, 4 per SM
-template <int AX>
-int flux_ws_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
-  using FT = FluxWS<AX>;
-  auto kern = k_flux_ws<AX>;
-  static bool attr = false;
-  const size_t smem = FT::smem_bytes();
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
-    attr = true;
-  }
-  long long nb;
-  {
-    const long long nbx = (a.fn[AX][0] + FT::FX - 1) / FT::FX;
-    nb = AX == 0 ? nbx * a.fn[0][1] * a.fn[0][2]
-                 : (AX == 1 ? nbx * ((a.fn[1][1] + FT::FY - 1) / FT::FY) * a.fn[1][2]
-                            : nbx * ((a.fn[2][2] + FT::FY - 1) / FT::FY) * a.fn[2][1]);
-  }
-  const long long g = std::min<long long>(nb, 4LL * a.nsm);
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (env.prof) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, env.stream);
-  }
-  kern<<<(unsigned)g, 96, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage,
-                                               a.tm_rec_ws[AX], a.tm_U_ws[AX]);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
-    return 5;
-  }
-  if (env.prof) {
-    cudaEventRecord(e1, env.stream);
-    env.pending->push_back({name, {e0, e1}});
-  }
-  return 0;
-}
-
 template <bool COMPACT, bool BOX, int AX>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
-  if constexpr (COMPACT && !BOX && D == 3) {
-    if (a.use_ws) return flux_ws_launch<AX>(env, name, a, stage);
-  }
   using FT = FluxTile<D, AX, COMPACT>;
   auto kern = k_flux<D, AX, COMPACT, BOX>;
   static bool attr = false;
@@ -221,12 +178,7 @@ int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part
   return diag_t<false, true, true>(env, a, wtab, part, nblk);
 }
 
-void flux_tile_fn(int ax, int ws, int* tx, int* tn) {
-  if (ws) {
-    *tx = ax == 0 ? FluxWS<0>::TX : (ax == 1 ? FluxWS<1>::TX : FluxWS<2>::TX);
-    *tn = ax == 0 ? FluxWS<0>::TN : (ax == 1 ? FluxWS<1>::TN : FluxWS<2>::TN);
-    return;
-  }
+void flux_tile_fn(int ax, int* tx, int* tn) {
   if (ax == 0) {
     *tx = FluxTile<D, 0, true>::TX;
     *tn = FluxTile<D, 0, true>::TN;
