@@ -83,6 +83,9 @@ inline CD sqrt(const CD& a) {
   tally().flops += 1;
   return CD::run(std::sqrt(a.v));
 }
+inline CD fmax(const CD& a, const CD& b) {  // a comparison: not counted
+  return (a.k && b.k) ? CD(std::fmax(a.v, b.v)) : CD::run(std::fmax(a.v, b.v));
+}
 inline CD fabs(const CD& a) { return a.k ? CD(std::fabs(a.v)) : CD::run(std::fabs(a.v)); }
 inline CD fma(const CD& a, const CD& b, const CD& c) { return a * b + c; }
 

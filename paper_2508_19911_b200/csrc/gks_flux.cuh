@@ -551,8 +551,11 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const
   park.mark(5);  // end of the part both lanes compute identically
   if (COMPACT) {
     // side-state relaxation of this side (R23)
-    const T tau0 = fc.relax_C * jump * dt;
-    const T ee = (tau0 > 0.0) ? exp(-dt / tau0) : T(0.0);
+    // ee = exp(-dt / tau0) with tau0 = C |pL - pR| / (pL + pR) dt = rC dt: exp(-1 / rC), which
+    // is below 1e-304 for rC < 1/700 (smooth regions) and is then taken as 0 -- the reciprocal is
+    // only formed in its safe range (no division slow path for tau0 -> 0)
+    const T rC = fc.relax_C * jump;
+    const T ee = (rC > 1.0 / 700.0) ? exp(-1.0 / fmax(rC, T(1.0 / 700.0))) : T(0.0);
     const T w = 1.0 - ee;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
