@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     for (int cc = 0; cc < 5; ++cc) {
       const double a = s == 0 ? o.Fn[cc] : (s == 1 ? o.Ft[cc] : (s == 2 ? o.QLn[cc] : o.QLt[cc]));
       const int g = cc == 0 ? 0 : (cc == 4 ? 4 : 1 + (cc == 1 ? P0 : (cc == 2 ? P1 : P2)));
-      y[s * 5 + g] = wgt * a;
+      y[s * 5 + g] = a;  // the 1/NG weight is applied after the Gauss-point sum (exact: a power of 2)
     }
   }
   if constexpr (NG == 1) {
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     if (valid && (o0 >= 10 || side == 0)) {
       double* dst = face + base + (long long)(o0 + (o0 >= 10 && side ? 10 : 0)) * fpl;
 #pragma unroll
-      for (int q = 0; q < NOUT; ++q) dst[q * fpl] = zz[q];
+      for (int q = 0; q < NOUT; ++q) dst[q * fpl] = wgt * zz[q];
     }
   }
 }
