@@ -146,6 +146,13 @@ int cgks_get_time(const cgks_ctx* ctx, double* t, int64_t* steps, double* last_d
  * CGKS_ERR_NUMERICAL if a result is not finite. */
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]);
 
+/* Q-criterion Q = (|Omega|^2 - |S|^2)/2 = -1/2 sum_ab dU_b/dx_a dU_a/dx_b at every cell centroid,
+ * from the cell's reconstruction of the current state (the paper's TGV
+ * iso-surfaces; DESIGN R35).  out: ncell doubles [nz][ny][nx] (x fastest, rank-local), host
+ * or device pointer, caller-owned.  Synchronous; reuses the reconstruction buffer; does not change
+ * the state.  CGKS_ERR_CONFIG for decomposed contexts in this version. */
+int cgks_qcriterion(cgks_ctx* ctx, double* out);
+
 /* Message of the last error (includes cell (i,j,k) and stage for positivity failures). */
 const char* cgks_last_error(const cgks_ctx* ctx);
 

@@ -81,6 +81,8 @@ def lib():
         L.orc_stage_residual.restype = ctypes.c_int
         L.orc_diagnostics.argtypes = [pp, dp, dp, dp]
         L.orc_diagnostics.restype = ctypes.c_int
+        L.orc_qcriterion.argtypes = [pp, dp, dp, dp]
+        L.orc_qcriterion.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -237,6 +239,18 @@ def diagnostics(prob: Problem, Q, G=None):
     rc = lib().orc_diagnostics(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
     if rc:
         raise ValueError(f"oracle diagnostics failed rc={rc}")
+    return out
+
+
+def qcriterion(prob: Problem, Q, G=None):
+    """Q-criterion at every cell centroid from the cell's reconstruction (orc_qcriterion): [nz][ny][nx]."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    G = np.zeros((3,) + Q.shape) if G is None else np.ascontiguousarray(G, dtype=np.float64)
+    out = np.zeros(Q.shape[1:])
+    p = prob.to_c()
+    rc = lib().orc_qcriterion(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
+    if rc:
+        raise ValueError(f"oracle qcriterion failed rc={rc}")
     return out
 
 

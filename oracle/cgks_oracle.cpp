@@ -1481,6 +1481,45 @@ int orc_diagnostics(const orc_params* p, const double* Q, const double* G, doubl
   return bad ? 3 : 0;
 }
 
+// Q-criterion at every cell centroid (the iso-surfaces of TGV-sup-1):
+// Q = (|Omega|^2 - |S|^2) / 2 = -1/2 sum_ab dU_b/dx_a dU_a/dx_b with the velocity gradient from the
+// cell's own reconstruction evaluated at its centroid (reading R35).  out: [ncell], x fastest.
+int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double* out) {
+  Solver S(*p);
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
+  load_state(S, Q, G);
+  const long nc = S.ncell();
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (long c = 0; c < nc; ++c) {
+    const int i = (int)(c % S.P.n[0]), j = (int)((c / S.P.n[0]) % S.P.n[1]), k = (int)(c / ((long)S.P.n[0] * S.P.n[1]));
+    CellRecon cr;
+    const double x[3] = {0.0, 0.0, 0.0};
+    double W[5], dW[3][5];
+    if (S.P.scheme == 1) {
+      recon5_cell(S, S.U, i, j, k, cr);
+      recon5_eval(S, cr, basis_at(S.rc, x), W, dW);
+    } else {
+      recon2_cell(S, S.U, i, j, k, cr);
+      recon2_eval(S, cr, x, W, dW);
+    }
+    if (!(W[0] > 0.0)) {
+      bad = 1;
+      out[c] = 0.0;
+      continue;
+    }
+    double U[3], dU[3][3];
+    for (int a = 0; a < 3; ++a) U[a] = W[1 + a] / W[0];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) dU[a][b] = (dW[a][1 + b] - U[b] * dW[a][0]) / W[0];
+    double q = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) q -= 0.5 * dU[a][b] * dU[b][a];
+    out[c] = q;
+  }
+  return bad ? 3 : 0;
+}
+
 // One stage's residual L, dL/dt and Gauss-theorem gradients for a given dt (for unit tests).
 // L, Lt: [5][ncell]; Gn, Gt: [3][5][ncell]
 int orc_stage_residual(const orc_params* p, const double* Q, const double* G, double dt, double* L, double* Lt,

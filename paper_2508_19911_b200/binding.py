@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH):
     L.cgks_get_state.argtypes = [vp, vp, vp]
     L.cgks_get_time.argtypes = [vp, dp, ctypes.POINTER(ctypes.c_int64), dp]
     L.cgks_diagnostics.argtypes = [vp, dp]
+    L.cgks_qcriterion.argtypes = [vp, dp]
     L.cgks_last_error.argtypes = [vp]
     L.cgks_last_error.restype = ctypes.c_char_p
     L.cgks_launches_per_step.argtypes = [vp]
@@ -245,6 +246,12 @@ class Solver:
         int rho dV) of the current state, by quadrature of the reconstruction (unnormalised)."""
         out = np.zeros(4)
         self._check(self._L.cgks_diagnostics(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def qcriterion(self):
+        """cgks_qcriterion: Q-criterion at every cell centroid, [nz][ny][nx] (rank-local)."""
+        out = np.zeros(self.n[::-1])
+        self._check(self._L.cgks_qcriterion(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def last_error(self):

@@ -107,6 +107,7 @@ struct cgks_ctx {
   CUtensorMap tm_U[3][3];
   bool use_tma = false;
   double* dpart = nullptr;  // diagnostics block partials
+  double* ctab = nullptr;   // basis values at the centroid p_k(0) (Q-criterion, CGKS-5th)
   long long dpart_n = 0;
   double* staging = nullptr;
   TimeState* ts = nullptr;
@@ -592,6 +593,13 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       set_msg(ctx, "diagnostics table upload failed");
       return fail(CGKS_ERR_CUDA);
     }
+    const double x0[3] = {0.0, 0.0, 0.0};
+    basis_at(ctx->cls, x0, val.data(), der.data());  // p_k(0) = -avg0_k
+    if (!alloc(&ctx->ctab, nb) ||
+        cudaMemcpy(ctx->ctab, val.data(), sizeof(double) * nb, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_msg(ctx, "centroid table upload failed");
+      return fail(CGKS_ERR_CUDA);
+    }
   }
   cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
   // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
@@ -951,6 +959,25 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   return CGKS_OK;
 }
 
+int cgks_qcriterion(cgks_ctx* ctx, double* out) {
+  if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (ctx->nranks > 1 || ctx->comm_mode == 2) {
+    set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
+    return CGKS_ERR_CONFIG;
+  }
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  StageArgs a = stage_args(ctx, ctx->U[ctx->cur], nullptr);
+  const bool dev = is_device_ptr(out);
+  double* dout = dev ? out : ctx->staging;  // staging holds >= ncell doubles
+  LaunchEnv env = env_of(ctx);
+  env.prof = false;
+  if (ctx->ops->qcrit(env, a, ctx->ctab, dout)) return CGKS_ERR_CUDA;
+  if (!dev) CK(cudaMemcpyAsync(out, dout, sizeof(double) * ctx->ncell, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CGKS_OK;
+}
+
 const char* cgks_last_error(const cgks_ctx* ctx) { return ctx ? ctx->msg : "null context"; }
 
 int cgks_launches_per_step(const cgks_ctx* ctx) { return ctx ? ctx->launches_per_step : 0; }
@@ -1146,7 +1173,8 @@ void cgks_destroy(cgks_ctx* ctx) {
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
-                    ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart};
+                    ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart,
+                    ctx->ctab};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);

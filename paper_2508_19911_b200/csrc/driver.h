@@ -57,6 +57,8 @@ struct DimOps {
   int (*diag)(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk);
   // flux tile extent (cells along x, cells along the normal axis) for the TMA boxes, CGKS-5th
   void (*flux_tile)(int ax, int* tx, int* tn);
+  // Q-criterion of a.Uin at the cell centroids (reconstruction + k_qcrit) into out[ncell]
+  int (*qcrit)(LaunchEnv& env, const StageArgs& a, const double* wc, double* out);
 };
 
 extern const DimOps kOps1, kOps2, kOps3;

@@ -1028,4 +1028,55 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Q-criterion at each cell centroid (reading R35): Q = -1/2 sum_ab dU_b/dx_a
+// dU_a/dx_b from the cell's reconstruction at xi = 0: the value is Q0 + sum_k a_k p_k(0) (wc = p_k(0)
+// = -avg0_k), the derivative along a only sees the linear basis function e_a (coefficient index a).
+// out: [nz][ny][nx] (x fastest), one thread per cell.
+// ---------------------------------------------------------------------------
+template <int DIM, bool COMPACT>
+__global__ void __launch_bounds__(256) k_qcrit(const double* __restrict__ U, const double* __restrict__ rec,
+                                                const double* __restrict__ wc, double* __restrict__ out) {
+  constexpr int NB = Sten<DIM>::NB;
+  constexpr int NV = COMPACT ? 20 : 5;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc) return;
+  const int i = (int)(t % c_geo.n[0]);
+  const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
+  const int k = (int)(t / c_geo.plane);
+  double W[5], dW[3][5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    W[v] = __ldg(U + sidx(NV, v, i, j, k));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dW[a][v] = 0.0;
+    if (COMPACT) {
+      for (int kk = 0; kk < NB; ++kk) W[v] = fma(__ldg(rec + eidx(NB * 5, kk * 5 + v, i, j, k)), wc[kk], W[v]);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        static_assert(ReconGen<DIM>::expo(0, 0) == 1, "linear basis functions first");
+        dW[a][v] = __ldg(rec + eidx(NB * 5, a * 5 + v, i, j, k)) * c_geo.ih[a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) dW[a][v] = __ldg(rec + eidx(15, a * 5 + v, i, j, k)) * c_geo.ih[a];
+    }
+  }
+  const double ir = 1.0 / W[0];
+  double Uv[3], dU[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) Uv[b] = W[1 + b] * ir;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) dU[a][b] = (dW[a][1 + b] - Uv[b] * dW[a][0]) * ir;
+  double q = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) q -= 0.5 * dU[a][b] * dU[b][a];
+  out[t] = q;
+}
+
 }  // namespace cgks

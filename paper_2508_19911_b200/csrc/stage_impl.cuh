@@ -166,6 +166,31 @@ int diag_t(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part,
   return 0;
 }
 
+// Q-criterion of a.Uin at the cell centroids into out[ncell] (reconstruction first)
+template <bool COMPACT, bool NONLIN, bool BOX>
+int qcrit_t(LaunchEnv& env, const StageArgs& a, const double* wc, double* out) {
+  if (COMPACT) {
+    int rc = recon5_launch<NONLIN, BOX>(env, a);
+    if (rc) return rc;
+  } else {
+    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  }
+  LAUNCH("qcrit", (k_qcrit<D, COMPACT>), a.ncell, 256, (const double*)a.Uin, (const double*)a.rec, wc, out);
+  return 0;
+}
+
+int qcrit_fn(LaunchEnv& env, const StageArgs& a, const double* wc, double* out) {
+  const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
+  if (c && !nl && !b) return qcrit_t<true, false, false>(env, a, wc, out);
+  if (c && nl && !b) return qcrit_t<true, true, false>(env, a, wc, out);
+  if (c && !nl && b) return qcrit_t<true, false, true>(env, a, wc, out);
+  if (c && nl && b) return qcrit_t<true, true, true>(env, a, wc, out);
+  if (!c && !nl && !b) return qcrit_t<false, false, false>(env, a, wc, out);
+  if (!c && nl && !b) return qcrit_t<false, true, false>(env, a, wc, out);
+  if (!c && !nl && b) return qcrit_t<false, false, true>(env, a, wc, out);
+  return qcrit_t<false, true, true>(env, a, wc, out);
+}
+
 int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk) {
   const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
   if (c && !nl && !b) return diag_t<true, false, false>(env, a, wtab, part, nblk);

@@ -302,3 +302,21 @@ def test_diagnostics_tgv128_value():
     V = (2 * np.pi) ** 3
     assert abs(d[0] / V - 0.125) < 1e-9 and abs(d[3] / V - 1.0) < 1e-12
     assert abs(d[1] / (case.mu * V) - 0.75) < 1e-6
+
+
+@pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 1)])
+def test_qcriterion_parity(scheme, nl):
+    """cgks_qcriterion against the oracle's Q-criterion of the reconstructed state (same cell, same
+    centroid evaluation) on the high-speed TGV at 20^3 after 3 steps; relative to max |Q|."""
+    case = tgv_supersonic(20)
+    d = case.problem_kwargs()
+    d["nonlinear"] = nl
+    prob = oracle.Problem(**d, scheme=scheme, time_scheme=2 if scheme == 1 else 1)
+    S = _gpu().from_case(case, scheme=scheme, nonlinear=nl)
+    S.set_state(case.Q, case.G)
+    S.step(3)
+    Qg, Gg = S.get_state()
+    qg = S.qcriterion()
+    S.close()
+    qo = oracle.qcriterion(prob, Qg, Gg if scheme == 1 else None)
+    assert np.abs(qg - qo).max() <= 1e-11 * np.abs(qo).max(), np.abs(qg - qo).max()

@@ -72,3 +72,47 @@ def test_supersonic_tgv_initial_values():
         assert abs(d[3] / V - 1.0) < 1e-13
     assert errs[1][0] < errs[0][0] / 32.0 and errs[1][1] < errs[0][1] / 12.0, errs
     assert errs[1][0] < 1e-5 and errs[1][1] < 2e-3, errs
+
+
+def _linear_velocity_case(n, grad, rho=1.0, p=1.0, U0=(0.0, 0.0, 0.0)):
+    """Constant density and pressure, velocity U = U0 + grad . x (grad[b][a] = dU_b/dx_a): exact cell
+    averages and gradients of the conservative variables on a box with inflow-free periodic copies
+    is not possible, so the field is used only on interior cells (the reconstruction is exact there)."""
+    L = 1.0
+    h = L / n
+    x = (np.arange(n) + 0.5) * h - 0.5
+    Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
+    pos = [X, Y, Z]
+    U = [U0[b] + sum(grad[b][a] * pos[a] for a in range(3)) for b in range(3)]
+    gam = 1.4
+    Q = np.zeros((5, n, n, n))
+    G = np.zeros((3, 5, n, n, n))
+    Q[0] = rho
+    for b in range(3):
+        Q[1 + b] = rho * U[b]
+        for a in range(3):
+            G[a, 1 + b] = rho * grad[b][a]
+    # rho E = p/(gamma-1) + rho |U|^2 / 2: the cell average of a quadratic adds the variance term
+    ke = 0.5 * rho * (U[0] ** 2 + U[1] ** 2 + U[2] ** 2)
+    var = 0.5 * rho * sum(sum(grad[b][a] ** 2 for b in range(3)) * h * h / 12.0 for a in range(3))
+    Q[4] = p / (gam - 1.0) + ke + var
+    for a in range(3):
+        G[a, 4] = rho * sum(U[b] * grad[b][a] for b in range(3))
+    return Q, G
+
+
+@pytest.mark.parametrize("scheme", [1, 0])
+def test_qcriterion_linear_fields(scheme):
+    """Q = (|Omega|^2 - |S|^2)/2: solid-body rotation about z with rate w gives w^2, pure strain
+    (a x, -a y) gives -a^2, exactly (a linear velocity is reproduced by both reconstructions);
+    checked on interior cells (the box boundary uses ghost rules)."""
+    n = 8
+    w, a = 0.7, 0.4
+    cases = [([[0, -w, 0], [w, 0, 0], [0, 0, 0]], w * w), ([[a, 0, 0], [0, -a, 0], [0, 0, 0]], -a * a)]
+    for grad, want in cases:
+        Q, G = _linear_velocity_case(n, grad)
+        prob = oracle.Problem(n=(n, n, n), lo=(-0.5,) * 3, hi=(0.5,) * 3, scheme=scheme, mu=0.0,
+                              bc=((2, 2), (2, 2), (2, 2)))
+        q = oracle.qcriterion(prob, Q, G if scheme == 1 else None)
+        inner = q[2:-2, 2:-2, 2:-2]
+        assert np.abs(inner - want).max() < 1e-12, (scheme, want, inner.min(), inner.max())
