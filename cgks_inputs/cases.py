@@ -107,6 +107,46 @@ def gl_average(fprim, n, lo, hi, gamma, nq=4, nudge=1e-11):
     return Q, G
 
 
+def line_points(dim: int, a: int):
+    """Transverse Gauss-point offsets (reference units) of the line-averaged derivatives along axis a:
+    g = p * n2 + q, p the sign (-, +) along t1 = (a+1)%3, q along t2 = (a+2)%3 (active axes only)."""
+    gq = 0.5 / math.sqrt(3.0)
+    t1, t2 = (a + 1) % 3, (a + 2) % 3
+    n1 = 2 if t1 < dim else 1
+    n2 = 2 if t2 < dim else 1
+    pts = []
+    for p_ in range(n1):
+        for q_ in range(n2):
+            t = [0.0, 0.0, 0.0]
+            if t1 < dim:
+                t[t1] = -gq if p_ == 0 else gq
+            if t2 < dim:
+                t[t2] = -gq if q_ == 0 else gq
+            pts.append(t)
+    return pts
+
+
+def line_derivatives(fprim, n, lo, hi, gamma):
+    """Exact line-averaged derivatives of cons(fprim(x, y, z)) for the line-DOF variant:
+    (Q(x_c + h_a/2 e_a + t) - Q(x_c - h_a/2 e_a + t)) / h_a at the transverse Gauss points t of each axis;
+    layout [nlines][5][nz][ny][nx] (see line_points)."""
+    n = tuple(int(a) for a in n)
+    dim = 3 if n[2] > 1 else (2 if n[1] > 1 else 1)
+    h = [(hi[a] - lo[a]) / n[a] for a in range(3)]
+    c = [lo[a] + (np.arange(n[a]) + 0.5) * h[a] for a in range(3)]
+    Z, Y, X = np.meshgrid(c[2], c[1], c[0], indexing="ij")
+    pos = [X, Y, Z]
+    out = []
+    for a in range(dim):
+        for t in line_points(dim, a):
+            xp = [pos[b] + t[b] * h[b] + (0.5 * h[a] if b == a else 0.0) for b in range(3)]
+            xm = [pos[b] + t[b] * h[b] - (0.5 * h[a] if b == a else 0.0) for b in range(3)]
+            qp = prim_to_cons(*fprim(*xp), gamma)
+            qm = prim_to_cons(*fprim(*xm), gamma)
+            out.append((qp - qm) / h[a])
+    return np.array(out)
+
+
 # ---------------------------------------------------------------------------
 # Config 1: 2-D isentropic vortex (BASELINE.json configs[0]; SURVEY D1 row 1)
 # ---------------------------------------------------------------------------

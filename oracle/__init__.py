@@ -50,6 +50,7 @@ class OrcParams(ctypes.Structure):
         ("k_venkat", ctypes.c_double),
         ("chi_c", ctypes.c_double),
         ("sutherland_S", ctypes.c_double),
+        ("lines", ctypes.c_int),
     ]
 
 
@@ -79,6 +80,13 @@ def lib():
         L.orc_recon_eval.restype = ctypes.c_int
         L.orc_stage_residual.argtypes = [pp, dp, dp, ctypes.c_double, dp, dp, dp, dp]
         L.orc_stage_residual.restype = ctypes.c_int
+        L.orc_recon_eval_l.argtypes = [pp, dp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp,
+                                       dp]
+        L.orc_recon_eval_l.restype = ctypes.c_int
+        L.orc_run_l.argtypes = [pp, dp, dp, dp, ctypes.c_int, ctypes.c_int, dp]
+        L.orc_run_l.restype = ctypes.c_int
+        L.orc_nlines.argtypes = [ctypes.c_int]
+        L.orc_nlines.restype = ctypes.c_int
         L.orc_diagnostics.argtypes = [pp, dp, dp, dp]
         L.orc_diagnostics.restype = ctypes.c_int
         L.orc_qcriterion.argtypes = [pp, dp, dp, dp]
@@ -114,6 +122,7 @@ class Problem:
     k_venkat: float = 0.3
     chi_c: float = 0.01
     sutherland_S: float = 0.0  # 0: constant mu; 0.4042: the paper's Sutherland law
+    lines: int = 0             # CGKS-5th: 1 = line-averaged derivatives as the own-cell data (NEXT-1)
     bc: tuple = ((0, 0), (0, 0), (0, 0))
     bc_state: np.ndarray = field(default_factory=lambda: np.zeros((3, 2, 5)))
 
@@ -133,6 +142,7 @@ class Problem:
         p.tau_eps, p.tau_C, p.relax_C = self.tau_eps, self.tau_C, self.relax_C
         p.k_venkat, p.chi_c = self.k_venkat, self.chi_c
         p.sutherland_S = self.sutherland_S
+        p.lines = int(self.lines)
         return p
 
 
@@ -146,6 +156,22 @@ def run(prob: Problem, Q: np.ndarray, G: np.ndarray | None, nsteps: int, nthread
     p = prob.to_c()
     rc = lib().orc_run(ctypes.byref(p), _ptr(Q), _ptr(Gc), int(nsteps), int(nthreads), _ptr(tout))
     return Q, Gc, float(tout[0]), float(tout[1]), int(rc)
+
+
+def nlines(dim: int) -> int:
+    return int(lib().orc_nlines(int(dim)))
+
+
+def run_lines(prob: Problem, Q: np.ndarray, G: np.ndarray, L: np.ndarray, nsteps: int, nthreads: int = 0):
+    """Line-DOF variant (prob.lines = 1): advance (Q, G, L) by nsteps; L = [nlines][5][nz][ny][nx].
+    Returns (Q, G, L, t, last_dt, rc).  Arrays are copied."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64).copy()
+    Gc = np.ascontiguousarray(G, dtype=np.float64).copy()
+    Lc = np.ascontiguousarray(L, dtype=np.float64).copy()
+    tout = np.zeros(3)
+    p = prob.to_c()
+    rc = lib().orc_run_l(ctypes.byref(p), _ptr(Q), _ptr(Gc), _ptr(Lc), int(nsteps), int(nthreads), _ptr(tout))
+    return Q, Gc, Lc, float(tout[0]), float(tout[1]), int(rc)
 
 
 def dt(prob: Problem, Q: np.ndarray) -> float:
@@ -210,6 +236,22 @@ def recon5_matrix(dim: int):
     ok = L.orc_recon5_matrix(dim, sizes, _ptr(R), B.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
                              N.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _ptr(LS))
     return dict(R=R, basis=B, nbrs=N, ls=LS, rank_ok=bool(ok), nb=nb, nc=nc, nd=nd)
+
+
+def recon_eval_lines(prob: Problem, Q, G, L, ijk, x):
+    """recon_eval with the line-averaged derivatives L ([nlines][5][nz][ny][nx]) of the line-DOF variant."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros((x.shape[0], 20))
+    chi = np.zeros(5)
+    p = prob.to_c()
+    rc = lib().orc_recon_eval_l(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(L), int(ijk[0]), int(ijk[1]), int(ijk[2]),
+                                x.shape[0], _ptr(x), _ptr(out), _ptr(chi))
+    if rc:
+        raise ValueError(f"recon_eval rc={rc}")
+    return out[:, :5], out[:, 5:].reshape(-1, 3, 5), chi
 
 
 def recon_eval(prob: Problem, Q, G, ijk, x):

@@ -47,6 +47,8 @@ typedef struct {
   double k_venkat;          // Venkatakrishnan K (R11)
   double chi_c;             // GENO chi constant (R8)
   double sutherland_S;      // 0: constant mu; > 0: Sutherland law mu(T) = mu (1+S) T^{3/2} / (T+S), T = p/rho
+  int    lines;             // CGKS-5th: 1 = line-averaged derivatives of the own cell as reconstruction data (P:166-172,
+                            // P:197-203), 0 = the own cell-averaged gradient (R1)
 } orc_params;
 
 }  // extern "C"
@@ -551,6 +553,27 @@ long double mono_avg(const int o[3], const int d[3]) {
 // The KKT system of  min |A a - d_a|^2  s.t.  C a = d_c  is solved by Gauss-Jordan
 // elimination in long double.
 // ---------------------------------------------------------------------------
+// line-averaged derivatives: per axis a, the segments through the cell along a at the
+// transverse Gauss points of the faces (R27), joining corresponding face Gauss points (SPEC layout);
+// index l = a * nga + g, g = p * n2 + q with p the sign (-, +) along t1 = (a+1)%3, q along t2 = (a+2)%3
+// (only active transverse axes; nga = 4 / 2 / 1 in 3-D / 2-D / 1-D)
+constexpr int MAXL = 12;
+
+// transverse Gauss points of the lines along axis a: count and reference offsets
+int line_points(int dim, int a, double tpos[4][3]) {
+  const double gq = 0.5 / std::sqrt(3.0);
+  int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
+  bool a1 = t1 < dim, a2 = t2 < dim;
+  int n1 = a1 ? 2 : 1, n2 = a2 ? 2 : 1, g = 0;
+  for (int p = 0; p < n1; ++p)
+    for (int q = 0; q < n2; ++q, ++g) {
+      tpos[g][0] = tpos[g][1] = tpos[g][2] = 0.0;
+      if (a1) tpos[g][t1] = p == 0 ? -gq : gq;
+      if (a2) tpos[g][t2] = q == 0 ? -gq : gq;
+    }
+  return n1 * n2;
+}
+
 struct Recon5 {
   int dim = 0;
   std::vector<MultiIdx> B;                 // basis
@@ -558,6 +581,9 @@ struct Recon5 {
   struct LSRow {
     int cell;         // index into nbrs, or -1 for own cell
     double dir[3];    // reference-unit direction tau (data = sum_a dir_a h_a dQ/dx_a)
+    int line = -1;    // >= 0: line-averaged derivative l of the own cell (data = h_a (dQ/dl)_l)
+    int axis = 0;     // line direction
+    double tpos[3] = {0.0, 0.0, 0.0};  // transverse position of the line (reference units)
   };
   std::vector<LSRow> ls;
   std::vector<double> R;  // nb x nd, row-major
@@ -566,7 +592,7 @@ struct Recon5 {
 };
 
 
-bool build_recon5(int dim, Recon5& rc) {
+bool build_recon5(int dim, Recon5& rc, int lines = 0) {
   rc.dim = dim;
   rc.B = basis(dim, 4);
   rc.nb = (int)rc.B.size();
@@ -618,10 +644,25 @@ bool build_recon5(int dim, Recon5& rc) {
       rc.ls.push_back(r2);
     }
   }
-  for (int a = 0; a < dim; ++a) {
-    Recon5::LSRow r{-1, {0, 0, 0}};
-    r.dir[a] = 1.0;
-    rc.ls.push_back(r);
+  if (!lines) {
+    for (int a = 0; a < dim; ++a) {
+      Recon5::LSRow r{-1, {0, 0, 0}};
+      r.dir[a] = 1.0;
+      rc.ls.push_back(r);
+    }
+  } else {
+    // S^0 = {Q_0, (d_l Q)_{0,G}}: the own cell's line-averaged derivatives (Eq. compact-big-5, 4th row)
+    for (int a = 0, l = 0; a < dim; ++a) {
+      double tp[4][3];
+      int ng = line_points(dim, a, tp);
+      for (int g = 0; g < ng; ++g, ++l) {
+        Recon5::LSRow r{-1, {0, 0, 0}};
+        r.line = l;
+        r.axis = a;
+        for (int b = 0; b < 3; ++b) r.tpos[b] = tp[g][b];
+        rc.ls.push_back(r);
+      }
+    }
   }
   int nb = rc.nb, nc = rc.nc, nl = (int)rc.ls.size();
   rc.nd = nc + nl;
@@ -633,8 +674,29 @@ bool build_recon5(int dim, Recon5& rc) {
       int o[3] = {rc.nbrs[r][0], rc.nbrs[r][1], rc.nbrs[r][2]};
       C[r * nb + k] = mono_avg(o, rc.B[k].d) - mono_avg(zero, rc.B[k].d);
     }
-  // LS rows: average over the cell of the reference directional derivative of p_d
+  // LS rows: average over the cell of the reference directional derivative of p_d; line rows:
+  // (1/|l|) int_l d p_d / dl dl in reference units = p_d(end) - p_d(start) (the zero-mean shift cancels)
   for (int r = 0; r < nl; ++r) {
+    if (rc.ls[r].line >= 0) {
+      const int a = rc.ls[r].axis;
+      for (int k = 0; k < nb; ++k) {
+        long double vp = 1.0L, vm = 1.0L;
+        for (int b = 0; b < 3; ++b) {
+          long double xp = rc.ls[r].tpos[b] + (b == a ? 0.5L : 0.0L);
+          long double xm = rc.ls[r].tpos[b] - (b == a ? 0.5L : 0.0L);
+          long double fp = 1.0L, fm = 1.0L, fact = 1.0L;
+          for (int e = 1; e <= rc.B[k].d[b]; ++e) {
+            fp *= xp;
+            fm *= xm;
+            fact *= e;
+          }
+          vp *= fp / fact;
+          vm *= fm / fact;
+        }
+        A[r * nb + k] = vp - vm;
+      }
+      continue;
+    }
     int o[3] = {0, 0, 0};
     if (rc.ls[r].cell >= 0)
       for (int a = 0; a < 3; ++a) o[a] = rc.nbrs[rc.ls[r].cell][a];
@@ -722,8 +784,11 @@ double basis_deriv(const MultiIdx& m, int a, const double x[3]) {
 // ---------------------------------------------------------------------------
 struct CellState {
   double Q[5];
-  double G[3][5];  // physical cell-averaged gradient, [axis][var]
+  double G[3][5];     // physical cell-averaged gradient, [axis][var]
+  double L[MAXL][5];  // line-averaged derivatives (physical units), used when P.lines
 };
+
+
 
 struct Solver {
   orc_params P;
@@ -762,6 +827,7 @@ struct Solver {
         CellState c;
         std::memcpy(c.Q, P.bc_state[a][side], sizeof(c.Q));
         std::memset(c.G, 0, sizeof(c.G));
+        std::memset(c.L, 0, sizeof(c.L));
         return c;
       } else {  // outflow: zero-order extrapolation of Q and grad Q
         idx[a] = side == 0 ? 0 : n - 1;
@@ -799,6 +865,10 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
     // data vector (exact part, then least-squares part), reference units
     for (int n = 0; n < rc.nc; ++n) d[n] = nb[n].Q[v] - c0.Q[v];
     for (size_t r = 0; r < rc.ls.size(); ++r) {
+      if (rc.ls[r].line >= 0) {  // h_a (d_l Q): reference-unit difference along the line
+        d[rc.nc + r] = S.h[rc.ls[r].axis] * c0.L[rc.ls[r].line][v];
+        continue;
+      }
       const CellState& src = rc.ls[r].cell >= 0 ? nb[rc.ls[r].cell] : c0;
       double s = 0.0;
       for (int a = 0; a < 3; ++a)
@@ -823,9 +893,20 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
       for (int a = 0; a < 3; ++a) cr.bsub[m][a][v] = 0.0;
       // exact constraint: average over Omega_{1,m} of P_m = Q_{1,m}  => b_ax * s = Q_{1,m} - Q_0
       cr.bsub[m][ax][v] = s * (nb[m].Q[v] - c0.Q[v]);
-      // transverse slopes from the target cell's own gradient (R6)
+      // transverse slopes from the target cell's own gradient (R6), or with line DOFs from the
+      // selected line-averaged derivatives: the lines along that transverse axis, averaged (SPEC)
       for (int a = 0; a < S.dim; ++a)
-        if (a != ax) cr.bsub[m][a][v] = S.h[a] * c0.G[a][v];
+        if (a != ax) {
+          if (S.P.lines) {
+            double tp[4][3];
+            const int ng = line_points(S.dim, a, tp);
+            double sum = 0.0;
+            for (int g = 0; g < ng; ++g) sum += c0.L[a * ng + g][v];
+            cr.bsub[m][a][v] = S.h[a] * sum / ng;
+          } else {
+            cr.bsub[m][a][v] = S.h[a] * c0.G[a][v];
+          }
+        }
       IS[m] = 0.0;  // R7
       for (int a = 0; a < 3; ++a) IS[m] += cr.bsub[m][a][v] * cr.bsub[m][a][v];
     }
@@ -961,11 +1042,14 @@ void recon2_eval(const Solver& S, const CellRecon& cr, const double x[3], double
 // ---------------------------------------------------------------------------
 struct FaceAvg {
   double Fn[5], Ft[5], QLn[5], QLt[5], QRn[5], QRt[5];
+  // per Gauss point (line DOFs): relaxed own-side interface values, global frame
+  double gLn[4][5], gLt[4][5], gRn[4][5], gRt[4][5];
 };
 
 struct StageOut {
   std::vector<double> L, Lt;     // 5 per cell
   std::vector<double> Gn, Gt;    // 15 per cell: Gauss theorem of relaxed values, [axis][var]
+  std::vector<double> Ln, Lnt;   // MAXL*5 per cell: line differences of relaxed values (line DOFs)
   int err = 0;
 };
 
@@ -1115,6 +1199,12 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
         back(o.QLt, fa.QLt, wts[g]);
         back(o.QRn, fa.QRn, wts[g]);
         back(o.QRt, fa.QRt, wts[g]);
+        if (g < 4) {
+          back(o.QLn, fa.gLn[g], 1.0);
+          back(o.QLt, fa.gLt[g], 1.0);
+          back(o.QRn, fa.gRn[g], 1.0);
+          back(o.QRt, fa.gRt[g], 1.0);
+        }
       }
       faces[ax][f] = fa;
     }
@@ -1128,6 +1218,8 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
   out.Lt.assign(nc * 5, 0.0);
   out.Gn.assign(nc * 15, 0.0);
   out.Gt.assign(nc * 15, 0.0);
+  out.Ln.assign(nc * MAXL * 5, 0.0);
+  out.Lnt.assign(nc * MAXL * 5, 0.0);
 #pragma omp parallel for schedule(static)
   for (long c = 0; c < nc; ++c) {
     int idx[3] = {(int)(c % S.P.n[0]), (int)((c / S.P.n[0]) % S.P.n[1]), (int)(c / ((long)S.P.n[0] * S.P.n[1]))};
@@ -1146,6 +1238,17 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
         // own side: left state at i+1/2, right state at i-1/2 (R24)
         out.Gn[c * 15 + ax * 5 + v] = (fr.QLn[v] - fl.QRn[v]) / S.h[ax];
         out.Gt[c * 15 + ax * 5 + v] = (fr.QLt[v] - fl.QRt[v]) / S.h[ax];
+      }
+      if (S.P.lines) {
+        // line-averaged derivative along ax at transverse Gauss point g: own-side relaxed values at
+        // the same Gauss point of the two faces, differenced over the cell
+        double tp[4][3];
+        const int ng = line_points(S.dim, ax, tp);
+        for (int g = 0; g < ng; ++g)
+          for (int v = 0; v < 5; ++v) {
+            out.Ln[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLn[g][v] - fl.gRn[g][v]) / S.h[ax];
+            out.Lnt[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLt[g][v] - fl.gRt[g][v]) / S.h[ax];
+          }
       }
     }
   }
@@ -1208,6 +1311,10 @@ int step(Solver& S) {
         for (int a = 0; a < S.dim; ++a)
           for (int v = 0; v < 5; ++v)
             next[c].G[a][v] = s1.Gn[c * 15 + a * 5 + v] + dt * s1.Gt[c * 15 + a * 5 + v];
+      if (compact && S.P.lines)
+        for (int l = 0; l < MAXL; ++l)
+          for (int v = 0; v < 5; ++v)
+            next[c].L[l][v] = s1.Ln[(c * MAXL + l) * 5 + v] + dt * s1.Lnt[(c * MAXL + l) * 5 + v];
     }
   } else {
     // S2O4, interface-value two-stage update for gradients (R24)
@@ -1220,6 +1327,10 @@ int step(Solver& S) {
         for (int a = 0; a < S.dim; ++a)
           for (int v = 0; v < 5; ++v)
             star[c].G[a][v] = s1.Gn[c * 15 + a * 5 + v] + 0.5 * dt * s1.Gt[c * 15 + a * 5 + v];
+      if (compact && S.P.lines)  // line DOFs: the same two-stage rule as the gradients (R24)
+        for (int l = 0; l < MAXL; ++l)
+          for (int v = 0; v < 5; ++v)
+            star[c].L[l][v] = s1.Ln[(c * MAXL + l) * 5 + v] + 0.5 * dt * s1.Lnt[(c * MAXL + l) * 5 + v];
     }
     if (check_positive(S, star)) {
       S.err_stage = 1;
@@ -1237,6 +1348,10 @@ int step(Solver& S) {
         for (int a = 0; a < S.dim; ++a)
           for (int v = 0; v < 5; ++v)
             next[c].G[a][v] = s1.Gn[c * 15 + a * 5 + v] + dt * s2.Gt[c * 15 + a * 5 + v];
+      if (compact && S.P.lines)
+        for (int l = 0; l < MAXL; ++l)
+          for (int v = 0; v < 5; ++v)
+            next[c].L[l][v] = s1.Ln[(c * MAXL + l) * 5 + v] + dt * s2.Lnt[(c * MAXL + l) * 5 + v];
     }
   }
   if (check_positive(S, next)) {
@@ -1250,23 +1365,45 @@ int step(Solver& S) {
   return 0;
 }
 
-void load_state(Solver& S, const double* Q, const double* G) {
+// number of line DOFs per cell for the grid's dimension
+int nlines(int dim) {
+  double tp[4][3];
+  int n = 0;
+  for (int a = 0; a < dim; ++a) n += line_points(dim, a, tp);
+  return n;
+}
+
+// Lq: [nlines][5][nz][ny][nx] or NULL (then each line along a starts from the gradient component a)
+void load_state(Solver& S, const double* Q, const double* G, const double* Lq = nullptr) {
   long nc = S.ncell();
   S.U.assign(nc, CellState());
+  const int nl = nlines(S.dim);
   for (long c = 0; c < nc; ++c) {
     for (int v = 0; v < 5; ++v) S.U[c].Q[v] = Q[v * nc + c];
     for (int a = 0; a < 3; ++a)
       for (int v = 0; v < 5; ++v) S.U[c].G[a][v] = G ? G[(a * 5 + v) * nc + c] : 0.0;
+    for (int a = 0, l = 0; a < S.dim; ++a) {
+      double tp[4][3];
+      const int ng = line_points(S.dim, a, tp);
+      for (int g = 0; g < ng; ++g, ++l)
+        for (int v = 0; v < 5; ++v) S.U[c].L[l][v] = Lq ? Lq[((long)l * 5 + v) * nc + c] : S.U[c].G[a][v];
+    }
+    for (int l = nl; l < MAXL; ++l)
+      for (int v = 0; v < 5; ++v) S.U[c].L[l][v] = 0.0;
   }
 }
 
-void store_state(const Solver& S, double* Q, double* G) {
+void store_state(const Solver& S, double* Q, double* G, double* Lq = nullptr) {
   long nc = S.ncell();
+  const int nl = nlines(S.dim);
   for (long c = 0; c < nc; ++c) {
     for (int v = 0; v < 5; ++v) Q[v * nc + c] = S.U[c].Q[v];
     if (G)
       for (int a = 0; a < 3; ++a)
         for (int v = 0; v < 5; ++v) G[(a * 5 + v) * nc + c] = S.U[c].G[a][v];
+    if (Lq)
+      for (int l = 0; l < nl; ++l)
+        for (int v = 0; v < 5; ++v) Lq[((long)l * 5 + v) * nc + c] = S.U[c].L[l][v];
   }
 }
 
@@ -1279,16 +1416,18 @@ extern "C" {
 
 // Run nsteps steps in place.  Q: [5][nz][ny][nx]; G: [3][5][nz][ny][nx] (may be NULL for GKS-2nd).
 // Returns 0, 2 (config), 3 (positivity).  time_out = [t, last_dt, steps].
-int orc_run(const orc_params* p, double* Q, double* G, int nsteps, int nthreads, double* time_out) {
+// Lq: line-averaged derivatives [nlines][5][nz][ny][nx] (CGKS-5th with p->lines; may be NULL: then the
+// lines start from the gradient components and are not returned)
+int orc_run_l(const orc_params* p, double* Q, double* G, double* Lq, int nsteps, int nthreads, double* time_out) {
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
   Solver S(*p);
-  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
-  load_state(S, Q, G);
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
+  load_state(S, Q, G, Lq);
   int rc = 0;
   for (int s = 0; s < nsteps && rc == 0; ++s) rc = step(S);
-  store_state(S, Q, G);
+  store_state(S, Q, G, Lq);
   if (time_out) {
     time_out[0] = S.t;
     time_out[1] = S.last_dt;
@@ -1296,6 +1435,12 @@ int orc_run(const orc_params* p, double* Q, double* G, int nsteps, int nthreads,
   }
   return rc;
 }
+
+int orc_run(const orc_params* p, double* Q, double* G, int nsteps, int nthreads, double* time_out) {
+  return orc_run_l(p, Q, G, nullptr, nsteps, nthreads, time_out);
+}
+
+int orc_nlines(int dim) { return nlines(dim); }
 
 // global time step from the state (R25); returns -1 on positivity failure
 double orc_dt(const orc_params* p, const double* Q, const double* G) {
@@ -1390,11 +1535,11 @@ int orc_recon5_matrix(int dim, int* sizes, double* R, int* basis_out, int* nbrs_
 
 // Reconstruct cell (i,j,k) of a state and evaluate value + physical derivatives at reference
 // points x (npts*3).  out: npts*(5 + 15) as W[5], dW[3][5].  Also returns chi[5] if chi_out.
-int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i, int j, int k, int npts,
-                   const double* x, double* out, double* chi_out) {
+int orc_recon_eval_l(const orc_params* p, const double* Q, const double* G, const double* Lq, int i, int j, int k,
+                     int npts, const double* x, double* out, double* chi_out) {
   Solver S(*p);
-  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
-  load_state(S, Q, G);
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
+  load_state(S, Q, G, Lq);
   CellRecon cr;
   if (p->scheme == 1)
     recon5_cell(S, S.U, i, j, k, cr);
@@ -1415,6 +1560,11 @@ int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i,
   return 0;
 }
 
+int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i, int j, int k, int npts,
+                   const double* x, double* out, double* chi_out) {
+  return orc_recon_eval_l(p, Q, G, nullptr, i, j, k, npts, x, out, chi_out);
+}
+
 // Flow diagnostics of a state:
 //   out[0] = int 1/2 rho |U|^2 dV              kinetic energy (E_k times rho0 U0^2 |Omega|)
 //   out[1] = int mu(T) |curl U|^2 dV          solenoidal dissipation (eps_S times rho0 U0^2 |Omega|)
@@ -1427,7 +1577,7 @@ int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i,
 // U = (rho U)/rho, dU = (d(rho U) - U d rho)/rho, T = p/rho, mu(T) by viscosity() (R19 / P:469-473).
 int orc_diagnostics(const orc_params* p, const double* Q, const double* G, double* out) {
   Solver S(*p);
-  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
   load_state(S, Q, G);
   const double gx[3] = {-0.5 * std::sqrt(0.6), 0.0, 0.5 * std::sqrt(0.6)};  // nodes on [-1/2, 1/2]
   const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};                // weights, sum 1
@@ -1486,7 +1636,7 @@ int orc_diagnostics(const orc_params* p, const double* Q, const double* G, doubl
 // cell's own reconstruction evaluated at its centroid (reading R35).  out: [ncell], x fastest.
 int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double* out) {
   Solver S(*p);
-  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
   load_state(S, Q, G);
   const long nc = S.ncell();
   int bad = 0;
@@ -1525,7 +1675,7 @@ int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double
 int orc_stage_residual(const orc_params* p, const double* Q, const double* G, double dt, double* L, double* Lt,
                        double* Gn, double* Gt) {
   Solver S(*p);
-  if (p->scheme == 1 && !build_recon5(S.dim, S.rc)) return 2;
+  if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
   load_state(S, Q, G);
   StageOut so;
   int rc = run_stage(S, S.U, dt, so);
