@@ -79,6 +79,9 @@ typedef struct {
   double sutherland_S; /* viscosity law: 0 = constant mu (R19, default); S > 0 = Sutherland law       */
                        /* mu(T) = mu (1 + S) T^{3/2} / (T + S), T = p / rho, with mu the value at T = 1 */
                        /* (S = 0.4042); used in the collision time and the viscous dt bound */
+  int lines;           /* CGKS-5th: 1 = line-averaged derivatives of the own cell as reconstruction data  */
+                       /* (SURVEY 8(f) NEXT-1), carried as extra DOFs per cell;    */
+                       /* 0 = the cell-averaged gradient (R1, default).  Single-rank contexts only.      */
 } cgks_scheme;
 
 /* Fill a cgks_scheme with the paper defaults for scheme id (CGKS_GKS2 / CGKS_CGKS5). */
@@ -122,6 +125,15 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps);
 /* Set the state (user layout, rank-local block).  gradQ may be NULL (zero gradients;
  * not recommended for CGKS-5th, R26; ignored by GKS-2nd).  Resets t and the step count. */
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);
+
+/* Line DOFs (scheme.lines = 1): set / get the line-averaged derivatives, user layout
+ * L[nl][5][nz][ny][nx] with nl = 12 / 4 / 1 (3-D / 2-D / 1-D): line l = a * ngl + g runs along axis a
+ * through the cell at the transverse Gauss point g = p * n2 + q of the faces (p: sign -, + along
+ * (a+1)%3, q along (a+2)%3, active axes only; offsets +-h/(2 sqrt 3)), value (Q(end) - Q(start)) / h_a.
+ * cgks_set_state initialises every line along a with dQ/dx_a; call cgks_set_lines after it to set
+ * exact line data.  Host or device pointers; CGKS_ERR_CONFIG without line DOFs. */
+int cgks_set_lines(cgks_ctx* ctx, const double* L);
+int cgks_get_lines(const cgks_ctx* ctx, double* L);
 
 /* Advance nsteps time steps (each: dt min-reduction, then one S2O4 or S1O2 step).
  * On CGKS_ERR_POSITIVITY / CGKS_ERR_NUMERICAL the state is the last completed step. */

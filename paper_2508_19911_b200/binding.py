@@ -46,6 +46,7 @@ class cgks_scheme(ctypes.Structure):
         ("k_venkat", ctypes.c_double),
         ("chi_c", ctypes.c_double),
         ("sutherland_S", ctypes.c_double),
+        ("lines", ctypes.c_int),
     ]
 
 
@@ -82,6 +83,8 @@ def load(path: str = LIB_PATH):
     L.cgks_get_state.argtypes = [vp, vp, vp]
     L.cgks_get_time.argtypes = [vp, dp, ctypes.POINTER(ctypes.c_int64), dp]
     L.cgks_diagnostics.argtypes = [vp, dp]
+    L.cgks_set_lines.argtypes = [vp, vp]
+    L.cgks_get_lines.argtypes = [vp, vp]
     L.cgks_qcriterion.argtypes = [vp, dp]
     L.cgks_last_error.argtypes = [vp]
     L.cgks_last_error.restype = ctypes.c_char_p
@@ -164,7 +167,7 @@ class Solver:
 
     def __init__(self, n, lo, hi, gamma=1.4, mu=0.0, Pr=1.0, scheme=CGKS_CGKS5, nonlinear=0,
                  time_scheme=CGKS_TIME_DEFAULT, cfl=None, fixed_dt=0.0, tau_eps=0.05, tau_C=10.0, relax_C=10.0,
-                 k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
+                 k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, lines=0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
                  stream=None,
                  nproc=(1, 1, 1), rank=0, nccl_id=None):
         L = load()
@@ -193,6 +196,7 @@ class Solver:
         sc.tau_eps, sc.tau_C, sc.relax_C = float(tau_eps), float(tau_C), float(relax_C)
         sc.k_venkat, sc.chi_c = float(k_venkat), float(chi_c)
         sc.sutherland_S = float(sutherland_S)
+        sc.lines = int(lines)
         ctx = ctypes.c_void_p()
         rc = L.cgks_create(ctypes.byref(g), float(gamma), float(mu), float(Pr), ctypes.byref(sc), ctypes.byref(ctx))
         if rc != CGKS_OK:
@@ -240,6 +244,19 @@ class Solver:
         d = ctypes.c_double()
         self._check(self._L.cgks_get_time(self.ctx, ctypes.byref(t), ctypes.byref(s), ctypes.byref(d)))
         return t.value, s.value, d.value
+
+    def set_lines(self, L):
+        """cgks_set_lines: line-averaged derivatives [nl][5][nz][ny][nx] (line-DOF contexts)."""
+        L = np.ascontiguousarray(L, dtype=np.float64)
+        self._check(self._L.cgks_set_lines(self.ctx, _ptr(L)))
+
+    def get_lines(self):
+        """cgks_get_lines: [nl][5][nz][ny][nx], nl = 12 / 4 / 1 for 3-D / 2-D / 1-D."""
+        dim = 3 if self.n[2] > 1 else (2 if self.n[1] > 1 else 1)
+        nl = {3: 12, 2: 4, 1: 1}[dim]
+        out = np.zeros((nl, 5) + tuple(self.n[::-1]))
+        self._check(self._L.cgks_get_lines(self.ctx, ctypes.c_void_p(out.ctypes.data)))
+        return out
 
     def diagnostics(self):
         """cgks_diagnostics: (int 1/2 rho|U|^2 dV, int mu|curl U|^2 dV, int 4/3 mu (div U)^2 dV,

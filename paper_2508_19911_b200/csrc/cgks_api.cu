@@ -24,6 +24,8 @@
 namespace cgks {
 template <int DIM>
 struct ReconGen;
+template <int DIM>
+struct ReconGenL;
 }
 #define CGKS_RECON_GEN_HOST_TABLES
 #include "recon_gen.cuh"
@@ -114,7 +116,12 @@ struct cgks_ctx {
   ErrState* err = nullptr;
   int cur = 0;
   ClsTables cls;
-  double Rp[ReconGen<3>::NNZ];  // parity-blocked CLS matrix packed in the generated FMA order
+  double Rp[ReconGen<3>::NNZ > ReconGenL<3>::NNZ ? ReconGen<3>::NNZ : ReconGenL<3>::NNZ];  // packed CLS matrix
+  // line DOFs (NEXT-1): lines per cell, buffers paired with U[0], U[1], Us, and the stage carry
+  int lines = 0, nl = 0;
+  double* Lb[2] = {nullptr, nullptr};
+  double* Ls = nullptr;
+  double* Lc = nullptr;
   int nnz = 0;
   char msg[512] = {0};
   // profiling
@@ -191,6 +198,15 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
   a.box = ctx->box;
+  if (ctx->lines) {
+    auto lbuf = [&](const double* X) -> double* {
+      return X == ctx->U[0] ? ctx->Lb[0] : (X == ctx->U[1] ? ctx->Lb[1] : (X == ctx->Us ? ctx->Ls : nullptr));
+    };
+    a.lines = 1;
+    a.Lin = lbuf(Uin);
+    a.Lout = lbuf(Uout);
+    a.Lcarry = ctx->Lc;
+  }
   if (ctx->use_tma) {
     const int b = Uin == ctx->U[0] ? 0 : (Uin == ctx->U[1] ? 1 : (Uin == ctx->Us ? 2 : -1));
     if (b >= 0) {
@@ -307,6 +323,7 @@ void cgks_scheme_defaults(int id, cgks_scheme* s) {
   s->k_venkat = 0.3;
   s->chi_c = 0.01;
   s->sutherland_S = 0.0;
+  s->lines = 0;
 }
 
 int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const cgks_scheme* scheme,
@@ -328,6 +345,10 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     }
   if (!(gamma > 1.0 && gamma <= 5.0 / 3.0 + 1e-12) || !(mu >= 0.0) || !(Pr > 0.0)) {
     set_msg(ctx, "invalid gas parameters gamma=%g mu=%g Pr=%g", gamma, mu, Pr);
+    return fail(CGKS_ERR_CONFIG);
+  }
+  if (scheme->lines && (scheme->id != CGKS_CGKS5 || (grid->nproc[2] > 1))) {
+    set_msg(ctx, "line DOFs need CGKS-5th on a single rank");
     return fail(CGKS_ERR_CONFIG);
   }
   if (!(scheme->sutherland_S >= 0.0)) {
@@ -411,6 +432,12 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   g.k_venkat = scheme->k_venkat;
   g.chi_c = scheme->chi_c;
   g.suth = scheme->sutherland_S;
+  {
+    const int ngl = dim == 3 ? 4 : (dim == 2 ? 2 : 1);
+    g.lines = (scheme->lines && scheme->id == CGKS_CGKS5) ? 1 : 0;
+    g.ngl = ngl;
+    g.nfr = scheme->id == CGKS_CGKS5 ? 30 + (g.lines ? 2 * ngl * 10 : 0) : 10;
+  }
   double hg = 1.0;
   for (int a = 0; a < dim; ++a) hg *= g.h[a];
   hg = std::pow(hg, 1.0 / dim);
@@ -430,16 +457,22 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   // ---- reconstruction tables
   if (ctx->scheme_id == CGKS_CGKS5) {
     char e[256];
-    if (!build_cls(dim, ctx->cls, e, sizeof(e))) {
+    ctx->lines = scheme->lines ? 1 : 0;
+    if (!build_cls(dim, ctx->cls, e, sizeof(e), ctx->lines)) {
       set_msg(ctx, "%s", e);
       return fail(CGKS_ERR_CONFIG);
     }
     // R' = R T^{-1} with T the parity-combination matrix (rows mutually orthogonal): T^{-1} = T^T diag(1/|T_c|^2)
     const int nd = ctx->cls.nd, nb = ctx->cls.nb;
-    const signed char* T = dim == 3 ? &kGenT3[0][0] : (dim == 2 ? &kGenT2[0][0] : &kGenT1[0][0]);
-    const short* P = dim == 3 ? &kGenPairs3[0][0] : (dim == 2 ? &kGenPairs2[0][0] : &kGenPairs1[0][0]);
-    const int nnz = dim == 3 ? kGenNNZ3 : (dim == 2 ? kGenNNZ2 : kGenNNZ1);
-    const int gnd = dim == 3 ? kGenND3 : (dim == 2 ? kGenND2 : kGenND1);
+    const bool L = ctx->lines != 0;
+    const signed char* T = L ? (dim == 3 ? &kGenLT3[0][0] : (dim == 2 ? &kGenLT2[0][0] : &kGenLT1[0][0]))
+                             : (dim == 3 ? &kGenT3[0][0] : (dim == 2 ? &kGenT2[0][0] : &kGenT1[0][0]));
+    const short* P = L ? (dim == 3 ? &kGenLPairs3[0][0] : (dim == 2 ? &kGenLPairs2[0][0] : &kGenLPairs1[0][0]))
+                       : (dim == 3 ? &kGenPairs3[0][0] : (dim == 2 ? &kGenPairs2[0][0] : &kGenPairs1[0][0]));
+    const int nnz = L ? (dim == 3 ? kGenLNNZ3 : (dim == 2 ? kGenLNNZ2 : kGenLNNZ1))
+                      : (dim == 3 ? kGenNNZ3 : (dim == 2 ? kGenNNZ2 : kGenNNZ1));
+    const int gnd = L ? (dim == 3 ? kGenLND3 : (dim == 2 ? kGenLND2 : kGenLND1))
+                      : (dim == 3 ? kGenND3 : (dim == 2 ? kGenND2 : kGenND1));
     if (gnd != nd) {
       set_msg(ctx, "generated reconstruction tables do not match the CLS data layout");
       return fail(CGKS_ERR_CONFIG);
@@ -485,11 +518,16 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   };
   int NV = ctx->NV;
   int nrec = ctx->scheme_id == CGKS_CGKS5 ? ctx->cls.nb * 5 : 15;
-  int nff = ctx->scheme_id == CGKS_CGKS5 ? 30 : 10;
+  int nff = g.nfr;
   const long long nstore = (long long)g.plane * (g.n[2] + 2 * g.zoff) * NV;  // incl. z ghost planes
   bool ok = alloc(&ctx->U[0], nstore) && alloc(&ctx->U[1], nstore) && alloc(&ctx->Us, nstore) &&
             alloc(&ctx->carry, nstore) &&
-            alloc(&ctx->rec, ctx->necell * nrec) && alloc(&ctx->staging, ctx->ncell * 15);
+            alloc(&ctx->rec, ctx->necell * nrec) && alloc(&ctx->staging, ctx->ncell * (g.lines ? 60 : 15));
+  if (ok && g.lines) {
+    ctx->nl = dim * g.ngl;
+    const long long nls = (long long)g.plane * (g.n[2] + 2 * g.zoff) * 5 * ctx->nl;
+    ok = alloc(&ctx->Lb[0], nls) && alloc(&ctx->Lb[1], nls) && alloc(&ctx->Ls, nls) && alloc(&ctx->Lc, nls);
+  }
   for (int a = 0; a < dim && ok; ++a)
     ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] * g.fn[a][2] * nff);
   if (!ok || cudaMalloc((void**)&ctx->ts, sizeof(TimeState)) != cudaSuccess ||
@@ -792,12 +830,52 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
     rc = put(gradQ, 5, 15);
     if (rc) return rc;
   }
+  if (ctx->lines) {  // lines start from the gradients (cgks_set_lines overrides)
+    if (ctx->ops->lines_init(ctx->stream, U, ctx->Lb[0], nc)) CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   TimeState t0;
   std::memset(&t0, 0, sizeof(t0));
   double big = 1e300;
   std::memcpy(&t0.dtmin_bits, &big, sizeof(big));
   CK(cudaMemcpyAsync(ctx->ts, &t0, sizeof(t0), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->err, 0, sizeof(ErrState), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CGKS_OK;
+}
+
+int cgks_set_lines(cgks_ctx* ctx, const double* L) {
+  if (!ctx || !L) return CGKS_ERR_CONFIG;
+  if (!ctx->lines) {
+    set_msg(ctx, "cgks_set_lines: the context has no line DOFs (scheme.lines = 0)");
+    return CGKS_ERR_CONFIG;
+  }
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  const int nf = 5 * ctx->nl;
+  const double* dsrc = L;
+  if (!is_device_ptr(L)) {
+    CK(cudaMemcpyAsync(ctx->staging, L, sizeof(double) * nc * nf, cudaMemcpyHostToDevice, ctx->stream));
+    dsrc = ctx->staging;
+  }
+  if (ctx->ops->pack(ctx->stream, dsrc, ctx->Lb[ctx->cur], nf, 0, nf, nc)) CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CGKS_OK;
+}
+
+int cgks_get_lines(const cgks_ctx* cctx, double* L) {
+  cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
+  if (!ctx || !L) return CGKS_ERR_CONFIG;
+  if (!ctx->lines) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  const int nf = 5 * ctx->nl;
+  const bool dev = is_device_ptr(L);
+  double* ddst = dev ? L : ctx->staging;
+  if (ctx->ops->unpack(ctx->stream, ctx->Lb[ctx->cur], ddst, nf, 0, nf, nc)) CK(cudaGetLastError());
+  if (!dev) CK(cudaMemcpyAsync(L, ctx->staging, sizeof(double) * nc * nf, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return CGKS_OK;
 }
@@ -921,6 +999,10 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (ctx->lines) {
+    set_msg(ctx, "cgks_diagnostics: not available with line DOFs in this version");
+    return CGKS_ERR_CONFIG;
+  }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
     set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
@@ -961,6 +1043,10 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (ctx->lines) {
+    set_msg(ctx, "cgks_qcriterion: not available with line DOFs in this version");
+    return CGKS_ERR_CONFIG;
+  }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
     set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
@@ -1174,7 +1260,7 @@ void cgks_destroy(cgks_ctx* ctx) {
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
                     ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart,
-                    ctx->ctab};
+                    ctx->ctab, ctx->Lb[0], ctx->Lb[1], ctx->Ls, ctx->Lc};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);

@@ -90,9 +90,10 @@ void householder_qr(int m, int n, std::vector<std::vector<ld>>& M, std::vector<s
 
 }  // namespace
 
-bool build_cls(int dim, ClsTables& T, char* err, int errlen) {
+bool build_cls(int dim, ClsTables& T, char* err, int errlen, int lines) {
   std::memset(&T, 0, sizeof(T));
   T.dim = dim;
+  T.lines = lines;
   // basis multi-indices, degree 1..4 over the active axes
   int nb = 0;
   for (int s = 1; s <= 4; ++s)
@@ -132,6 +133,7 @@ bool build_cls(int dim, ClsTables& T, char* err, int errlen) {
     T.lsrow_dir[nl][0] = d0;
     T.lsrow_dir[nl][1] = d1;
     T.lsrow_dir[nl][2] = d2;
+    T.lsrow_line[nl] = -1;
     ++nl;
   };
   for (int m = 0; m < T.nface; ++m)
@@ -148,7 +150,27 @@ bool build_cls(int dim, ClsTables& T, char* err, int errlen) {
       add_row(n, o[0] * r2, o[1] * r2, o[2] * r2);         // towards the target centroid (R2)
     }
   }
-  for (int a = 0; a < dim; ++a) add_row(-1, a == 0, a == 1, a == 2);  // own gradient (R1)
+  if (!lines) {
+    for (int a = 0; a < dim; ++a) add_row(-1, a == 0, a == 1, a == 2);  // own gradient (R1)
+  } else {
+    // own-cell line-averaged derivatives: per axis a, lines at the transverse Gauss points
+    // g = p * n2 + q (p: sign along t1 = (a+1)%3, q: along t2 = (a+2)%3, active axes only)
+    const double gq = 0.5 / std::sqrt(3.0);
+    int l = 0;
+    for (int a = 0; a < dim; ++a) {
+      const int t1 = (a + 1) % 3, t2 = (a + 2) % 3;
+      const int n1 = t1 < dim ? 2 : 1, n2 = t2 < dim ? 2 : 1;
+      for (int p = 0; p < n1; ++p)
+        for (int q = 0; q < n2; ++q, ++l) {
+          add_row(-1, 0, 0, 0);
+          T.lsrow_line[nl - 1] = l;
+          T.lsrow_axis[nl - 1] = a;
+          T.lsrow_t[nl - 1][0] = T.lsrow_t[nl - 1][1] = T.lsrow_t[nl - 1][2] = 0.0;
+          if (t1 < dim) T.lsrow_t[nl - 1][t1] = p == 0 ? -gq : gq;
+          if (t2 < dim) T.lsrow_t[nl - 1][t2] = q == 0 ? -gq : gq;
+        }
+    }
+  }
   T.nl = nl;
   T.nd = nc + nl;
 
@@ -158,6 +180,27 @@ bool build_cls(int dim, ClsTables& T, char* err, int errlen) {
   for (int r = 0; r < nc; ++r)
     for (int k = 0; k < nb; ++k) C[r][k] = mavg(T.nbr[r], T.expo[k]) - mavg(zero, T.expo[k]);
   for (int r = 0; r < nl; ++r) {
+    if (T.lsrow_line[r] >= 0) {
+      // (1/|l|) int_l dp/dl dl in reference units: p at the line's end minus p at its start
+      const int a = T.lsrow_axis[r];
+      for (int k = 0; k < nb; ++k) {
+        ld vp = 1, vm = 1;
+        for (int b = 0; b < 3; ++b) {
+          const ld xp = (ld)T.lsrow_t[r][b] + (b == a ? 0.5L : 0.0L);
+          const ld xm = (ld)T.lsrow_t[r][b] - (b == a ? 0.5L : 0.0L);
+          ld fp = 1, fm = 1, fa = 1;
+          for (int e = 1; e <= T.expo[k][b]; ++e) {
+            fp *= xp;
+            fm *= xm;
+            fa *= e;
+          }
+          vp *= fp / fa;
+          vm *= fm / fa;
+        }
+        A[r][k] = vp - vm;
+      }
+      continue;
+    }
     int o[3] = {0, 0, 0};
     if (T.lsrow_cell[r] >= 0)
       for (int a = 0; a < 3; ++a) o[a] = T.nbr[T.lsrow_cell[r]][a];

@@ -38,6 +38,11 @@ struct StageArgs {
   int scheme;     // 0 GKS-2nd, 1 CGKS-5th
   int nonlinear;
   int box;
+  // line DOFs (CGKS-5th, NEXT-1): lines of Uin, of Uout, and the stage carry ([z][l*5+v][y][x])
+  const double* Lin = nullptr;
+  double* Lout = nullptr;
+  double* Lcarry = nullptr;
+  int lines = 0;
   // TMA descriptors of the flux tiles per normal axis (reconstruction fields; cell averages of Uin)
   const CUtensorMap* tm_rec = nullptr;
   const CUtensorMap* tm_U = nullptr;
@@ -59,6 +64,8 @@ struct DimOps {
   void (*flux_tile)(int ax, int* tx, int* tn);
   // Q-criterion of a.Uin at the cell centroids (reconstruction + k_qcrit) into out[ncell]
   int (*qcrit)(LaunchEnv& env, const StageArgs& a, const double* wc, double* out);
+  // line DOFs initialised from the gradients of U
+  int (*lines_init)(cudaStream_t s, const double* U, double* Lb, long long ncell);
 };
 
 extern const DimOps kOps1, kOps2, kOps3;

@@ -21,6 +21,8 @@
 namespace cgks {
 template <int DIM>
 struct ReconGen;
+template <int DIM>
+struct ReconGenL;  // line-DOF variant
 }
 #include "recon_gen.cuh"
 
@@ -31,7 +33,8 @@ constexpr int NBmax = 34;
 // per translation unit (one per dimension, see stage_impl.cuh): internal linkage
 static __constant__ Geo c_geo;
 static __constant__ FluxConst c_fc;
-static __constant__ double c_Rp[ReconGen<3>::NNZ];  // parity-blocked CLS matrix (gen_recon.py), packed
+constexpr int kMaxNNZ = ReconGen<3>::NNZ > ReconGenL<3>::NNZ ? ReconGen<3>::NNZ : ReconGenL<3>::NNZ;
+static __constant__ double c_Rp[kMaxNNZ];  // parity-blocked CLS matrix (gen_recon.py), packed
 
 // ---------------------------------------------------------------------------
 // compile-time stencil tables (match cls_build.cpp ordering)
@@ -195,6 +198,8 @@ template <int DIM>
 struct Recon5TileLoader {
   const double* __restrict__ s;  // staged fields of this component, at this thread's cell
   double q0, h0, h1, h2;
+  const double* __restrict__ lv = nullptr;  // line DOFs: line 0 of this component at this cell (field stride plane)
+  long long lstride = 0;                    // 5 * plane: next line
   static constexpr int HALO = ReconTile<DIM>::HALO;
   static constexpr int SY = ReconTile<DIM>::HX, SZ = ReconTile<DIM>::HX * ReconTile<DIM>::HY;
   __device__ __forceinline__ double at(int f, int ox, int oy, int oz) const {
@@ -203,6 +208,12 @@ struct Recon5TileLoader {
   __device__ __forceinline__ double q(int ox, int oy, int oz) const { return at(0, ox, oy, oz) - q0; }
   __device__ __forceinline__ double g(int a, int ox, int oy, int oz) const {
     return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * at(1 + a, ox, oy, oz);
+  }
+  // own-cell line-averaged derivative l in reference units (h_a (d_l Q)_l, a = l / lines per axis)
+  __device__ __forceinline__ double line(int l) const {
+    constexpr int NGL = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
+    const int a = l / NGL;
+    return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * __ldg(lv + l * lstride);
   }
 };
 
@@ -247,10 +258,11 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int DIM, bool NONLIN, bool BOX>
+template <int DIM, bool NONLIN, bool BOX, bool LINES = false>
 __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double* __restrict__ U,
                                                                     double* __restrict__ coef,
-                                                                    const ErrState* __restrict__ err) {
+                                                                    const ErrState* __restrict__ err,
+                                                                    const double* __restrict__ Lin = nullptr) {
   using S = Sten<DIM>;
   using RT = ReconTile<DIM>;
   constexpr int NCO = S::NB * 5;
@@ -286,18 +298,36 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
     __syncthreads();
     Recon5TileLoader<DIM> L{cur + own, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
     L.q0 = L.at(0, 0, 0, 0);
+    if (LINES) {  // own-cell lines, [z][l*5+v][y][x] (valid cells only; ragged threads read cell 0)
+      constexpr int NLF = 5 * (DIM == 3 ? 12 : (DIM == 2 ? 4 : 1));
+      L.lv = Lin + (valid ? sidx(NLF, v, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, k)) : 0);
+      L.lstride = 5 * c_geo.plane;
+    }
     double acc[S::NB];
 #pragma unroll
     for (int q = 0; q < S::NB; ++q) acc[q] = 0.0;
     // parity-blocked constrained least squares: data in difference form, so a
     // uniform field gives exactly zero coefficients
-    ReconGen<DIM>::matvec(L, c_Rp, acc);
+    if (LINES)
+      ReconGenL<DIM>::matvec(L, c_Rp, acc);
+    else
+      ReconGen<DIM>::matvec(L, c_Rp, acc);
     if (NONLIN) {
       // GENO: sub-stencil linears P_m (R6), IS (R7), weights (R9), chi (R8);
       // Eq. (weno-new) folded into the coefficients (shared zero-mean basis, sum omega = 1)
       double IS[S::NFACE], bm[S::NFACE][3], gown[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) gown[a] = L.g(a, 0, 0, 0);
+      for (int a = 0; a < DIM; ++a) {
+        if (LINES) {  // the selected line derivatives: the lines along a, averaged (SPEC)
+          constexpr int NGL = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
+          double sum = 0.0;
+#pragma unroll
+          for (int g = 0; g < NGL; ++g) sum += L.line(a * NGL + g);
+          gown[a] = sum * (1.0 / NGL);
+        } else {
+          gown[a] = L.g(a, 0, 0, 0);
+        }
+      }
 #pragma unroll
       for (int m = 0; m < S::NFACE; ++m) {
         const int ax = m / 2;
@@ -454,7 +484,7 @@ struct FluxTile {
   static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128) + 16; }
 };
 
-template <int DIM, int AX, bool COMPACT, bool BOX>
+template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false>
 __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
                                                const double* __restrict__ gtab, double* __restrict__ face,
                                                const TimeState* __restrict__ ts, ErrState* __restrict__ err,
@@ -662,7 +692,9 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
   const int fn1 = c_geo.fn[AX][1];
   const long long fpl = (long long)fn0 * fn1;
-  const long long base = (long long)k * NF * fpl + (long long)j * fn0 + i;
+  constexpr int NGL_ = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
+  constexpr int NFR = COMPACT ? (LINES ? 30 + 2 * NGL_ * 10 : 30) : NF;  // face record fields
+  const long long base = (long long)k * NFR * fpl + (long long)j * fn0 + i;
   const double wgt = 1.0 / NG;
   // back to the global frame with weight 1/NG: y[0..9] = Fn, Ft (equal in both lanes), y[10..19] =
   // this side's Qn, Qt (QL on side 0, QR on side 1)
@@ -675,6 +707,14 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       const int g = cc == 0 ? 0 : (cc == 4 ? 4 : 1 + (cc == 1 ? P0 : (cc == 2 ? P1 : P2)));
       y[s * 5 + g] = a;  // the 1/NG weight is applied after the Gauss-point sum (exact: a power of 2)
     }
+  }
+  if (COMPACT && LINES && valid) {
+    // line DOFs: this lane's own-side relaxed values at its Gauss point, in the line order g = p * n2 + q
+    // (p along TA, q along TB): Gauss point gp has signs (sA, sB) = (bit 0, bit 1)
+    const int gcan = NG == 4 ? 2 * (gp & 1) + ((gp >> 1) & 1) : gp;
+    double* dst = face + base + (long long)(30 + (side * NG + gcan) * 10) * fpl;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) dst[q * fpl] = y[10 + q];
   }
   if constexpr (NG == 1) {
     if (valid && side == 0) {
@@ -730,13 +770,15 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
 //   MODE 1: S2O4 stage 2  (carry -> Uout = U^{n+1})
 //   MODE 2: S1O2          (Uin = U^n -> Uout = U^{n+1})
 // ---------------------------------------------------------------------------
-template <int DIM, bool COMPACT, int MODE>
+template <int DIM, bool COMPACT, int MODE, bool LINES = false>
 __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, const double* __restrict__ fx,
                                                  const double* __restrict__ fy, const double* __restrict__ fz,
                                                  double* __restrict__ Uout, double* __restrict__ carry,
-                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err) {
+                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
+                                                 double* __restrict__ Lout = nullptr,
+                                                 double* __restrict__ Lcarry = nullptr) {
   constexpr int NV = COMPACT ? 20 : 5;
-  constexpr int NF = COMPACT ? 30 : 10;
+  constexpr int NF = COMPACT ? (LINES ? 30 + 2 * (DIM == 3 ? 4 : (DIM == 2 ? 2 : 1)) * 10 : 30) : 10;
   if (err->code) return;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
@@ -818,6 +860,41 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
         for (int v = 0; v < 5; ++v) {
           const double gn = a < DIM ? Gn[a][v] : 0.0, gt = a < DIM ? Gt[a][v] : 0.0;
           Uout[sidx(NV, 5 + a * 5 + v, i, j, k)] = gn + dt * gt;
+        }
+    }
+  }
+  if (COMPACT && LINES) {
+    // line-averaged derivatives: per axis a and line g, the own-side relaxed values at
+    // Gauss point g of the faces i+1/2 (left side) and i-1/2 (right side), with the gradients'
+    // two-stage rule (R24); layout [z][l*5+v][y][x]
+    constexpr int NGL = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
+    constexpr int NLF = 5 * DIM * NGL;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const int fn0 = c_geo.fn[a][0], fn1 = c_geo.fn[a][1];
+      const long long fpl = (long long)fn0 * fn1;
+      const int wi = c_geo.bounded[0] ? i + (a == 0) : wrapi(i + (a == 0), c_geo.n[0]);
+      const int wj = c_geo.bounded[1] ? j + (a == 1) : wrapi(j + (a == 1), c_geo.n[1]);
+      const int wk = c_geo.bounded[2] ? k + (a == 2) : wrapi(k + (a == 2), c_geo.n[2]);
+      const double* flo = F[a] + (long long)k * NF * fpl + (long long)j * fn0 + i;
+      const double* fhi = F[a] + (long long)wk * NF * fpl + (long long)wj * fn0 + wi;
+      const double ih = c_geo.ih[a];
+#pragma unroll
+      for (int g = 0; g < NGL; ++g)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double ln = (__ldg(fhi + (30 + g * 10 + v) * fpl) - __ldg(flo + (30 + (NGL + g) * 10 + v) * fpl)) * ih;
+          const double lt =
+              (__ldg(fhi + (35 + g * 10 + v) * fpl) - __ldg(flo + (35 + (NGL + g) * 10 + v) * fpl)) * ih;
+          const long long o = sidx(NLF, (a * NGL + g) * 5 + v, i, j, k);
+          if (MODE == 0) {
+            Lout[o] = ln + 0.5 * dt * lt;
+            Lcarry[o] = ln;
+          } else if (MODE == 1) {
+            Lout[o] = Lcarry[o] + dt * lt;
+          } else {
+            Lout[o] = ln + dt * lt;
+          }
         }
     }
   }
@@ -1077,6 +1154,23 @@ __global__ void __launch_bounds__(256) k_qcrit(const double* __restrict__ U, con
 #pragma unroll
     for (int b = 0; b < 3; ++b) q -= 0.5 * dU[a][b] * dU[b][a];
   out[t] = q;
+}
+
+// line DOFs from the cell-averaged gradients (each line along a starts as dQ/dx_a), [z][l*5+v][y][x]
+template <int DIM>
+__global__ void k_lines_from_grad(const double* __restrict__ U, double* __restrict__ Lb) {
+  constexpr int NGL = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
+  constexpr int NLF = 5 * DIM * NGL;
+  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc) return;
+  const int i = (int)(t % c_geo.n[0]);
+  const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
+  const int k = (int)(t / c_geo.plane);
+  for (int a = 0; a < DIM; ++a)
+    for (int g = 0; g < NGL; ++g)
+      for (int v = 0; v < 5; ++v)
+        Lb[sidx(NLF, (a * NGL + g) * 5 + v, i, j, k)] = U[sidx(20, 5 + a * 5 + v, i, j, k)];
 }
 
 }  // namespace cgks

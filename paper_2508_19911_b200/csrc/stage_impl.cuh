@@ -44,10 +44,10 @@ int launch(LaunchEnv& env, const char* name, void (*kern)(KArgs...), long long n
 constexpr int D = CGKS_DIM;
 
 // reconstruction: one block per TX x TY x TZ cells of the extended range, shared-memory halo tile
-template <bool NONLIN, bool BOX>
+template <bool NONLIN, bool BOX, bool LINES = false>
 int recon5_launch(LaunchEnv& env, const StageArgs& a) {
   using RT = ReconTile<D>;
-  auto kern = k_recon5<D, NONLIN, BOX>;
+  auto kern = k_recon5<D, NONLIN, BOX, LINES>;
   static bool attr = false;
   const size_t smem = RT::smem_bytes();
   if (!attr) {
@@ -62,7 +62,7 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0, env.stream);
   }
-  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err);
+  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err, a.Lin);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of recon5 failed: %s", cudaGetErrorString(e));
@@ -76,10 +76,10 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 }
 
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
-template <bool COMPACT, bool BOX, int AX>
+template <bool COMPACT, bool BOX, int AX, bool LINES = false>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
   using FT = FluxTile<D, AX, COMPACT>;
-  auto kern = k_flux<D, AX, COMPACT, BOX>;
+  auto kern = k_flux<D, AX, COMPACT, BOX, LINES>;
   static bool attr = false;
   const size_t smem = FT::smem_bytes();
   if (!attr) {
@@ -112,34 +112,40 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
   return 0;
 }
 
-template <bool COMPACT, bool NONLIN, bool BOX>
+template <bool COMPACT, bool NONLIN, bool BOX, bool LINES = false>
 int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   if (COMPACT) {
-    int rc = recon5_launch<NONLIN, BOX>(env, a);
+    int rc = recon5_launch<NONLIN, BOX, LINES>(env, a);
     if (rc) return rc;
   } else {
     LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
   {
-    int rc = flux_launch<COMPACT, BOX, 0>(env, "flux_x", a, stage);
-    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0)>(env, "flux_y", a, stage);
-    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0)>(env, "flux_z", a, stage);
+    int rc = flux_launch<COMPACT, BOX, 0, LINES>(env, "flux_x", a, stage);
+    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0), LINES>(env, "flux_y", a, stage);
+    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES>(env, "flux_z", a, stage);
     if (rc) return rc;
   }
   if (mode == 0)
-    LAUNCH("update", (k_update<D, COMPACT, 0>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err);
+    LAUNCH("update", (k_update<D, COMPACT, 0, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
   else if (mode == 1)
-    LAUNCH("update", (k_update<D, COMPACT, 1>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err);
+    LAUNCH("update", (k_update<D, COMPACT, 1, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
   else
-    LAUNCH("update", (k_update<D, COMPACT, 2>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err);
+    LAUNCH("update", (k_update<D, COMPACT, 2, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
+           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
   return 0;
 }
 
 int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
+  if (c && a.lines) {  // CGKS-5th with line DOFs (NEXT-1)
+    if (!nl && !b) return stage_t<true, false, false, true>(env, a, mode, stage);
+    if (nl && !b) return stage_t<true, true, false, true>(env, a, mode, stage);
+    if (!nl && b) return stage_t<true, false, true, true>(env, a, mode, stage);
+    return stage_t<true, true, true, true>(env, a, mode, stage);
+  }
   if (c && !nl && !b) return stage_t<true, false, false>(env, a, mode, stage);
   if (c && nl && !b) return stage_t<true, true, false>(env, a, mode, stage);
   if (c && !nl && b) return stage_t<true, false, true>(env, a, mode, stage);
@@ -214,6 +220,11 @@ void flux_tile_fn(int ax, int* tx, int* tn) {
     *tx = FluxTile<D, (D > 2 ? 2 : 0), true>::TX;
     *tn = FluxTile<D, (D > 2 ? 2 : 0), true>::TN;
   }
+}
+
+int lines_init_fn(cudaStream_t s, const double* U, double* Lb, long long ncell) {
+  k_lines_from_grad<D><<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(U, Lb);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
 int upload_fn(const Geo& g, const FluxConst& fc, const double* Rp, int nnz, cudaStream_t s) {

@@ -26,6 +26,9 @@ struct Geo {
   double cfl, fixed_dt, mu, gamma;
   double k_venkat, chi_c, eps_venkat2;
   double suth;  // Sutherland constant S (0: constant mu)
+  int lines;    // CGKS-5th line-DOF variant
+  int ngl;      // lines per axis (transverse face Gauss points: 4 / 2 / 1)
+  int nfr;      // fields of a face record (30, plus 2 x ngl x 10 per-Gauss-point values with lines)
 };
 
 struct ErrState {

@@ -26,8 +26,27 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "csrc", "recon_gen.cuh")
 
 
-def items_for(dim):
-    """Raw data items in the order of cls_build.cpp: (offset, direction or None)."""
+def line_points(dim, a):
+    """sign patterns of the transverse Gauss points of the lines along a (cls_build.cpp order):
+    g = p * n2 + q, p the sign along t1 = (a+1)%3, q along t2 = (a+2)%3 (active axes only)"""
+    t1, t2 = (a + 1) % 3, (a + 2) % 3
+    n1 = 2 if t1 < dim else 1
+    n2 = 2 if t2 < dim else 1
+    pts = []
+    for p in range(n1):
+        for q in range(n2):
+            t = [0, 0, 0]
+            if t1 < dim:
+                t[t1] = -1 if p == 0 else 1
+            if t2 < dim:
+                t[t2] = -1 if q == 0 else 1
+            pts.append(tuple(t))
+    return pts
+
+
+def items_for(dim, lines=False):
+    """Raw data items in the order of cls_build.cpp: (offset, direction or None); with line DOFs the
+    own-gradient items are replaced by ('L', l, axis, transverse sign pattern) items."""
     nbrs = []
     for a in range(dim):
         for s in (-1, 1):
@@ -61,10 +80,17 @@ def items_for(dim):
             d[t] = 1.0
             items.append((o, tuple(d)))
             items.append((o, (o[0] * r2, o[1] * r2, o[2] * r2)))
-    for a in range(dim):
-        d = [0.0, 0.0, 0.0]
-        d[a] = 1.0
-        items.append(((0, 0, 0), tuple(d)))
+    if not lines:
+        for a in range(dim):
+            d = [0.0, 0.0, 0.0]
+            d[a] = 1.0
+            items.append(((0, 0, 0), tuple(d)))
+    else:
+        l = 0
+        for a in range(dim):
+            for t in line_points(dim, a):
+                items.append(("L", l, a, t))
+                l += 1
     return items
 
 
@@ -84,8 +110,22 @@ def _key(o, d):
     return (o, None if d is None else tuple(round(x, 12) for x in d))
 
 
+def _ikey(item):
+    if item[0] == "L":
+        return ("L", item[2], item[3])
+    return _key(*item)
+
+
 def reflect(item, a, index):
-    """Image of a data item under reflection of axis a: (item index, sign)."""
+    """Image of a data item under reflection of axis a: (item index, sign).  A line along a changes
+    sign (its two ends swap); a reflection of a transverse axis maps it to the mirrored line."""
+    if item[0] == "L":
+        _, l, ax, t = item
+        if a == ax:
+            return index[("L", ax, t)], -1
+        t2 = list(t)
+        t2[a] = -t2[a]
+        return index[("L", ax, tuple(t2))], 1
     o, d = item
     o2 = list(o)
     o2[a] = -o2[a]
@@ -101,9 +141,9 @@ def reflect(item, a, index):
     return index[k], -1
 
 
-def build(dim):
-    items = items_for(dim)
-    index = {_key(*it): i for i, it in enumerate(items)}
+def build(dim, lines=False):
+    items = items_for(dim, lines)
+    index = {_ikey(it): i for i, it in enumerate(items)}
     n = len(items)
     # group elements g in {0,1}^dim; action of g = product of reflections
     def act(i, g):
@@ -157,11 +197,13 @@ def emit():
              "// Parity-blocked CLS matvec of the CGKS-5th reconstruction (see gen_recon.py).",
              "#pragma once", "", "namespace cgks {", ""]
     host = []
-    for dim in (1, 2, 3):
-        items, combos, orbits, B, pairs = build(dim)
+    for dim, lv in [(d, v) for v in (False, True) for d in (1, 2, 3)]:
+        items, combos, orbits, B, pairs = build(dim, lv)
         n, nb = len(items), len(B)
-        lines.append(f"// dim {dim}: {n} data, {nb} coefficients, {len(pairs)} FMA per component")
-        lines.append(f"template <> struct ReconGen<{dim}> {{")
+        sname = "ReconGenL" if lv else "ReconGen"
+        tp = "kGenL" if lv else "kGen"
+        lines.append(f"// dim {dim}{' (line DOFs)' if lv else ''}: {n} data, {nb} coefficients, {len(pairs)} FMA per component")
+        lines.append(f"template <> struct {sname}<{dim}> {{")
         lines.append(f"  static constexpr int ND = {n}, NB = {nb}, NNZ = {len(pairs)};")
         ex = ",".join("{%d,%d,%d}" % b for b in B)
         lines.append("  // basis exponents d of p_d (Eq. base), in coefficient order")
@@ -184,6 +226,9 @@ def emit():
         for orb in orbits:
             lines.append("    {")
             for j in orb:
+                if items[j][0] == "L":
+                    lines.append(f"      const double r{j} = L.line({items[j][1]});")
+                    continue
                 o, d = items[j]
                 if d is None:
                     lines.append(f"      const double r{j} = L.q({o[0]}, {o[1]}, {o[2]});")
@@ -226,15 +271,15 @@ def emit():
         lines.append("};")
         lines.append("")
         # host tables
-        host.append(f"static const int kGenND{dim} = {n}, kGenNB{dim} = {nb}, kGenNNZ{dim} = {len(pairs)};")
+        host.append(f"static const int {tp}ND{dim} = {n}, {tp}NB{dim} = {nb}, {tp}NNZ{dim} = {len(pairs)};")
         rows = []
         for c, (cls, vec) in enumerate(combos):
             row = [0] * n
             for j, v in vec.items():
                 row[j] = v
             rows.append("{" + ",".join(str(x) for x in row) + "}")
-        host.append(f"static const signed char kGenT{dim}[{n}][{n}] = {{" + ",\n  ".join(rows) + "};")
-        host.append(f"static const short kGenPairs{dim}[{len(pairs)}][2] = {{" +
+        host.append(f"static const signed char {tp}T{dim}[{n}][{n}] = {{" + ",\n  ".join(rows) + "};")
+        host.append(f"static const short {tp}Pairs{dim}[{len(pairs)}][2] = {{" +
                     ",".join(f"{{{k},{c}}}" for (k, c) in emitted_pairs) + "};")
         host.append("")
     lines.append("}  // namespace cgks")
@@ -253,8 +298,8 @@ def emit():
 
 
 if __name__ == "__main__":
-    for d in (1, 2, 3):
-        it, co, orb, B, pairs = build(d)
+    for d, lv in [(d, v) for v in (False, True) for d in (1, 2, 3)]:
+        it, co, orb, B, pairs = build(d, lv)
         print(f"dim {d}: data {len(it)}, basis {len(B)}, orbits {len(orb)}, FMA/component {len(pairs)}"
               f" (dense {len(it) * len(B)})")
     print(emit())
