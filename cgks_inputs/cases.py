@@ -65,16 +65,21 @@ def _gl(nq):
     return 0.5 * x, 0.5 * w  # nodes on [-1/2, 1/2], weights sum to 1
 
 
-def gl_average(fprim, n, lo, hi, gamma, nq=4, nudge=1e-11):
+def gl_average(fprim, n, lo, hi, gamma, nq=4, nudge=1e-11, mesh_nodes=None):
     """Cell averages and cell-averaged gradients of cons(fprim(x, y, z)) by
     nq-point Gauss-Legendre per active axis; gradient by the Gauss theorem
-    (face averages of the point values, evaluated just inside the cell)."""
+    (face averages of the point values, evaluated just inside the cell).
+    mesh_nodes: per-axis node coordinates of a stretched tensor-product mesh (or None: uniform)."""
     n = tuple(int(a) for a in n)
     dim = 3 if n[2] > 1 else (2 if n[1] > 1 else 1)
-    h = [(hi[a] - lo[a]) / n[a] for a in range(3)]
+    if mesh_nodes is None:
+        h = [(hi[a] - lo[a]) / n[a] * np.ones(n[a]) for a in range(3)]
+        centres = [lo[a] + (np.arange(n[a]) + 0.5) * (hi[a] - lo[a]) / n[a] for a in range(3)]
+    else:
+        h = [np.diff(np.asarray(mesh_nodes[a], dtype=np.float64)) for a in range(3)]
+        centres = [0.5 * (np.asarray(mesh_nodes[a])[1:] + np.asarray(mesh_nodes[a])[:-1]) for a in range(3)]
     xi, wi = _gl(nq)
     nodes = [(xi, wi) if a < dim else (np.zeros(1), np.ones(1)) for a in range(3)]
-    centres = [lo[a] + (np.arange(n[a]) + 0.5) * h[a] for a in range(3)]
 
     def fcons(x, y, z):
         return prim_to_cons(*fprim(x, y, z), gamma)
@@ -84,12 +89,13 @@ def gl_average(fprim, n, lo, hi, gamma, nq=4, nudge=1e-11):
     for k in range(n[2]):
         zc = centres[2][k]
         Z3, Y3, X3 = np.meshgrid([zc], centres[1], centres[0], indexing="ij")
+        H3 = [h[0][None, None, :], h[1][None, :, None], np.array(h[2][k])[None, None, None]]
         # volume average
         acc = np.zeros((5, 1, n[1], n[0]))
         for (pz, wz) in zip(*nodes[2]):
             for (py, wy) in zip(*nodes[1]):
                 for (px, wx) in zip(*nodes[0]):
-                    acc += wx * wy * wz * fcons(X3 + px * h[0], Y3 + py * h[1], Z3 + pz * h[2])
+                    acc += wx * wy * wz * fcons(X3 + px * H3[0], Y3 + py * H3[1], Z3 + pz * H3[2])
         Q[:, k] = acc[:, 0]
         # Gauss theorem: (face avg at +1/2 - face avg at -1/2)/h along each active axis
         for a in range(dim):
@@ -101,10 +107,38 @@ def gl_average(fprim, n, lo, hi, gamma, nq=4, nudge=1e-11):
                 for (pz, wz) in zip(*tn[2]):
                     for (py, wy) in zip(*tn[1]):
                         for (px, wx) in zip(*tn[0]):
-                            acc += wx * wy * wz * fcons(X3 + px * h[0], Y3 + py * h[1], Z3 + pz * h[2])
+                            acc += wx * wy * wz * fcons(X3 + px * H3[0], Y3 + py * H3[1], Z3 + pz * H3[2])
                 face.append(acc[:, 0])
-            G[a, :, k] = (face[0] - face[1]) / h[a]
+            G[a, :, k] = (face[0] - face[1]) / H3[a][0]
     return Q, G
+
+
+def stretched_nodes(n: int, lo: float, hi: float, beta: float = 0.0, kind: str = "sine"):
+    """Node coordinates of a smoothly stretched axis (NEXT-4; tensor-product meshes of the jet runs,
+    P:574-594): 'sine' x = lo + L (s + beta sin(2 pi s) / (2 pi)) on s = k/n (periodic-compatible,
+    spacing ratio (1 + beta) / (1 - beta)); 'tanh' clusters nodes at the centre (jet shear layer):
+    x = lo + L (1 + tanh(beta (s - 1/2)) / tanh(beta / 2)) / 2."""
+    s_ = np.arange(n + 1) / n
+    L = hi - lo
+    if kind == "sine":
+        return lo + L * (s_ + beta * np.sin(2 * math.pi * s_) / (2 * math.pi))
+    if kind == "tanh":
+        return lo + L * 0.5 * (1.0 + np.tanh(beta * (s_ - 0.5)) / math.tanh(0.5 * beta))
+    raise ValueError(kind)
+
+
+def jet_inflow(r, M_j=0.9, T_j=1.0, T_inf=1.0, R0=0.5, theta=0.02, gamma=1.4):
+    """Round-jet inflow profile (NEXT-4 input generator, the jet runs of P:574-594 stay out of scope):
+    hyperbolic-tangent axial velocity u(r) = (U_j/2)(1 + tanh((R0 - r)/(2 theta))), with the Crocco-Busemann
+    relation for the temperature, T = T_inf + (T_j - T_inf) u/U_j + (gamma-1)/2 M_j^2 T_j (u/U_j)(1 - u/U_j),
+    uniform pressure p = 1/gamma (sound speed 1 at T = 1), rho = gamma p / T.  Returns (rho, u, p)."""
+    Uj = M_j * math.sqrt(T_j)
+    u = 0.5 * Uj * (1.0 + np.tanh((R0 - np.asarray(r)) / (2.0 * theta)))
+    f = u / Uj
+    T = T_inf + (T_j - T_inf) * f + 0.5 * (gamma - 1.0) * M_j ** 2 * T_j * f * (1.0 - f)
+    p = np.full_like(u, 1.0 / gamma)
+    rho = gamma * p / T
+    return rho, u, p
 
 
 def line_points(dim: int, a: int):

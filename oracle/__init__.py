@@ -51,6 +51,7 @@ class OrcParams(ctypes.Structure):
         ("chi_c", ctypes.c_double),
         ("sutherland_S", ctypes.c_double),
         ("lines", ctypes.c_int),
+        ("nodes", ctypes.POINTER(ctypes.c_double) * 3),
     ]
 
 
@@ -123,6 +124,7 @@ class Problem:
     chi_c: float = 0.01
     sutherland_S: float = 0.0  # 0: constant mu; 0.4042: the paper's Sutherland law
     lines: int = 0             # CGKS-5th: 1 = line-averaged derivatives as the own-cell data (NEXT-1)
+    nodes: tuple = None        # stretched tensor-product mesh (NEXT-4): per-axis node coordinates (n_a + 1) or None
     bc: tuple = ((0, 0), (0, 0), (0, 0))
     bc_state: np.ndarray = field(default_factory=lambda: np.zeros((3, 2, 5)))
 
@@ -143,6 +145,13 @@ class Problem:
         p.k_venkat, p.chi_c = self.k_venkat, self.chi_c
         p.sutherland_S = self.sutherland_S
         p.lines = int(self.lines)
+        self._keep = []
+        for a in range(3):
+            if self.nodes is not None and self.nodes[a] is not None:
+                arr = np.ascontiguousarray(self.nodes[a], dtype=np.float64)
+                assert arr.shape == (self.n[a] + 1,)
+                self._keep.append(arr)
+                p.nodes[a] = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         return p
 
 

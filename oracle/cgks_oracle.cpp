@@ -49,6 +49,8 @@ typedef struct {
   double sutherland_S;      // 0: constant mu; > 0: Sutherland law mu(T) = mu (1+S) T^{3/2} / (T+S), T = p/rho
   int    lines;             // CGKS-5th: 1 = line-averaged derivatives of the own cell as reconstruction data (P:166-172,
                             // P:197-203), 0 = the own cell-averaged gradient (R1)
+  const double* nodes[3];   // stretched tensor-product mesh (NEXT-4): node coordinates x_a[0..n_a] per axis, or
+                            // NULL for the uniform spacing (hi - lo) / n
 } orc_params;
 
 }  // extern "C"
@@ -786,6 +788,7 @@ struct CellState {
   double Q[5];
   double G[3][5];     // physical cell-averaged gradient, [axis][var]
   double L[MAXL][5];  // line-averaged derivatives (physical units), used when P.lines
+  double hw[3];       // cell widths (geometry, not state): the reference-cell map x = x_c + hw xi (R37)
 };
 
 
@@ -810,6 +813,16 @@ struct Solver {
     if (P.n[2] > 1) dim = 3;
     for (int a = 0; a < 3; ++a) h[a] = (P.hi[a] - P.lo[a]) / P.n[a];
   }
+  // width of cell index i along a (stretched tensor-product mesh, P:255 / R37); ghost indices take the
+  // width of the periodic image, or of the boundary cell on a bounded axis
+  double width(int a, int i) const {
+    const int n = P.n[a];
+    if (i < 0 || i >= n) {
+      const bool per = P.bc[a][0] == 0 && P.bc[a][1] == 0;
+      i = per ? ((i % n) + n) % n : (i < 0 ? 0 : n - 1);
+    }
+    return P.nodes[a] ? P.nodes[a][i + 1] - P.nodes[a][i] : h[a];
+  }
   long ncell() const { return (long)P.n[0] * P.n[1] * P.n[2]; }
   long lin(int i, int j, int k) const { return ((long)k * P.n[1] + j) * P.n[0] + i; }
 
@@ -828,6 +841,7 @@ struct Solver {
         std::memcpy(c.Q, P.bc_state[a][side], sizeof(c.Q));
         std::memset(c.G, 0, sizeof(c.G));
         std::memset(c.L, 0, sizeof(c.L));
+        for (int b = 0; b < 3; ++b) c.hw[b] = width(b, b == 0 ? i : (b == 1 ? j : k));
         return c;
       } else {  // outflow: zero-order extrapolation of Q and grad Q
         idx[a] = side == 0 ? 0 : n - 1;
@@ -842,6 +856,7 @@ struct Solver {
 // ---------------------------------------------------------------------------
 struct CellRecon {
   double Q0[5];
+  double hw[3];  // the cell's widths (reference-cell map)
   // CGKS-5th: quartic coefficients a[k][v]; GENO data
   std::vector<double> a;   // nb*5
   double chi[5];
@@ -857,6 +872,7 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
   const Recon5& rc = S.rc;
   CellState c0 = S.fetch(F, i, j, k);
   std::memcpy(cr.Q0, c0.Q, sizeof(cr.Q0));
+  std::memcpy(cr.hw, c0.hw, sizeof(cr.hw));
   std::vector<CellState> nb(rc.nc);
   for (int n = 0; n < rc.nc; ++n) nb[n] = S.fetch(F, i + rc.nbrs[n][0], j + rc.nbrs[n][1], k + rc.nbrs[n][2]);
   cr.a.assign(rc.nb * 5, 0.0);
@@ -866,13 +882,13 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
     for (int n = 0; n < rc.nc; ++n) d[n] = nb[n].Q[v] - c0.Q[v];
     for (size_t r = 0; r < rc.ls.size(); ++r) {
       if (rc.ls[r].line >= 0) {  // h_a (d_l Q): reference-unit difference along the line
-        d[rc.nc + r] = S.h[rc.ls[r].axis] * c0.L[rc.ls[r].line][v];
+        d[rc.nc + r] = c0.hw[rc.ls[r].axis] * c0.L[rc.ls[r].line][v];
         continue;
       }
       const CellState& src = rc.ls[r].cell >= 0 ? nb[rc.ls[r].cell] : c0;
       double s = 0.0;
       for (int a = 0; a < 3; ++a)
-        if (rc.ls[r].dir[a] != 0.0) s += rc.ls[r].dir[a] * S.h[a] * src.G[a][v];
+        if (rc.ls[r].dir[a] != 0.0) s += rc.ls[r].dir[a] * src.hw[a] * src.G[a][v];  // the cell's own reference units
       d[rc.nc + r] = s;
     }
     for (int kk = 0; kk < rc.nb; ++kk) {
@@ -902,9 +918,9 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
             const int ng = line_points(S.dim, a, tp);
             double sum = 0.0;
             for (int g = 0; g < ng; ++g) sum += c0.L[a * ng + g][v];
-            cr.bsub[m][a][v] = S.h[a] * sum / ng;
+            cr.bsub[m][a][v] = c0.hw[a] * sum / ng;
           } else {
-            cr.bsub[m][a][v] = S.h[a] * c0.G[a][v];
+            cr.bsub[m][a][v] = c0.hw[a] * c0.G[a][v];
           }
         }
       IS[m] = 0.0;  // R7
@@ -957,7 +973,7 @@ void recon5_eval(const Solver& S, const CellRecon& cr, const BasisAt& ba, double
       p4 += cr.a[k * 5 + v] * ba.v[k];
       for (int a = 0; a < 3; ++a) dp4[a] += cr.a[k * 5 + v] * ba.d[a][k];
     }
-    for (int a = 0; a < 3; ++a) dp4[a] /= S.h[a];
+    for (int a = 0; a < 3; ++a) dp4[a] /= cr.hw[a];
     if (!S.P.nonlinear) {
       W[v] = p4;
       for (int a = 0; a < 3; ++a) dW[a][v] = dp4[a];
@@ -969,7 +985,7 @@ void recon5_eval(const Solver& S, const CellRecon& cr, const BasisAt& ba, double
       double pm = cr.Q0[v];
       for (int a = 0; a < 3; ++a) pm += cr.bsub[m][a][v] * x[a];
       p1 += cr.omega[m][v] * pm;
-      for (int a = 0; a < 3; ++a) dp1[a] += cr.omega[m][v] * cr.bsub[m][a][v] / S.h[a];
+      for (int a = 0; a < 3; ++a) dp1[a] += cr.omega[m][v] * cr.bsub[m][a][v] / cr.hw[a];
     }
     double chi = cr.chi[v];
     W[v] = chi * p4 + (1.0 - chi) * p1;
@@ -980,6 +996,7 @@ void recon5_eval(const Solver& S, const CellRecon& cr, const BasisAt& ba, double
 // GKS-2nd reconstruction: least-squares linear + Venkatakrishnan
 void recon2_cell(const Solver& S, const std::vector<CellState>& F, int i, int j, int k, CellRecon& cr) {
   CellState c0 = S.fetch(F, i, j, k);
+  std::memcpy(cr.hw, c0.hw, sizeof(cr.hw));
   std::memcpy(cr.Q0, c0.Q, sizeof(cr.Q0));
   int nf = 2 * S.dim;
   CellState nb[6];
@@ -1011,7 +1028,7 @@ void recon2_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
       qmin = std::min(qmin, nb[m].Q[v]);
     }
     double hg = 1.0;
-    for (int a = 0; a < S.dim; ++a) hg *= S.h[a];
+    for (int a = 0; a < S.dim; ++a) hg *= c0.hw[a];
     hg = std::pow(hg, 1.0 / S.dim);
     double eps2 = std::pow(S.P.k_venkat * hg, 3);
     double phi0 = 1.0;
@@ -1033,7 +1050,7 @@ void recon2_eval(const Solver& S, const CellRecon& cr, const double x[3], double
   for (int v = 0; v < 5; ++v) {
     W[v] = cr.Q0[v];
     for (int a = 0; a < 3; ++a) W[v] += cr.phi[v] * cr.b[a][v] * x[a];
-    for (int a = 0; a < 3; ++a) dW[a][v] = cr.phi[v] * cr.b[a][v] / S.h[a];
+    for (int a = 0; a < 3; ++a) dW[a][v] = cr.phi[v] * cr.b[a][v] / cr.hw[a];
   }
 }
 
@@ -1233,11 +1250,12 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
       const FaceAvg& fl = faces[ax][((long)lo[2] * fn[1] + lo[1]) * fn[0] + lo[0]];  // face i-1/2
       const FaceAvg& fr = faces[ax][((long)hi[2] * fn[1] + hi[1]) * fn[0] + hi[0]];  // face i+1/2
       for (int v = 0; v < 5; ++v) {
-        out.L[c * 5 + v] += (fl.Fn[v] - fr.Fn[v]) / S.h[ax];
-        out.Lt[c * 5 + v] += (fl.Ft[v] - fr.Ft[v]) / S.h[ax];
+        // box cells: the two a-faces have equal areas, so flux differences divide by the own width
+        out.L[c * 5 + v] += (fl.Fn[v] - fr.Fn[v]) / F[c].hw[ax];
+        out.Lt[c * 5 + v] += (fl.Ft[v] - fr.Ft[v]) / F[c].hw[ax];
         // own side: left state at i+1/2, right state at i-1/2 (R24)
-        out.Gn[c * 15 + ax * 5 + v] = (fr.QLn[v] - fl.QRn[v]) / S.h[ax];
-        out.Gt[c * 15 + ax * 5 + v] = (fr.QLt[v] - fl.QRt[v]) / S.h[ax];
+        out.Gn[c * 15 + ax * 5 + v] = (fr.QLn[v] - fl.QRn[v]) / F[c].hw[ax];
+        out.Gt[c * 15 + ax * 5 + v] = (fr.QLt[v] - fl.QRt[v]) / F[c].hw[ax];
       }
       if (S.P.lines) {
         // line-averaged derivative along ax at transverse Gauss point g: own-side relaxed values at
@@ -1246,8 +1264,8 @@ int run_stage(Solver& S, const std::vector<CellState>& F, double dt, StageOut& o
         const int ng = line_points(S.dim, ax, tp);
         for (int g = 0; g < ng; ++g)
           for (int v = 0; v < 5; ++v) {
-            out.Ln[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLn[g][v] - fl.gRn[g][v]) / S.h[ax];
-            out.Lnt[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLt[g][v] - fl.gRt[g][v]) / S.h[ax];
+            out.Ln[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLn[g][v] - fl.gRn[g][v]) / F[c].hw[ax];
+            out.Lnt[(c * MAXL + ax * ng + g) * 5 + v] = (fr.gLt[g][v] - fl.gRt[g][v]) / F[c].hw[ax];
           }
       }
     }
@@ -1271,9 +1289,10 @@ double compute_dt(const Solver& S, const std::vector<CellState>& F, int* err) {
     }
     double cs = std::sqrt(S.gas.gamma * w.p / w.rho);
     for (int a = 0; a < S.dim; ++a) {
-      double d = S.h[a] / (std::fabs(w.U[a]) + cs);
+      const double hc = F[c].hw[a];
+      double d = hc / (std::fabs(w.U[a]) + cs);
       if (S.P.mu > 0.0)  // nu = mu(T) / rho (R25)
-        d = std::min(d, S.h[a] * S.h[a] / (3.0 * viscosity(S.P.mu, S.P.sutherland_S, w.p / w.rho) / w.rho));
+        d = std::min(d, hc * hc / (3.0 * viscosity(S.P.mu, S.P.sutherland_S, w.p / w.rho) / w.rho));
       dtmin = std::min(dtmin, d);
     }
   }
@@ -1382,6 +1401,8 @@ void load_state(Solver& S, const double* Q, const double* G, const double* Lq = 
     for (int v = 0; v < 5; ++v) S.U[c].Q[v] = Q[v * nc + c];
     for (int a = 0; a < 3; ++a)
       for (int v = 0; v < 5; ++v) S.U[c].G[a][v] = G ? G[(a * 5 + v) * nc + c] : 0.0;
+    const int ci[3] = {(int)(c % S.P.n[0]), (int)((c / S.P.n[0]) % S.P.n[1]), (int)(c / ((long)S.P.n[0] * S.P.n[1]))};
+    for (int a = 0; a < 3; ++a) S.U[c].hw[a] = S.width(a, ci[a]);
     for (int a = 0, l = 0; a < S.dim; ++a) {
       double tp[4][3];
       const int ng = line_points(S.dim, a, tp);
@@ -1582,7 +1603,7 @@ int orc_diagnostics(const orc_params* p, const double* Q, const double* G, doubl
   const double gx[3] = {-0.5 * std::sqrt(0.6), 0.0, 0.5 * std::sqrt(0.6)};  // nodes on [-1/2, 1/2]
   const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};                // weights, sum 1
   const int nq[3] = {S.dim >= 1 ? 3 : 1, S.dim >= 2 ? 3 : 1, S.dim >= 3 ? 3 : 1};
-  const double vol = S.h[0] * S.h[1] * S.h[2];
+
   const long nc = S.ncell();
   std::vector<double> part((size_t)nc * 4, 0.0);
   int bad = 0;
@@ -1598,6 +1619,7 @@ int orc_diagnostics(const orc_params* p, const double* Q, const double* G, doubl
       for (int qy = 0; qy < nq[1]; ++qy)
         for (int qx = 0; qx < nq[0]; ++qx) {
           const double x[3] = {nq[0] == 3 ? gx[qx] : 0.0, nq[1] == 3 ? gx[qy] : 0.0, nq[2] == 3 ? gx[qz] : 0.0};
+          const double vol = S.U[c].hw[0] * S.U[c].hw[1] * S.U[c].hw[2];
           const double w = (nq[0] == 3 ? gw[qx] : 1.0) * (nq[1] == 3 ? gw[qy] : 1.0) * (nq[2] == 3 ? gw[qz] : 1.0) * vol;
           double W[5], dW[3][5];
           if (S.P.scheme == 1)
