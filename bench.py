@@ -220,7 +220,12 @@ def run_ours(args, rank, ws, lr):
         case = make_case(args.workload)
         if args.nonlinear is not None:
             case.nonlinear = args.nonlinear
-        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, lines=args.lines)
+        nodes = None
+        if args.stretch:  # sine-stretched tensor-product mesh (NEXT-4); the state is the workload's own IC
+            from cgks_inputs import stretched_nodes
+            nodes = tuple(stretched_nodes(case.n[a], case.lo[a], case.hi[a], args.stretch) if case.n[a] > 1 else None
+                          for a in range(3))
+        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, lines=args.lines, nodes=nodes)
     NV = 20 if scheme_id == 1 else 5
     Qd = torch.from_numpy(np.ascontiguousarray(case.Q)).cuda()
     Gd = torch.from_numpy(np.ascontiguousarray(case.G)).cuda()
@@ -313,7 +318,7 @@ def run_ours(args, rank, ws, lr):
             "config": {"workload": f"{case.name} {case.n[0]}x{case.n[1]}x{case.n[2]}"
                                    + (f" ({case.n[0]}^3 per GPU)" if ws > 1 else ""),
                        "scheme": args.scheme + ("-geno" if case.nonlinear else "-linear")
-                       + ("-lines" if args.lines else ""),
+                       + ("-lines" if args.lines else "") + (f"-stretched{args.stretch:g}" if args.stretch else ""),
                        "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
                        "parallelism": f"zslab{ws} (NCCL halo + allreduce-min)" if ws > 1 else "1gpu",
                        "l2": "state larger than L2 (no flush)"},
@@ -341,6 +346,8 @@ def main():
     ap.add_argument("--scheme", default="cgks5", choices=["cgks5", "gks2"])
     ap.add_argument("--nonlinear", type=int, default=None)
     ap.add_argument("--lines", type=int, default=0, help="CGKS-5th with line-averaged derivative DOFs (NEXT-1)")
+    ap.add_argument("--stretch", type=float, default=0.0,
+                    help="sine-stretched tensor-product mesh with this amplitude (NEXT-4; timing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, ws, lr = dist_init()

@@ -63,6 +63,9 @@ typedef struct {
   int rank;                  /* this process' rank in [0, nproc product)                           */
   const void* nccl_id;       /* 128-byte ncclUniqueId, or NULL when there is one rank              */
   void* stream;              /* cudaStream_t to run on, or NULL for a library-owned stream         */
+  const double* nodes[3];    /* stretched tensor-product mesh (DESIGN R37):
+                                per axis the n[a]+1 increasing node coordinates (host pointer, copied
+                                at create; global mesh), or NULL for the uniform spacing from lo/hi   */
 } cgks_grid;
 
 typedef struct {

@@ -30,6 +30,7 @@ class cgks_grid(ctypes.Structure):
         ("rank", ctypes.c_int),
         ("nccl_id", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
+        ("nodes", ctypes.POINTER(ctypes.c_double) * 3),
     ]
 
 
@@ -168,7 +169,7 @@ class Solver:
     def __init__(self, n, lo, hi, gamma=1.4, mu=0.0, Pr=1.0, scheme=CGKS_CGKS5, nonlinear=0,
                  time_scheme=CGKS_TIME_DEFAULT, cfl=None, fixed_dt=0.0, tau_eps=0.05, tau_C=10.0, relax_C=10.0,
                  k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, lines=0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
-                 stream=None,
+                 stream=None, nodes=None,
                  nproc=(1, 1, 1), rank=0, nccl_id=None):
         L = load()
         g = cgks_grid()
@@ -183,6 +184,15 @@ class Solver:
                     for v in range(5):
                         g.bc_state[a][s][v] = float(np.asarray(bc_state)[a, s, v])
         g.rank = int(rank)
+        self._nodes = []
+        if nodes is not None:
+            for a in range(3):
+                if nodes[a] is not None:
+                    arr = np.ascontiguousarray(nodes[a], dtype=np.float64)
+                    if arr.shape != (int(n[a]) + 1,):
+                        raise ValueError(f"nodes[{a}] must hold n[{a}]+1 coordinates")
+                    self._nodes.append(arr)
+                    g.nodes[a] = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         self._nccl_id = nccl_id
         self._nccl_buf = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
         g.nccl_id = None if nccl_id is None else ctypes.cast(self._nccl_buf, ctypes.c_void_p)

@@ -110,6 +110,8 @@ struct cgks_ctx {
   bool use_tma = false;
   double* dpart = nullptr;  // diagnostics block partials
   double* ctab = nullptr;   // basis values at the centroid p_k(0) (Q-criterion, CGKS-5th)
+  double* hwd[3] = {nullptr, nullptr, nullptr};   // stretched mesh: cell widths (cells -2 .. n+1)
+  double* ihwd[3] = {nullptr, nullptr, nullptr};  // and their inverses
   long long dpart_n = 0;
   double* staging = nullptr;
   TimeState* ts = nullptr;
@@ -198,6 +200,7 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
   a.box = ctx->box;
+  a.stretched = ctx->geo.stretched;
   if (ctx->lines) {
     auto lbuf = [&](const double* X) -> double* {
       return X == ctx->U[0] ? ctx->Lb[0] : (X == ctx->U[1] ? ctx->Lb[1] : (X == ctx->Us ? ctx->Ls : nullptr));
@@ -639,6 +642,46 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       return fail(CGKS_ERR_CUDA);
     }
   }
+  // ---- stretched tensor-product mesh (NEXT-4, R37): per-axis widths of the local cells -2 .. n+1
+  {
+    bool any = false;
+    for (int a = 0; a < dim; ++a) any = any || grid->nodes[a] != nullptr;
+    if (any) {
+      if (ctx->lines) {
+        set_msg(ctx, "line DOFs are not combined with stretched meshes in this version");
+        return fail(CGKS_ERR_CONFIG);
+      }
+      g.stretched = 1;
+      for (int a = 0; a < 3; ++a) {
+        const long long N = grid->n[a];
+        const double* xn = a < dim ? grid->nodes[a] : nullptr;
+        if (xn)
+          for (long long q = 0; q < N; ++q)
+            if (!(xn[q + 1] > xn[q])) {
+              set_msg(ctx, "nodes[%d] must be strictly increasing", a);
+              return fail(CGKS_ERR_CONFIG);
+            }
+        const bool per = grid->bc[a][0] == CGKS_BC_PERIODIC && grid->bc[a][1] == CGKS_BC_PERIODIC;
+        const long long off = a == 2 ? ctx->zoff_global : 0;
+        std::vector<double> w((size_t)g.n[a] + 4), iw((size_t)g.n[a] + 4);
+        for (int c = -2; c < g.n[a] + 2; ++c) {
+          long long gi = c + off;
+          if (gi < 0 || gi >= N) gi = per ? ((gi % N) + N) % N : (gi < 0 ? 0 : N - 1);
+          const double wv = xn ? xn[gi + 1] - xn[gi] : (grid->hi[a] - grid->lo[a]) / (double)N;
+          w[c + 2] = wv;
+          iw[c + 2] = 1.0 / wv;
+        }
+        if (!alloc(&ctx->hwd[a], (long long)w.size()) || !alloc(&ctx->ihwd[a], (long long)w.size()) ||
+            cudaMemcpy(ctx->hwd[a], w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(ctx->ihwd[a], iw.data(), sizeof(double) * iw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+          set_msg(ctx, "width table upload failed");
+          return fail(CGKS_ERR_CUDA);
+        }
+        g.hw[a] = ctx->hwd[a];
+        g.ihw[a] = ctx->ihwd[a];
+      }
+    }
+  }
   cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
   // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
   // group stepped by cgks_step_group (halo copies on one device)
@@ -999,8 +1042,8 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->lines) {
-    set_msg(ctx, "cgks_diagnostics: not available with line DOFs in this version");
+  if (ctx->lines || ctx->geo.stretched) {
+    set_msg(ctx, "cgks_diagnostics: not available with line DOFs or stretched meshes in this version");
     return CGKS_ERR_CONFIG;
   }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
@@ -1043,8 +1086,8 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->lines) {
-    set_msg(ctx, "cgks_qcriterion: not available with line DOFs in this version");
+  if (ctx->lines || ctx->geo.stretched) {
+    set_msg(ctx, "cgks_qcriterion: not available with line DOFs or stretched meshes in this version");
     return CGKS_ERR_CONFIG;
   }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
@@ -1260,7 +1303,8 @@ void cgks_destroy(cgks_ctx* ctx) {
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
                     ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart,
-                    ctx->ctab, ctx->Lb[0], ctx->Lb[1], ctx->Ls, ctx->Lc};
+                    ctx->ctab, ctx->Lb[0], ctx->Lb[1], ctx->Ls, ctx->Lc,
+                    ctx->hwd[0], ctx->hwd[1], ctx->hwd[2], ctx->ihwd[0], ctx->ihwd[1], ctx->ihwd[2]};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);

@@ -43,6 +43,7 @@ struct StageArgs {
   double* Lout = nullptr;
   double* Lcarry = nullptr;
   int lines = 0;
+  int stretched = 0;  // stretched tensor-product mesh (NEXT-4)
   // TMA descriptors of the flux tiles per normal axis (reconstruction fields; cell averages of Uin)
   const CUtensorMap* tm_rec = nullptr;
   const CUtensorMap* tm_U = nullptr;

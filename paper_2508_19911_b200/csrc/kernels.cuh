@@ -120,6 +120,10 @@ __device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
   return ((long long)kk * NF + f) * c_geo.eplane + (long long)jj * c_geo.en[0] + ii;
 }
 
+// stretched meshes (R37): width / inverse width of cell index c along a (c in -2 .. n+1)
+__device__ __forceinline__ double cw(int a, int c) { return __ldg(c_geo.hw[a] + c + 2); }
+__device__ __forceinline__ double icw(int a, int c) { return __ldg(c_geo.ihw[a] + c + 2); }
+
 // 8-byte asynchronous global -> shared copy (cp.async.ca, LDGSTS) and the matching wait
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -194,10 +198,11 @@ struct ReconTile {
   static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO + sizeof(unsigned) * NFS * HALO; }
 };
 
-template <int DIM>
+template <int DIM, bool STR = false>
 struct Recon5TileLoader {
   const double* __restrict__ s;  // staged fields of this component, at this thread's cell
   double q0, h0, h1, h2;
+  double w[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // STR: widths of the cells at offsets -1, 0, +1 per axis
   const double* __restrict__ lv = nullptr;  // line DOFs: line 0 of this component at this cell (field stride plane)
   long long lstride = 0;                    // 5 * plane: next line
   static constexpr int HALO = ReconTile<DIM>::HALO;
@@ -207,6 +212,8 @@ struct Recon5TileLoader {
   }
   __device__ __forceinline__ double q(int ox, int oy, int oz) const { return at(0, ox, oy, oz) - q0; }
   __device__ __forceinline__ double g(int a, int ox, int oy, int oz) const {
+    if (STR)  // each cell in its own reference units (R37)
+      return w[a][(a == 0 ? ox : (a == 1 ? oy : oz)) + 1] * at(1 + a, ox, oy, oz);
     return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * at(1 + a, ox, oy, oz);
   }
   // own-cell line-averaged derivative l in reference units (h_a (d_l Q)_l, a = l / lines per axis)
@@ -258,7 +265,7 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int DIM, bool NONLIN, bool BOX, bool LINES = false>
+template <int DIM, bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
 __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double* __restrict__ U,
                                                                     double* __restrict__ coef,
                                                                     const ErrState* __restrict__ err,
@@ -296,8 +303,15 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    Recon5TileLoader<DIM> L{cur + own, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
+    Recon5TileLoader<DIM, STR> L{cur + own, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
     L.q0 = L.at(0, 0, 0, 0);
+    if (STR) {
+      const int ci[3] = {i, j, k};
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int o = -1; o <= 1; ++o) L.w[a][o + 1] = cw(a, min(max(ci[a] + o, -2), c_geo.n[a] + 1));
+    }
     if (LINES) {  // own-cell lines, [z][l*5+v][y][x] (valid cells only; ragged threads read cell 0)
       constexpr int NLF = 5 * (DIM == 3 ? 12 : (DIM == 2 ? 4 : 1));
       L.lv = Lin + (valid ? sidx(NLF, v, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, k)) : 0);
@@ -412,7 +426,13 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
     }
     double phi = 1.0;
     if (NONLIN) {  // Venkatakrishnan (R11)
-      const double e2 = c_geo.eps_venkat2;
+      double e2 = c_geo.eps_venkat2;
+      if (c_geo.stretched) {  // (K h_g)^3 with the cell's own geometric-mean width (R37)
+        double hp = 1.0;
+        for (int a = 0; a < DIM; ++a) hp *= cw(a, a == 0 ? i : (a == 1 ? j : k));
+        const double kv = c_geo.k_venkat;
+        e2 = kv * kv * kv * (DIM == 3 ? hp : (DIM == 2 ? hp * sqrt(hp) : hp * hp * hp));
+      }
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
 #pragma unroll
@@ -484,7 +504,7 @@ struct FluxTile {
   static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128) + 16; }
 };
 
-template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false>
+template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR = false>
 __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
                                                const double* __restrict__ gtab, double* __restrict__ face,
                                                const TimeState* __restrict__ ts, ErrState* __restrict__ err,
@@ -593,6 +613,13 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
 
   // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)
   constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
+  // inverse widths of this lane's cell (the left cell of the face for side 0): uniform or per cell (R37)
+  double ihc[3] = {0.0, 0.0, 0.0};
+  if (STR) {
+    const int cc[3] = {AX == 0 ? i - 1 + side : i, AX == 1 ? j - 1 + side : j, AX == 2 ? k - 1 + side : k};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) ihc[a] = icw(a, min(cc[a], c_geo.n[a] + 1));
+  }
   double wn[5], dn[3][5];
   if (COMPACT) {
     // Evaluation of the side's quartic at the face Gauss points in the face-plane
@@ -649,9 +676,9 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
       g[0][v] = g[1][v] = g[2][v] = 0.0;
-      g[AX][v] = dW[1][v] * c_geo.ih[AX];
-      if (DIM > 1) g[TA][v] = dW[2 % NQ][v] * c_geo.ih[TA];
-      if (DIM > 2) g[TB][v] = dW[3 % NQ][v] * c_geo.ih[TB];
+      g[AX][v] = dW[1][v] * (STR ? ihc[AX] : c_geo.ih[AX]);
+      if (DIM > 1) g[TA][v] = dW[2 % NQ][v] * (STR ? ihc[TA] : c_geo.ih[TA]);
+      if (DIM > 2) g[TB][v] = dW[3 % NQ][v] * (STR ? ihc[TB] : c_geo.ih[TB]);
     }
     wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
     const int pp[3] = {P0, P1, P2};
@@ -671,7 +698,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
       const double q = sc[v * FT::FS];
       W[v] = q + hs * tc[(AX * 5 + v) * FT::FS];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * FT::FS] * c_geo.ih[a];
+      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * FT::FS] * (STR ? ihc[a] : c_geo.ih[a]);
     }
     wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
     const int pp[3] = {P0, P1, P2};
@@ -801,7 +828,8 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
     const int wk = c_geo.bounded[2] ? hi_k : wrapi(hi_k, c_geo.n[2]);
     const long long lo = (long long)k * NF * fpl + (long long)j * fn0 + i;
     const long long hi = (long long)wk * NF * fpl + (long long)wj * fn0 + wi;
-    const double ih = c_geo.ih[a];
+    // own width (box cells: equal face areas on both sides, R37)
+    const double ih = c_geo.stretched ? icw(a, a == 0 ? i : (a == 1 ? j : k)) : c_geo.ih[a];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
       L[v] += (__ldg(F[a] + lo + v * fpl) - __ldg(F[a] + hi + v * fpl)) * ih;
@@ -937,8 +965,9 @@ __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV
       }
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
-        double d = c_geo.h[a] / (fabs(u[a]) + c);
-        if (c_geo.mu > 0.0) d = fmin(d, c_geo.h[a] * c_geo.h[a] / (3.0 * mu_T * ir));  // nu = mu(T) / rho (R25)
+        const double ha = c_geo.stretched ? cw(a, a == 0 ? i : (a == 1 ? j : k)) : c_geo.h[a];
+        double d = ha / (fabs(u[a]) + c);
+        if (c_geo.mu > 0.0) d = fmin(d, ha * ha / (3.0 * mu_T * ir));  // nu = mu(T) / rho (R25)
         cand = fmin(cand, d);
       }
       if (!(cand == cand)) flag_error(err, 4, 3, 0, ts->steps, i, j, k);

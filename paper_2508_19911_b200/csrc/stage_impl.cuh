@@ -44,10 +44,10 @@ int launch(LaunchEnv& env, const char* name, void (*kern)(KArgs...), long long n
 constexpr int D = CGKS_DIM;
 
 // reconstruction: one block per TX x TY x TZ cells of the extended range, shared-memory halo tile
-template <bool NONLIN, bool BOX, bool LINES = false>
+template <bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
 int recon5_launch(LaunchEnv& env, const StageArgs& a) {
   using RT = ReconTile<D>;
-  auto kern = k_recon5<D, NONLIN, BOX, LINES>;
+  auto kern = k_recon5<D, NONLIN, BOX, LINES, STR>;
   static bool attr = false;
   const size_t smem = RT::smem_bytes();
   if (!attr) {
@@ -76,10 +76,10 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 }
 
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
-template <bool COMPACT, bool BOX, int AX, bool LINES = false>
+template <bool COMPACT, bool BOX, int AX, bool LINES = false, bool STR = false>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
   using FT = FluxTile<D, AX, COMPACT>;
-  auto kern = k_flux<D, AX, COMPACT, BOX, LINES>;
+  auto kern = k_flux<D, AX, COMPACT, BOX, LINES, STR>;
   static bool attr = false;
   const size_t smem = FT::smem_bytes();
   if (!attr) {
@@ -112,18 +112,18 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
   return 0;
 }
 
-template <bool COMPACT, bool NONLIN, bool BOX, bool LINES = false>
+template <bool COMPACT, bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
 int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   if (COMPACT) {
-    int rc = recon5_launch<NONLIN, BOX, LINES>(env, a);
+    int rc = recon5_launch<NONLIN, BOX, LINES, STR>(env, a);
     if (rc) return rc;
   } else {
     LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
   {
-    int rc = flux_launch<COMPACT, BOX, 0, LINES>(env, "flux_x", a, stage);
-    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0), LINES>(env, "flux_y", a, stage);
-    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES>(env, "flux_z", a, stage);
+    int rc = flux_launch<COMPACT, BOX, 0, LINES, STR>(env, "flux_x", a, stage);
+    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0), LINES, STR>(env, "flux_y", a, stage);
+    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES, STR>(env, "flux_z", a, stage);
     if (rc) return rc;
   }
   if (mode == 0)
@@ -140,6 +140,16 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
 
 int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
+  if (a.stretched) {  // stretched tensor-product mesh (NEXT-4)
+    if (c && !nl && !b) return stage_t<true, false, false, false, true>(env, a, mode, stage);
+    if (c && nl && !b) return stage_t<true, true, false, false, true>(env, a, mode, stage);
+    if (c && !nl && b) return stage_t<true, false, true, false, true>(env, a, mode, stage);
+    if (c && nl && b) return stage_t<true, true, true, false, true>(env, a, mode, stage);
+    if (!c && !nl && !b) return stage_t<false, false, false, false, true>(env, a, mode, stage);
+    if (!c && nl && !b) return stage_t<false, true, false, false, true>(env, a, mode, stage);
+    if (!c && !nl && b) return stage_t<false, false, true, false, true>(env, a, mode, stage);
+    return stage_t<false, true, true, false, true>(env, a, mode, stage);
+  }
   if (c && a.lines) {  // CGKS-5th with line DOFs (NEXT-1)
     if (!nl && !b) return stage_t<true, false, false, true>(env, a, mode, stage);
     if (nl && !b) return stage_t<true, true, false, true>(env, a, mode, stage);

@@ -29,6 +29,11 @@ struct Geo {
   int lines;    // CGKS-5th line-DOF variant
   int ngl;      // lines per axis (transverse face Gauss points: 4 / 2 / 1)
   int nfr;      // fields of a face record (30, plus 2 x ngl x 10 per-Gauss-point values with lines)
+  // stretched tensor-product mesh (NEXT-4, R37): per-axis cell widths and their inverses, indexed
+  // cell + 2 for cells -2 .. n+1 (ghost widths: periodic image or boundary cell)
+  int stretched;
+  const double* hw[3];
+  const double* ihw[3];
 };
 
 struct ErrState {
