@@ -92,6 +92,10 @@ def lib():
         L.orc_diagnostics.restype = ctypes.c_int
         L.orc_qcriterion.argtypes = [pp, dp, dp, dp]
         L.orc_qcriterion.restype = ctypes.c_int
+        L.orc_diagnostics_l.argtypes = [pp, dp, dp, dp, dp]
+        L.orc_diagnostics_l.restype = ctypes.c_int
+        L.orc_qcriterion_l.argtypes = [pp, dp, dp, dp, dp]
+        L.orc_qcriterion_l.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -280,26 +284,34 @@ def recon_eval(prob: Problem, Q, G, ijk, x):
     return out[:, :5], out[:, 5:].reshape(-1, 3, 5), chi
 
 
-def diagnostics(prob: Problem, Q, G=None):
+def diagnostics(prob: Problem, Q, G=None, L=None):
     """Quadrature of the reconstructed state (orc_diagnostics): returns
-    (int 1/2 rho|U|^2 dV, int mu|curl U|^2 dV, int 4/3 mu (div U)^2 dV, int rho dV)."""
+    (int 1/2 rho|U|^2 dV, int mu|curl U|^2 dV, int 4/3 mu (div U)^2 dV, int rho dV).  L: line DOFs."""
     Q = np.ascontiguousarray(Q, dtype=np.float64)
     G = np.zeros((3,) + Q.shape) if G is None else np.ascontiguousarray(G, dtype=np.float64)
     out = np.zeros(4)
     p = prob.to_c()
-    rc = lib().orc_diagnostics(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
+    if L is not None:
+        L = np.ascontiguousarray(L, dtype=np.float64)
+        rc = lib().orc_diagnostics_l(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(L), _ptr(out))
+    else:
+        rc = lib().orc_diagnostics(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
     if rc:
         raise ValueError(f"oracle diagnostics failed rc={rc}")
     return out
 
 
-def qcriterion(prob: Problem, Q, G=None):
+def qcriterion(prob: Problem, Q, G=None, L=None):
     """Q-criterion at every cell centroid from the cell's reconstruction (orc_qcriterion): [nz][ny][nx]."""
     Q = np.ascontiguousarray(Q, dtype=np.float64)
     G = np.zeros((3,) + Q.shape) if G is None else np.ascontiguousarray(G, dtype=np.float64)
     out = np.zeros(Q.shape[1:])
     p = prob.to_c()
-    rc = lib().orc_qcriterion(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
+    if L is not None:
+        L = np.ascontiguousarray(L, dtype=np.float64)
+        rc = lib().orc_qcriterion_l(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(L), _ptr(out))
+    else:
+        rc = lib().orc_qcriterion(ctypes.byref(p), _ptr(Q), _ptr(G), _ptr(out))
     if rc:
         raise ValueError(f"oracle qcriterion failed rc={rc}")
     return out

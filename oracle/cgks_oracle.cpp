@@ -1596,10 +1596,10 @@ int orc_recon_eval(const orc_params* p, const double* Q, const double* G, int i,
 // quartic, blended with the GENO linears when nonlinear; GKS-2nd limited linear) is evaluated at the
 // 3-point Gauss-Legendre nodes of every active axis (reading R35), weights times the cell volume.
 // U = (rho U)/rho, dU = (d(rho U) - U d rho)/rho, T = p/rho, mu(T) by viscosity() (R19 / P:469-473).
-int orc_diagnostics(const orc_params* p, const double* Q, const double* G, double* out) {
+int orc_diagnostics_l(const orc_params* p, const double* Q, const double* G, const double* Lq, double* out) {
   Solver S(*p);
   if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
-  load_state(S, Q, G);
+  load_state(S, Q, G, Lq);
   const double gx[3] = {-0.5 * std::sqrt(0.6), 0.0, 0.5 * std::sqrt(0.6)};  // nodes on [-1/2, 1/2]
   const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};                // weights, sum 1
   const int nq[3] = {S.dim >= 1 ? 3 : 1, S.dim >= 2 ? 3 : 1, S.dim >= 3 ? 3 : 1};
@@ -1656,10 +1656,10 @@ int orc_diagnostics(const orc_params* p, const double* Q, const double* G, doubl
 // Q-criterion at every cell centroid (the iso-surfaces of TGV-sup-1):
 // Q = (|Omega|^2 - |S|^2) / 2 = -1/2 sum_ab dU_b/dx_a dU_a/dx_b with the velocity gradient from the
 // cell's own reconstruction evaluated at its centroid (reading R35).  out: [ncell], x fastest.
-int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double* out) {
+int orc_qcriterion_l(const orc_params* p, const double* Q, const double* G, const double* Lq, double* out) {
   Solver S(*p);
   if (p->scheme == 1 && !build_recon5(S.dim, S.rc, p->lines)) return 2;
-  load_state(S, Q, G);
+  load_state(S, Q, G, Lq);
   const long nc = S.ncell();
   int bad = 0;
 #pragma omp parallel for schedule(static) reduction(max : bad)
@@ -1690,6 +1690,13 @@ int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double
     out[c] = q;
   }
   return bad ? 3 : 0;
+}
+
+int orc_diagnostics(const orc_params* p, const double* Q, const double* G, double* out) {
+  return orc_diagnostics_l(p, Q, G, nullptr, out);
+}
+int orc_qcriterion(const orc_params* p, const double* Q, const double* G, double* out) {
+  return orc_qcriterion_l(p, Q, G, nullptr, out);
 }
 
 // One stage's residual L, dL/dt and Gauss-theorem gradients for a given dt (for unit tests).

@@ -1042,10 +1042,6 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->lines || ctx->geo.stretched) {
-    set_msg(ctx, "cgks_diagnostics: not available with line DOFs or stretched meshes in this version");
-    return CGKS_ERR_CONFIG;
-  }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
     set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
@@ -1086,10 +1082,6 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->lines || ctx->geo.stretched) {
-    set_msg(ctx, "cgks_qcriterion: not available with line DOFs or stretched meshes in this version");
-    return CGKS_ERR_CONFIG;
-  }
   if (ctx->nranks > 1 || ctx->comm_mode == 2) {
     set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;

@@ -1063,7 +1063,16 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
     const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
     const int pi = p % 3, pj = (p / 3) % 3, pk = p / 9;
     const double xi[3] = {gx[pi], DIM >= 2 ? gx[pj] : 0.0, DIM >= 3 ? gx[pk] : 0.0};
-    const double w = gw[pi] * (DIM >= 2 ? gw[pj] : 1.0) * (DIM >= 3 ? gw[pk] : 1.0) * c_geo.h[0] * c_geo.h[1] * c_geo.h[2];
+    // cell widths (stretched meshes: the cell's own, R37)
+    double hc[3] = {c_geo.h[0], c_geo.h[1], c_geo.h[2]}, ihc[3] = {c_geo.ih[0], c_geo.ih[1], c_geo.ih[2]};
+    if (c_geo.stretched) {
+      const int ci[3] = {i, j, k};
+      for (int a = 0; a < DIM; ++a) {
+        hc[a] = cw(a, ci[a]);
+        ihc[a] = icw(a, ci[a]);
+      }
+    }
+    const double w = gw[pi] * (DIM >= 2 ? gw[pj] : 1.0) * (DIM >= 3 ? gw[pk] : 1.0) * hc[0] * hc[1] * hc[2];
     double W[5], dW[3][5];
     if (COMPACT) {
       const double* cb = rec + eidx(NB * 5, 0, i, j, k);
@@ -1080,9 +1089,9 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
           d2 = fma(c, wv[3 * NB + kk], d2);
         }
         W[v] = val;
-        dW[0][v] = d0 * c_geo.ih[0];
-        dW[1][v] = d1 * c_geo.ih[1];
-        dW[2][v] = d2 * c_geo.ih[2];
+        dW[0][v] = d0 * ihc[0];
+        dW[1][v] = d1 * ihc[1];
+        dW[2][v] = d2 * ihc[2];
       }
     } else {
 #pragma unroll
@@ -1092,7 +1101,7 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
         for (int a = 0; a < 3; ++a) {
           const double sl = __ldg(rec + eidx(15, a * 5 + v, i, j, k));  // limited slope, reference units
           W[v] = fma(sl, xi[a], W[v]);
-          dW[a][v] = sl * c_geo.ih[a];
+          dW[a][v] = sl * ihc[a];
         }
       }
     }
@@ -1151,6 +1160,11 @@ __global__ void __launch_bounds__(256) k_qcrit(const double* __restrict__ U, con
   const int i = (int)(t % c_geo.n[0]);
   const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
   const int k = (int)(t / c_geo.plane);
+  double ihc[3] = {c_geo.ih[0], c_geo.ih[1], c_geo.ih[2]};
+  if (c_geo.stretched) {
+    const int ci[3] = {i, j, k};
+    for (int a = 0; a < DIM; ++a) ihc[a] = icw(a, ci[a]);
+  }
   double W[5], dW[3][5];
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
@@ -1162,11 +1176,11 @@ __global__ void __launch_bounds__(256) k_qcrit(const double* __restrict__ U, con
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
         static_assert(ReconGen<DIM>::expo(0, 0) == 1, "linear basis functions first");
-        dW[a][v] = __ldg(rec + eidx(NB * 5, a * 5 + v, i, j, k)) * c_geo.ih[a];
+        dW[a][v] = __ldg(rec + eidx(NB * 5, a * 5 + v, i, j, k)) * ihc[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) dW[a][v] = __ldg(rec + eidx(15, a * 5 + v, i, j, k)) * c_geo.ih[a];
+      for (int a = 0; a < DIM; ++a) dW[a][v] = __ldg(rec + eidx(15, a * 5 + v, i, j, k)) * ihc[a];
     }
   }
   const double ir = 1.0 / W[0];

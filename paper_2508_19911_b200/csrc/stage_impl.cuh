@@ -168,13 +168,23 @@ int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
 
 // diagnostics: reconstruction of the state a.Uin, then quadrature per (cell, node); returns the number of
 // block partials written to part (4 doubles each)
+// the reconstruction of a.Uin in the context's variant (line DOFs, stretched mesh), for the diagnostics
+template <bool COMPACT, bool NONLIN, bool BOX>
+int recon_any(LaunchEnv& env, const StageArgs& a) {
+  if (COMPACT) {
+    if (a.lines) return recon5_launch<NONLIN, BOX, true, false>(env, a);
+    if (a.stretched) return recon5_launch<NONLIN, BOX, false, true>(env, a);
+    return recon5_launch<NONLIN, BOX>(env, a);
+  }
+  LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  return 0;
+}
+
 template <bool COMPACT, bool NONLIN, bool BOX>
 int diag_t(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk) {
-  if (COMPACT) {
-    int rc = recon5_launch<NONLIN, BOX>(env, a);
+  {
+    int rc = recon_any<COMPACT, NONLIN, BOX>(env, a);
     if (rc) return rc;
-  } else {
-    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
   constexpr int NP = DiagQuad<D>::NP;
   *nblk = (a.ncell * NP + 255) / 256;
@@ -185,11 +195,9 @@ int diag_t(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part,
 // Q-criterion of a.Uin at the cell centroids into out[ncell] (reconstruction first)
 template <bool COMPACT, bool NONLIN, bool BOX>
 int qcrit_t(LaunchEnv& env, const StageArgs& a, const double* wc, double* out) {
-  if (COMPACT) {
-    int rc = recon5_launch<NONLIN, BOX>(env, a);
+  {
+    int rc = recon_any<COMPACT, NONLIN, BOX>(env, a);
     if (rc) return rc;
-  } else {
-    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
   }
   LAUNCH("qcrit", (k_qcrit<D, COMPACT>), a.ncell, 256, (const double*)a.Uin, (const double*)a.rec, wc, out);
   return 0;

@@ -92,3 +92,22 @@ def test_lines_default_from_gradients():
     S.close()
     k, v = worst(rel_linf(Qg, Qo, Gg, Go, L=2 * math.pi))
     assert v <= 1e-10, (k, v)
+
+
+def test_lines_diagnostics_and_qcriterion():
+    from paper_2508_19911_b200 import Solver
+    n, lo, hi, Q, G, L = _smooth3d()
+    kw = dict(gamma=1.4, mu=2e-3, Pr=0.72)
+    prob = oracle.Problem(n=n, lo=lo, hi=hi, scheme=1, time_scheme=2, lines=1, cfl=0.3, **kw)
+    S = Solver(n, lo, hi, scheme=1, lines=1, cfl=0.3, **kw)
+    S.set_state(Q, G)
+    S.set_lines(L)
+    S.step(3)
+    Qg, Gg = S.get_state()
+    Lg = S.get_lines()
+    dg, qg = S.diagnostics(), S.qcriterion()
+    S.close()
+    do = oracle.diagnostics(prob, Qg, Gg, Lg)
+    qo = oracle.qcriterion(prob, Qg, Gg, Lg)
+    assert np.all(np.abs(dg - do) <= 1e-12 * np.abs(do) + 1e-300), (dg, do)
+    assert np.abs(qg - qo).max() <= 1e-11 * np.abs(qo).max()

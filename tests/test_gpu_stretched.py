@@ -76,3 +76,19 @@ def test_uniform_nodes_bitwise_gpu():
         out.append(S.get_state())
         S.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_stretched_diagnostics_and_qcriterion():
+    n = 32
+    nodes = (stretched_nodes(n, 0.0, 10.0, 0.3), stretched_nodes(n, 0.0, 10.0, 0.2), np.array([0.0, 1.0]))
+    Q, G = gl_average(_vortex_prim(0.0), (n, n, 1), (0, 0, 0), (10, 10, 1), 1.4, nq=5, mesh_nodes=nodes)
+    for scheme in (1, 0):
+        p = oracle.Problem(n=(n, n, 1), lo=(0, 0, 0), hi=(10, 10, 1), scheme=scheme, mu=1e-3, nodes=nodes)
+        S = _solver(n=(n, n, 1), lo=(0, 0, 0), hi=(10, 10, 1), scheme=scheme, mu=1e-3, nodes=nodes)
+        S.set_state(Q, G if scheme == 1 else None)
+        dg, qg = S.diagnostics(), S.qcriterion()
+        S.close()
+        do = oracle.diagnostics(p, Q, G if scheme == 1 else None)
+        qo = oracle.qcriterion(p, Q, G if scheme == 1 else None)
+        assert np.all(np.abs(dg - do) <= 1e-12 * np.abs(do) + 1e-300), (scheme, dg, do)
+        assert np.abs(qg - qo).max() <= 1e-11 * np.abs(qo).max()
