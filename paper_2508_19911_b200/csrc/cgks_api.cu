@@ -590,7 +590,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     for (int a = 0; a < dim; ++a) {
       const int tA = dim == 3 ? (a + 1) % 3 : (dim == 2 ? 1 - a : -1);
       const int tB = dim == 3 ? (a + 2) % 3 : -1;
-      const int ts = nb + 1;  // padded row (FluxTile::TS): bank-conflict-free per-quantity rows
+      const int ts = ((nb / 2) % 2 == 1) ? nb : nb + 2;  // row (FluxTile::TS): aligned, conflict-free pairs
       std::vector<double> tab((size_t)2 * nq * ts, 0.0);
       for (int side = 0; side < 2; ++side) {
         const double dn = side == 0 ? 0.5 : -0.5;

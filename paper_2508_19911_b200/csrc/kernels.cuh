@@ -489,7 +489,9 @@ struct FluxTile {
   static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
   static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
   static constexpr int NQ = DIM + 1;                         // value + DIM derivatives
-  static constexpr int TS = NB + 1;                          // padded per-(side, quantity) row (no bank conflicts)
+  // per-(side, quantity) table row: even with TS / 2 odd, so 128-bit loads of entry pairs are aligned
+  // and conflict-free across the 8 rows a warp reads
+  static constexpr int TS = ((NB / 2) % 2 == 1) ? NB : NB + 2;
   static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
   // Tile layout = the TMA box layout of the [z][field][y][x] arrays: reconstruction fields, then the
   // cell averages.  x- and y-faces: [field][cell] (field stride NT); z-faces: [cz][field][cx]
@@ -640,12 +642,17 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
 #pragma unroll
         for (int cc = 0; cc < NG; ++cc) S[v][cc] = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < NB; ++kk) {
-        const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
-                                 : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
-        const double t = T[kk];
+      for (int k2 = 0; k2 < NB; k2 += 2) {
+        const double2 tt = *reinterpret_cast<const double2*>(T + k2);  // table entries k2, k2 + 1
 #pragma unroll
-        for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * FT::FS], t, S[v][cls]);
+        for (int h = 0; h < 2; ++h) {
+          const int kk = k2 + h;
+          const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
+                                   : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
+          const double t = h ? tt.y : tt.x;
+#pragma unroll
+          for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * FT::FS], t, S[v][cls]);
+        }
       }
       const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);  // derivative along tA / tB flips that parity
 #pragma unroll
