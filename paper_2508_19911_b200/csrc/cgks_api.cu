@@ -538,10 +538,10 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
     return fail(CGKS_ERR_CUDA);
   }
-  // TMA descriptors (3-D CGKS-5th, periodic or z-decomposed, even x extent so that rows are
+  // TMA descriptors (3-D, both schemes, periodic or z-decomposed, even x extent so that rows are
   // multiples of 16 bytes): 4-D views [z][field][y][x] of the reconstruction fields and of each
   // state buffer, boxes = the flux tiles of each normal axis; CGKS_NO_TMA=1 disables
-  if (ctx->scheme_id == CGKS_CGKS5 && dim == 3 && !ctx->box && g.en[0] % 2 == 0 && g.n[0] % 2 == 0 &&
+  if (dim == 3 && !ctx->box && g.en[0] % 2 == 0 && g.n[0] % 2 == 0 &&
       std::getenv("CGKS_NO_TMA") == nullptr) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -552,7 +552,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       bool good = true;
       for (int a = 0; a < 3 && good; ++a) {
         int tx = 0, tn = 0;
-        ctx->ops->flux_tile(a, &tx, &tn);
+        ctx->ops->flux_tile(a, ctx->scheme_id == CGKS_CGKS5 ? 1 : 0, &tx, &tn);
         const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
         {
           const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)g.en[1], (cuuint64_t)nrec, (cuuint64_t)g.en[2]};

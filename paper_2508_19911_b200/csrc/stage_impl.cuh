@@ -99,7 +99,7 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
   static const CUtensorMap none{};
   kern<<<grid, 128, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage,
                                         a.use_tma ? a.tm_rec[AX] : none, a.use_tma ? a.tm_U[AX] : none,
-                                        a.use_tma && COMPACT && !BOX ? 1 : 0);
+                                        a.use_tma && !BOX ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
@@ -227,17 +227,25 @@ int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part
   return diag_t<false, true, true>(env, a, wtab, part, nblk);
 }
 
-void flux_tile_fn(int ax, int* tx, int* tn) {
+template <bool C>
+void flux_tile_t(int ax, int* tx, int* tn) {
   if (ax == 0) {
-    *tx = FluxTile<D, 0, true>::TX;
-    *tn = FluxTile<D, 0, true>::TN;
+    *tx = FluxTile<D, 0, C>::TX;
+    *tn = FluxTile<D, 0, C>::TN;
   } else if (ax == 1) {
-    *tx = FluxTile<D, (D > 1 ? 1 : 0), true>::TX;
-    *tn = FluxTile<D, (D > 1 ? 1 : 0), true>::TN;
+    *tx = FluxTile<D, (D > 1 ? 1 : 0), C>::TX;
+    *tn = FluxTile<D, (D > 1 ? 1 : 0), C>::TN;
   } else {
-    *tx = FluxTile<D, (D > 2 ? 2 : 0), true>::TX;
-    *tn = FluxTile<D, (D > 2 ? 2 : 0), true>::TN;
+    *tx = FluxTile<D, (D > 2 ? 2 : 0), C>::TX;
+    *tn = FluxTile<D, (D > 2 ? 2 : 0), C>::TN;
   }
+}
+
+void flux_tile_fn(int ax, int compact, int* tx, int* tn) {
+  if (compact)
+    flux_tile_t<true>(ax, tx, tn);
+  else
+    flux_tile_t<false>(ax, tx, tn);
 }
 
 int lines_init_fn(cudaStream_t s, const double* U, double* Lb, long long ncell) {
