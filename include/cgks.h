@@ -134,7 +134,8 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);
  * through the cell at the transverse Gauss point g = p * n2 + q of the faces (p: sign -, + along
  * (a+1)%3, q along (a+2)%3, active axes only; offsets +-h/(2 sqrt 3)), value (Q(end) - Q(start)) / h_a.
  * cgks_set_state initialises every line along a with dQ/dx_a; call cgks_set_lines after it to set
- * exact line data.  Host or device pointers; CGKS_ERR_CONFIG without line DOFs. */
+ * exact line data.  Rank-local block on decomposed contexts (their 2-plane z halos travel with the
+ * state's, cgks_step_group / NCCL).  Host or device pointers; CGKS_ERR_CONFIG without line DOFs. */
 int cgks_set_lines(cgks_ctx* ctx, const double* L);
 int cgks_get_lines(const cgks_ctx* ctx, double* L);
 

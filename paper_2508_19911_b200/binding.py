@@ -261,10 +261,11 @@ class Solver:
         self._check(self._L.cgks_set_lines(self.ctx, _ptr(L)))
 
     def get_lines(self):
-        """cgks_get_lines: [nl][5][nz][ny][nx], nl = 12 / 4 / 1 for 3-D / 2-D / 1-D."""
+        """cgks_get_lines: [nl][5][nz][ny][nx] of this rank's cells, nl = 12 / 4 / 1 for 3-D / 2-D / 1-D."""
         dim = 3 if self.n[2] > 1 else (2 if self.n[1] > 1 else 1)
         nl = {3: 12, 2: 4, 1: 1}[dim]
-        out = np.zeros((nl, 5) + tuple(self.n[::-1]))
+        _, nn = self.local_shape
+        out = np.zeros((nl, 5, nn[2], nn[1], nn[0]))
         self._check(self._L.cgks_get_lines(self.ctx, ctypes.c_void_p(out.ctypes.data)))
         return out
 

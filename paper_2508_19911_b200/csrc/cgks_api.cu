@@ -232,14 +232,25 @@ static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
 // z-slab halo: 2 ghost planes per side of every field (R: dependency radius 2 per stage).
 // With the [z][field][y][x] layout each halo is one contiguous block of 2 planes.
 // ---------------------------------------------------------------------------
-static long long plane_block(const cgks_ctx* c) { return (long long)c->NV * c->geo.plane; }
-static double* low_send(const cgks_ctx* c, double* X) { return X + (long long)c->geo.zoff * plane_block(c); }
-static double* high_send(const cgks_ctx* c, double* X) {
-  return X + (long long)(c->geo.zoff + c->geo.n[2] - 2) * plane_block(c);
+// The line DOFs (NEXT-1) have the same [z][field][y][x] layout with 5 * nl fields, so their halo is
+// one more contiguous block per side, exchanged with the state it is paired with.
+static long long plane_block(const cgks_ctx* c, bool lines = false) {
+  return (long long)(lines ? 5 * c->nl : c->NV) * c->geo.plane;
 }
-static double* low_ghost(const cgks_ctx* c, double* X) { return X; }
-static double* high_ghost(const cgks_ctx* c, double* X) {
-  return X + (long long)(c->geo.zoff + c->geo.n[2]) * plane_block(c);
+static double* low_send(const cgks_ctx* c, double* X, bool l = false) {
+  return X + (long long)c->geo.zoff * plane_block(c, l);
+}
+static double* high_send(const cgks_ctx* c, double* X, bool l = false) {
+  return X + (long long)(c->geo.zoff + c->geo.n[2] - 2) * plane_block(c, l);
+}
+static double* low_ghost(const cgks_ctx*, double* X, bool = false) { return X; }
+static double* high_ghost(const cgks_ctx* c, double* X, bool l = false) {
+  return X + (long long)(c->geo.zoff + c->geo.n[2]) * plane_block(c, l);
+}
+// the line buffer paired with state buffer X (nullptr without line DOFs)
+static double* lines_of(const cgks_ctx* c, const double* X) {
+  if (!c->lines) return nullptr;
+  return X == c->U[0] ? c->Lb[0] : (X == c->U[1] ? c->Lb[1] : (X == c->Us ? c->Ls : nullptr));
 }
 
 static int nccl_check(cgks_ctx* ctx, int r, const char* what) {
@@ -248,18 +259,24 @@ static int nccl_check(cgks_ctx* ctx, int r, const char* what) {
   return CGKS_ERR_COMM;
 }
 
-// halo exchange of buffer X with the two z neighbours through NCCL (one group per stage)
+// halo exchange of buffer X (and its line DOFs) with the two z neighbours through NCCL (one group
+// per stage)
 static int exchange_nccl(cgks_ctx* ctx, double* X) {
   const int P = ctx->nranks, r = ctx->rank;
   const int lo = (r + P - 1) % P, hi = (r + 1) % P;
-  const size_t cnt = (size_t)(2 * plane_block(ctx));
   auto& A = nccl::g_api;
   cudaStream_t st = ctx->capturing ? ctx->cap_stream : ctx->stream;
+  double* Xl = lines_of(ctx, X);
   int e = A.GroupStart();
-  if (!e) e = A.Send(low_send(ctx, X), cnt, nccl::Float64, lo, ctx->comm, st);
-  if (!e) e = A.Send(high_send(ctx, X), cnt, nccl::Float64, hi, ctx->comm, st);
-  if (!e) e = A.Recv(high_ghost(ctx, X), cnt, nccl::Float64, hi, ctx->comm, st);
-  if (!e) e = A.Recv(low_ghost(ctx, X), cnt, nccl::Float64, lo, ctx->comm, st);
+  for (int part = 0; part < (Xl ? 2 : 1) && !e; ++part) {
+    const bool l = part == 1;
+    double* B = l ? Xl : X;
+    const size_t cnt = (size_t)(2 * plane_block(ctx, l));
+    if (!e) e = A.Send(low_send(ctx, B, l), cnt, nccl::Float64, lo, ctx->comm, st);
+    if (!e) e = A.Send(high_send(ctx, B, l), cnt, nccl::Float64, hi, ctx->comm, st);
+    if (!e) e = A.Recv(high_ghost(ctx, B, l), cnt, nccl::Float64, hi, ctx->comm, st);
+    if (!e) e = A.Recv(low_ghost(ctx, B, l), cnt, nccl::Float64, lo, ctx->comm, st);
+  }
   int e2 = A.GroupEnd();
   return nccl_check(ctx, e ? e : e2, "halo exchange");
 }
@@ -350,8 +367,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "invalid gas parameters gamma=%g mu=%g Pr=%g", gamma, mu, Pr);
     return fail(CGKS_ERR_CONFIG);
   }
-  if (scheme->lines && (scheme->id != CGKS_CGKS5 || (grid->nproc[2] > 1))) {
-    set_msg(ctx, "line DOFs need CGKS-5th on a single rank");
+  if (scheme->lines && scheme->id != CGKS_CGKS5) {
+    set_msg(ctx, "line DOFs need CGKS-5th");
     return fail(CGKS_ERR_CONFIG);
   }
   if (!(scheme->sutherland_S >= 0.0)) {
@@ -789,17 +806,23 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
   const int cur0 = c0->cur;
   auto xchg = [&](int which) -> int {  // which: 0 = U[cur], 1 = Us
     if (n == 1) return CGKS_OK;
-    const size_t bytes = sizeof(double) * (size_t)(2 * plane_block(c0));
-    for (int r = 0; r < n; ++r) {
-      cgks_ctx* me = ctxs[r];
-      cgks_ctx* lo = ctxs[(r + n - 1) % n];
-      cgks_ctx* hi = ctxs[(r + 1) % n];
-      double* Xm = which ? me->Us : me->U[me->cur];
-      double* Xl = which ? lo->Us : lo->U[lo->cur];
-      double* Xh = which ? hi->Us : hi->U[hi->cur];
-      if (cudaMemcpyAsync(low_ghost(me, Xm), high_send(lo, Xl), bytes, cudaMemcpyDeviceToDevice, c0->stream) ||
-          cudaMemcpyAsync(high_ghost(me, Xm), low_send(hi, Xh), bytes, cudaMemcpyDeviceToDevice, c0->stream))
-        return CGKS_ERR_CUDA;
+    for (int part = 0; part < (c0->lines ? 2 : 1); ++part) {
+      const bool l = part == 1;
+      const size_t bytes = sizeof(double) * (size_t)(2 * plane_block(c0, l));
+      for (int r = 0; r < n; ++r) {
+        cgks_ctx* me = ctxs[r];
+        cgks_ctx* lo = ctxs[(r + n - 1) % n];
+        cgks_ctx* hi = ctxs[(r + 1) % n];
+        auto buf = [&](cgks_ctx* c) -> double* {
+          double* X = which ? c->Us : c->U[c->cur];
+          return l ? lines_of(c, X) : X;
+        };
+        if (cudaMemcpyAsync(low_ghost(me, buf(me), l), high_send(lo, buf(lo), l), bytes, cudaMemcpyDeviceToDevice,
+                            c0->stream) ||
+            cudaMemcpyAsync(high_ghost(me, buf(me), l), low_send(hi, buf(hi), l), bytes, cudaMemcpyDeviceToDevice,
+                            c0->stream))
+          return CGKS_ERR_CUDA;
+      }
     }
     return CGKS_OK;
   };
