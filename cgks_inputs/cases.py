@@ -160,14 +160,27 @@ def line_points(dim: int, a: int):
     return pts
 
 
-def line_derivatives(fprim, n, lo, hi, gamma):
+def line_derivatives(fprim, n, lo, hi, gamma, mesh_nodes=None):
     """Exact line-averaged derivatives of cons(fprim(x, y, z)) for the line-DOF variant:
-    (Q(x_c + h_a/2 e_a + t) - Q(x_c - h_a/2 e_a + t)) / h_a at the transverse Gauss points t of each axis;
-    layout [nlines][5][nz][ny][nx] (see line_points)."""
+    (Q(x_c + h_a/2 e_a + t) - Q(x_c - h_a/2 e_a + t)) / h_a at the transverse Gauss points t of each axis
+    (offsets in units of the cell's own widths); layout [nlines][5][nz][ny][nx] (see line_points).
+    mesh_nodes: optional per-axis node arrays of a stretched mesh (NEXT-4), as in gl_average."""
     n = tuple(int(a) for a in n)
     dim = 3 if n[2] > 1 else (2 if n[1] > 1 else 1)
-    h = [(hi[a] - lo[a]) / n[a] for a in range(3)]
-    c = [lo[a] + (np.arange(n[a]) + 0.5) * h[a] for a in range(3)]
+    c, hh = [], []
+    for a in range(3):
+        nd = None if mesh_nodes is None else mesh_nodes[a]
+        if nd is None:
+            ha = (hi[a] - lo[a]) / n[a]
+            c.append(lo[a] + (np.arange(n[a]) + 0.5) * ha)
+            hh.append(np.full(n[a], ha))
+        else:
+            nd = np.asarray(nd, dtype=np.float64)
+            c.append(0.5 * (nd[1:] + nd[:-1]))
+            hh.append(np.diff(nd))
+    Z, Y, X = np.meshgrid(c[2], c[1], c[0], indexing="ij")
+    HZ, HY, HX = np.meshgrid(hh[2], hh[1], hh[0], indexing="ij")
+    h = [HX, HY, HZ]
     Z, Y, X = np.meshgrid(c[2], c[1], c[0], indexing="ij")
     pos = [X, Y, Z]
     out = []

@@ -664,10 +664,6 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     bool any = false;
     for (int a = 0; a < dim; ++a) any = any || grid->nodes[a] != nullptr;
     if (any) {
-      if (ctx->lines) {
-        set_msg(ctx, "line DOFs are not combined with stretched meshes in this version");
-        return fail(CGKS_ERR_CONFIG);
-      }
       g.stretched = 1;
       for (int a = 0; a < 3; ++a) {
         const long long N = grid->n[a];

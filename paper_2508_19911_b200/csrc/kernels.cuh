@@ -205,6 +205,7 @@ struct Recon5TileLoader {
   double w[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // STR: widths of the cells at offsets -1, 0, +1 per axis
   const double* __restrict__ lv = nullptr;  // line DOFs: line 0 of this component at this cell (field stride plane)
   long long lstride = 0;                    // 5 * plane: next line
+  double lmask = 1.0;                       // 0 for the ghost cell of an inflow boundary (no lines)
   static constexpr int HALO = ReconTile<DIM>::HALO;
   static constexpr int SY = ReconTile<DIM>::HX, SZ = ReconTile<DIM>::HX * ReconTile<DIM>::HY;
   __device__ __forceinline__ double at(int f, int ox, int oy, int oz) const {
@@ -220,7 +221,8 @@ struct Recon5TileLoader {
   __device__ __forceinline__ double line(int l) const {
     constexpr int NGL = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
     const int a = l / NGL;
-    return (a == 0 ? h0 : (a == 1 ? h1 : h2)) * __ldg(lv + l * lstride);
+    if (STR) return lmask * w[a][1] * __ldg(lv + l * lstride);  // the own width (R37)
+    return lmask * (a == 0 ? h0 : (a == 1 ? h1 : h2)) * __ldg(lv + l * lstride);
   }
 };
 
@@ -314,7 +316,25 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
     }
     if (LINES) {  // own-cell lines, [z][l*5+v][y][x] (valid cells only; ragged threads read cell 0)
       constexpr int NLF = 5 * (DIM == 3 ? 12 : (DIM == 2 ? 4 : 1));
-      L.lv = Lin + (valid ? sidx(NLF, v, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, k)) : 0);
+      int li[3] = {i, j, k};
+      if (BOX) {  // box ghost cells: the boundary cell's lines (outflow), none (inflow), as ld_state
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (c_geo.halo[a]) continue;
+          if (c_geo.bounded[a]) {
+            if (li[a] < 0 || li[a] >= c_geo.n[a]) {
+              if (c_geo.bc[a][li[a] < 0 ? 0 : 1] == 1) L.lmask = 0.0;
+              li[a] = li[a] < 0 ? 0 : c_geo.n[a] - 1;
+            }
+          } else {
+            li[a] = wrapi(li[a], c_geo.n[a]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) li[a] = wrap_ax(a, li[a]);
+      }
+      L.lv = Lin + (valid ? sidx(NLF, v, li[0], li[1], li[2]) : 0);
       L.lstride = 5 * c_geo.plane;
     }
     double acc[S::NB];
@@ -913,7 +933,7 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
       const int wk = c_geo.bounded[2] ? k + (a == 2) : wrapi(k + (a == 2), c_geo.n[2]);
       const double* flo = F[a] + (long long)k * NF * fpl + (long long)j * fn0 + i;
       const double* fhi = F[a] + (long long)wk * NF * fpl + (long long)wj * fn0 + wi;
-      const double ih = c_geo.ih[a];
+      const double ih = c_geo.stretched ? icw(a, a == 0 ? i : (a == 1 ? j : k)) : c_geo.ih[a];  // own width (R37)
 #pragma unroll
       for (int g = 0; g < NGL; ++g)
 #pragma unroll

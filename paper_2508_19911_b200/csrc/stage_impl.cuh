@@ -141,6 +141,12 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
 int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
   const bool c = a.scheme == 1, nl = a.nonlinear != 0, b = a.box != 0;
   if (a.stretched) {  // stretched tensor-product mesh (NEXT-4)
+    if (c && a.lines) {  // with line DOFs (NEXT-1)
+      if (!nl && !b) return stage_t<true, false, false, true, true>(env, a, mode, stage);
+      if (nl && !b) return stage_t<true, true, false, true, true>(env, a, mode, stage);
+      if (!nl && b) return stage_t<true, false, true, true, true>(env, a, mode, stage);
+      return stage_t<true, true, true, true, true>(env, a, mode, stage);
+    }
     if (c && !nl && !b) return stage_t<true, false, false, false, true>(env, a, mode, stage);
     if (c && nl && !b) return stage_t<true, true, false, false, true>(env, a, mode, stage);
     if (c && !nl && b) return stage_t<true, false, true, false, true>(env, a, mode, stage);
@@ -172,6 +178,7 @@ int stage_fn(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
 template <bool COMPACT, bool NONLIN, bool BOX>
 int recon_any(LaunchEnv& env, const StageArgs& a) {
   if (COMPACT) {
+    if (a.lines && a.stretched) return recon5_launch<NONLIN, BOX, true, true>(env, a);
     if (a.lines) return recon5_launch<NONLIN, BOX, true, false>(env, a);
     if (a.stretched) return recon5_launch<NONLIN, BOX, false, true>(env, a);
     return recon5_launch<NONLIN, BOX>(env, a);

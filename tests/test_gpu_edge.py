@@ -22,7 +22,7 @@ def _S():
     dict(gamma=0.9),
     dict(mu=-1.0),
     dict(scheme=0, lines=1),
-    dict(lines=1, nodes=(np.array([0.0, 0.2, 0.5, 0.7, 1.0]), None, None)),
+    dict(sutherland_S=-1.0),
     dict(nodes=(np.array([0.0, 0.5, 0.4, 1.0]), None, None), n=(3, 4, 4)),
 ])
 def test_invalid_configurations_are_refused(kw):

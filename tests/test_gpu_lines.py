@@ -111,3 +111,28 @@ def test_lines_diagnostics_and_qcriterion():
     qo = oracle.qcriterion(prob, Qg, Gg, Lg)
     assert np.all(np.abs(dg - do) <= 1e-12 * np.abs(do) + 1e-300), (dg, do)
     assert np.abs(qg - qo).max() <= 1e-11 * np.abs(qo).max()
+
+
+@pytest.mark.parametrize("nl", [0, 1])
+@pytest.mark.parametrize("bc", [((2, 2), (0, 0), (0, 0)), ((0, 0), (1, 1), (2, 2))])
+def test_lines_parity_box(nl, bc):
+    # box boundaries: a ghost cell takes the boundary cell's lines (outflow) or none (inflow), as in
+    # the oracle's ghost rule
+    from paper_2508_19911_b200 import Solver
+    n, lo, hi, Q, G, L = _smooth3d()
+    bs = np.zeros((3, 2, 5))
+    bs[:, :] = (1.0, 0.1, 0.0, 0.0, 1.0 / 0.4 + 0.005)  # inflow: rho = 1, u = 0.1, p = 1
+    kw = dict(gamma=1.4, mu=2e-3, Pr=0.72, nonlinear=nl, bc=bc, bc_state=bs)
+    prob = oracle.Problem(n=n, lo=lo, hi=hi, scheme=1, time_scheme=2, lines=1, cfl=0.3, **kw)
+    Qo, Go, Lo, to, _, rc = oracle.run_lines(prob, Q, G, L, 10)
+    assert rc == 0
+    S = Solver(n, lo, hi, scheme=1, lines=1, cfl=0.3, **kw)
+    S.set_state(Q, G)
+    S.set_lines(L)
+    S.step(10)
+    Qg, Gg = S.get_state()
+    Lg = S.get_lines()
+    tg, _, _ = S.get_time()
+    S.close()
+    assert abs(tg - to) <= 1e-13 * to
+    _compare(Qg, Gg, Lg, Qo, Go, Lo, 2 * math.pi, 1e-10)

@@ -88,3 +88,60 @@ def test_jet_inflow_crocco_busemann():
     want = 1.0 + 0.2 * f + 0.5 * (gam - 1.0) * 0.81 * 1.2 * f * (1.0 - f)
     assert np.abs(T - want).max() < 1e-12
     assert np.all(np.diff(u) <= 1e-15)  # monotone profile
+
+
+# ---- line DOFs (NEXT-1) on stretched meshes: the own cell's lines in its own reference units
+def _vortex_lines_on(n, beta):
+    from cgks_inputs import line_derivatives
+    nodes, Q, G = _vortex_on(n, beta)
+    L = line_derivatives(_vortex_prim(0.0), (n, n, 1), (0, 0, 0), (10, 10, 1), 1.4, mesh_nodes=nodes)
+    return nodes, Q, G, L
+
+
+def test_lines_uniform_nodes_reproduce_uniform_path():
+    from cgks_inputs import line_derivatives
+    c = vortex(40)
+    nodes = (np.arange(41) * 0.25, np.arange(41) * 0.25, np.array([0.0, 1.0]))
+    L = line_derivatives(_vortex_prim(0.0), c.n, c.lo, c.hi, c.gamma)
+    L2 = line_derivatives(_vortex_prim(0.0), c.n, c.lo, c.hi, c.gamma, mesh_nodes=nodes)
+    assert np.array_equal(L, L2)
+    d = c.problem_kwargs()
+    p0 = oracle.Problem(**d, scheme=1, time_scheme=2, lines=1)
+    p1 = oracle.Problem(**d, scheme=1, time_scheme=2, lines=1, nodes=nodes)
+    a = oracle.run_lines(p0, c.Q, c.G, L, 5)
+    b = oracle.run_lines(p1, c.Q, c.G, L, 5)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
+
+
+def test_lines_conservation_on_stretched_periodic_mesh():
+    nodes, Q, G, L = _vortex_lines_on(24, 0.3)
+    V = np.diff(nodes[0])[None, :] * np.diff(nodes[1])[:, None] * 1.0
+    p = oracle.Problem(n=(24, 24, 1), lo=(0, 0, 0), hi=(10, 10, 1), scheme=1, time_scheme=2, lines=1,
+                       mu=1e-3, Pr=0.72, nodes=nodes, nonlinear=1)
+    Q1, G1, L1, t, dt, rc = oracle.run_lines(p, Q, G, L, 6)
+    assert rc == 0
+    for v in range(5):
+        m0 = (Q[v, 0] * V).sum()
+        m1 = (Q1[v, 0] * V).sum()
+        assert abs(m1 - m0) <= 1e-13 * max(1.0, abs(m0)), (v, m0, m1)
+
+
+def test_lines_vortex_converges_on_stretched_mesh():
+    """the line data scaled by the own widths (R37): high-order convergence on a stretched mesh, with
+    errors of the size the gradient-DOF scheme has on the same meshes (a line scaled by a wrong width
+    is an O(1) relative error in the own-cell data and costs orders of magnitude at n = 40)."""
+    errs, errs_g = [], []
+    for n, ns in ((20, 10), (40, 24)):
+        nodes, Q, G, L = _vortex_lines_on(n, 0.2)
+        kw = dict(n=(n, n, 1), lo=(0, 0, 0), hi=(10, 10, 1), scheme=1, time_scheme=2, fixed_dt=1.0 / ns,
+                  mu=0.0, Pr=1.0, tau_eps=0.0, tau_C=0.0, nodes=nodes)
+        Q1, _, _, t, _, rc = oracle.run_lines(oracle.Problem(**kw, lines=1), Q, G, L, ns)
+        assert rc == 0
+        Qg, _, tg, _, rc = oracle.run(oracle.Problem(**kw), Q, G, ns)
+        assert rc == 0 and tg == t
+        Qe, _ = gl_average(_vortex_prim(t), (n, n, 1), (0, 0, 0), (10, 10, 1), 1.4, nq=5, mesh_nodes=nodes)
+        errs.append(np.abs(Q1[0] - Qe[0]).mean())
+        errs_g.append(np.abs(Qg[0] - Qe[0]).mean())
+    o = math.log2(errs[0] / errs[1])
+    assert o > 3.0, (errs, o)
+    assert errs[1] < 3.0 * errs_g[1], (errs, errs_g)
