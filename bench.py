@@ -225,7 +225,12 @@ def run_ours(args, rank, ws, lr):
             from cgks_inputs import stretched_nodes
             nodes = tuple(stretched_nodes(case.n[a], case.lo[a], case.hi[a], args.stretch) if case.n[a] > 1 else None
                           for a in range(3))
-        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, lines=args.lines, nodes=nodes)
+        nid = None
+        if args.nccl_self:  # the slab path on one GPU: NCCL halo exchange with itself (overlapped)
+            from paper_2508_19911_b200 import nccl_unique_id
+            nid = nccl_unique_id()
+        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, lines=args.lines, nodes=nodes,
+                             nccl_id=nid)
     NV = 20 if scheme_id == 1 else 5
     Qd = torch.from_numpy(np.ascontiguousarray(case.Q)).cuda()
     Gd = torch.from_numpy(np.ascontiguousarray(case.G)).cuda()
@@ -320,7 +325,8 @@ def run_ours(args, rank, ws, lr):
                        "scheme": args.scheme + ("-geno" if case.nonlinear else "-linear")
                        + ("-lines" if args.lines else "") + (f"-stretched{args.stretch:g}" if args.stretch else ""),
                        "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
-                       "parallelism": f"zslab{ws} (NCCL halo + allreduce-min)" if ws > 1 else "1gpu",
+                       "parallelism": f"zslab{ws} (NCCL halo + allreduce-min)" if ws > 1 else (
+                           "zslab1 (NCCL self halo, overlapped)" if args.nccl_self else "1gpu"),
                        "l2": "state larger than L2 (no flush)"},
             "roofline": roof,
             "algorithmic_flops_per_cell_update": per_cell,
@@ -349,6 +355,8 @@ def main():
     ap.add_argument("--stretch", type=float, default=0.0,
                     help="sine-stretched tensor-product mesh with this amplitude (NEXT-4; timing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="1 GPU through the z-slab path: ghost planes + NCCL halo exchange with itself")
     args = ap.parse_args()
     rank, ws, lr = dist_init()
     if args.impl == "reference":

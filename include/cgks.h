@@ -116,8 +116,10 @@ int cgks_nccl_unique_id(void* out128);
 
 /* Multi-rank contexts (grid.nproc = (1,1,P), P > 1):
  *   - with grid.nccl_id set, each process owns one rank; cgks_step exchanges a 2-plane halo
- *     of all fields with the z neighbours (ncclSend/ncclRecv, one group per stage) and
- *     reduces dt with ncclAllReduce(min);
+ *     of all fields (and line DOFs) with the z neighbours (ncclSend/ncclRecv, one group per
+ *     stage, on a second stream overlapped with the interior reconstruction; CGKS_NO_OVERLAP=1
+ *     serialises it) and reduces dt with ncclAllReduce(min).  P = 1 with grid.nccl_id set runs
+ *     the same slab path with the rank as its own neighbour (bitwise equal to the plain context);
  *   - with grid.nccl_id == NULL the P contexts of one process (same device) form an
  *     in-process decomposition advanced in lock-step by cgks_step_group (halo copies,
  *     shared time state); cgks_step refuses such contexts.

@@ -138,6 +138,11 @@ struct cgks_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   bool capturing = false;
+  // halo overlap (NCCL ranks): the exchange runs on halo_stream while the interior planes are
+  // reconstructed (fork / join events; captured into the step graph like the main stream)
+  bool overlap = false;
+  cudaStream_t halo_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
@@ -221,11 +226,36 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   return a;
 }
 
-static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage) {
+static int run_stage(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage, int part = 0, int rz0 = 0,
+                     int rz1 = -1, cudaStream_t st = nullptr) {
   StageArgs a = stage_args(ctx, Uin, Uout);
+  a.part = part;
+  a.rz0 = rz0;
+  a.rz1 = rz1;
   LaunchEnv env = env_of(ctx);
+  if (st) env.stream = st;
   int rc = ctx->ops->stage(env, a, mode, stage);
   return rc ? CGKS_ERR_CUDA : CGKS_OK;
+}
+
+// Halo-overlapped stage of a z-slab rank, in two halves around the exchange: (0) the reconstruction
+// of the interior planes k = 1 .. nz-2 (extended planes [2, nz)), which read no ghost plane;
+// (1) the reconstruction of the planes next to the ghosts (k = -1, 0, nz-1, nz), then the fluxes and
+// the update.  Same kernels, same per-cell arithmetic: bitwise equal to the unsplit stage.
+// half 1 may put the two boundary reconstructions on another stream (bst): the NCCL ranks run them on
+// the halo stream right after the exchange, concurrently with the tail of the interior one.
+static int run_stage_half(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage, int half,
+                          cudaStream_t bst = nullptr, cudaEvent_t join = nullptr) {
+  const int nz = ctx->geo.n[2];
+  if (half == 0) return run_stage(ctx, Uin, Uout, mode, stage, 1, 2, nz);
+  int rc = run_stage(ctx, Uin, Uout, mode, stage, 1, 0, 2, bst);
+  if (!rc) rc = run_stage(ctx, Uin, Uout, mode, stage, 1, nz, nz + 2, bst);
+  if (rc) return rc;
+  if (join) {
+    CK(cudaEventRecord(join, bst));
+    CK(cudaStreamWaitEvent(ctx->capturing ? ctx->cap_stream : ctx->stream, join, 0));
+  }
+  return run_stage(ctx, Uin, Uout, mode, stage, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -261,11 +291,10 @@ static int nccl_check(cgks_ctx* ctx, int r, const char* what) {
 
 // halo exchange of buffer X (and its line DOFs) with the two z neighbours through NCCL (one group
 // per stage)
-static int exchange_nccl(cgks_ctx* ctx, double* X) {
+static int exchange_nccl(cgks_ctx* ctx, double* X, cudaStream_t st) {
   const int P = ctx->nranks, r = ctx->rank;
   const int lo = (r + P - 1) % P, hi = (r + 1) % P;
   auto& A = nccl::g_api;
-  cudaStream_t st = ctx->capturing ? ctx->cap_stream : ctx->stream;
   double* Xl = lines_of(ctx, X);
   int e = A.GroupStart();
   for (int part = 0; part < (Xl ? 2 : 1) && !e; ++part) {
@@ -283,8 +312,24 @@ static int exchange_nccl(cgks_ctx* ctx, double* X) {
 
 static int exchange(cgks_ctx* ctx, double* X) {
   if (!ctx->geo.halo[2]) return CGKS_OK;
-  if (ctx->comm_mode == 1) return exchange_nccl(ctx, X);
+  if (ctx->comm_mode == 1) return exchange_nccl(ctx, X, ctx->capturing ? ctx->cap_stream : ctx->stream);
   return CGKS_OK;  // group mode exchanges in cgks_step_group
+}
+
+// one stage of a rank: halo exchange of Uin, then the stage; NCCL ranks overlap the exchange (on
+// halo_stream) with the interior reconstruction
+static int halo_stage(cgks_ctx* ctx, double* Uin, double* Uout, int mode, int stage) {
+  if (!(ctx->geo.halo[2] && ctx->comm_mode == 1 && ctx->overlap)) {
+    int rc = exchange(ctx, Uin);
+    return rc ? rc : run_stage(ctx, Uin, Uout, mode, stage);
+  }
+  cudaStream_t main = ctx->capturing ? ctx->cap_stream : ctx->stream;
+  CK(cudaEventRecord(ctx->ev_fork, main));  // Uin is complete
+  CK(cudaStreamWaitEvent(ctx->halo_stream, ctx->ev_fork, 0));
+  int rc = exchange_nccl(ctx, Uin, ctx->halo_stream);
+  if (!rc) rc = run_stage_half(ctx, Uin, Uout, mode, stage, 0);
+  if (!rc) rc = run_stage_half(ctx, Uin, Uout, mode, stage, 1, ctx->halo_stream, ctx->ev_join);
+  return rc;
 }
 
 static int dt_reduce(cgks_ctx* ctx) {
@@ -304,14 +349,11 @@ static int one_step(cgks_ctx* ctx) {
   int rc = dt_reduce(ctx);
   if (rc) return rc;
   if (ctx->ops->dt_final(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
-  rc = exchange(ctx, Un);
-  if (rc) return rc;
   if (ctx->time_scheme == CGKS_TIME_S1O2) {
-    rc = run_stage(ctx, Un, Unext, 2, 1);
+    rc = halo_stage(ctx, Un, Unext, 2, 1);
   } else {
-    rc = run_stage(ctx, Un, ctx->Us, 0, 1);
-    if (!rc) rc = exchange(ctx, ctx->Us);
-    if (!rc) rc = run_stage(ctx, ctx->Us, Unext, 1, 2);
+    rc = halo_stage(ctx, Un, ctx->Us, 0, 1);
+    if (!rc) rc = halo_stage(ctx, ctx->Us, Unext, 1, 2);
   }
   if (rc) return rc;
   if (ctx->ops->step_end(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
@@ -320,7 +362,7 @@ static int one_step(cgks_ctx* ctx) {
 }
 
 static int count_launches(cgks_ctx* c) {
-  int per_stage = 1 + c->dim + 1;
+  int per_stage = (c->overlap ? 3 : 1) + c->dim + 1;  // overlapped halo: the reconstruction in 3 launches
   int stages = (c->time_scheme == CGKS_TIME_S1O2) ? 1 : 2;
   return 2 + stages * per_stage + 1;
 }
@@ -385,7 +427,10 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "only z-slab decompositions nproc = (1,1,P) are supported");
     return fail(CGKS_ERR_CONFIG);
   }
-  if (P > 1) {
+  // one rank with an NCCL id: the slab machinery with the rank as its own z neighbour (the exchange
+  // is the periodic wrap through NCCL); exercises the multi-rank path on one GPU
+  const bool slab = P > 1 || grid->nccl_id != nullptr;
+  if (slab) {
     const bool zper = grid->bc[2][0] == CGKS_BC_PERIODIC && grid->bc[2][1] == CGKS_BC_PERIODIC;
     if (grid->n[2] <= 1 || !zper || grid->n[2] % P != 0 || grid->n[2] / P < 4 || grid->rank < 0 ||
         grid->rank >= P) {
@@ -421,7 +466,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     g.n[a] = (int)grid->n[a];
     g.h[a] = (grid->hi[a] - grid->lo[a]) / grid->n[a];
     g.ih[a] = 1.0 / g.h[a];
-    if (a == 2 && P > 1) {  // this rank's slab; ghost planes filled by the halo exchange
+    if (a == 2 && slab) {  // this rank's slab; ghost planes filled by the halo exchange
       g.n[2] = (int)(grid->n[2] / P);
       g.halo[2] = 1;
       g.zoff = 2;
@@ -698,7 +743,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
   // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
   // group stepped by cgks_step_group (halo copies on one device)
-  if (P > 1) {
+  if (slab) {
     if (grid->nccl_id) {
       if (!nccl::load()) {
         set_msg(ctx, "cannot load libnccl.so.2 (set CGKS_NCCL_LIB)");
@@ -712,6 +757,13 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
         return fail(CGKS_ERR_COMM);
       }
       ctx->comm_mode = 1;
+      ctx->overlap = std::getenv("CGKS_NO_OVERLAP") == nullptr;
+      if (cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        set_msg(ctx, "halo stream creation failed");
+        return fail(CGKS_ERR_CUDA);
+      }
     } else {
       ctx->comm_mode = 2;
     }
@@ -828,14 +880,26 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
       if (ctxs[r]->ops->dt(env, ctxs[r]->U[ctxs[r]->cur], ctxs[r]->NV, c0->ts, c0->err, ctxs[r]->ncell))
         rc = CGKS_ERR_CUDA;
     if (!rc && c0->ops->dt_final(env, c0->ts, c0->err)) rc = CGKS_ERR_CUDA;
-    if (!rc) rc = xchg(0);
+    // each stage in the two halves of the NCCL ranks' overlapped schedule (interior reconstruction,
+    // exchange, the rest), so the split stage is covered on one device
+    auto stage_all = [&](int which, int mode, int stg) -> int {
+      int r2 = CGKS_OK;
+      for (int half = 0; half < 2 && !r2; ++half) {
+        if (half == 1 && n > 1) r2 = xchg(which);
+        for (int r = 0; r < n && !r2; ++r) {
+          cgks_ctx* c = ctxs[r];
+          double* in = which ? c->Us : c->U[c->cur];
+          double* out = (mode == 0) ? c->Us : c->U[1 - c->cur];
+          r2 = n > 1 ? run_stage_half(c, in, out, mode, stg, half) : (half ? CGKS_OK : run_stage(c, in, out, mode, stg));
+        }
+      }
+      return r2;
+    };
     if (c0->time_scheme == CGKS_TIME_S1O2) {
-      for (int r = 0; r < n && !rc; ++r)
-        rc = run_stage(ctxs[r], ctxs[r]->U[ctxs[r]->cur], ctxs[r]->U[1 - ctxs[r]->cur], 2, 1);
+      if (!rc) rc = stage_all(0, 2, 1);
     } else {
-      for (int r = 0; r < n && !rc; ++r) rc = run_stage(ctxs[r], ctxs[r]->U[ctxs[r]->cur], ctxs[r]->Us, 0, 1);
-      if (!rc) rc = xchg(1);
-      for (int r = 0; r < n && !rc; ++r) rc = run_stage(ctxs[r], ctxs[r]->Us, ctxs[r]->U[1 - ctxs[r]->cur], 1, 2);
+      if (!rc) rc = stage_all(0, 0, 1);
+      if (!rc) rc = stage_all(1, 1, 2);
     }
     if (!rc && c0->ops->step_end(env, c0->ts, c0->err)) rc = CGKS_ERR_CUDA;
     for (int r = 0; r < n; ++r) ctxs[r]->cur = 1 - ctxs[r]->cur;
@@ -1061,7 +1125,7 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->nranks > 1 || ctx->comm_mode == 2) {
+  if (ctx->geo.halo[2]) {
     set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
@@ -1101,7 +1165,7 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
-  if (ctx->nranks > 1 || ctx->comm_mode == 2) {
+  if (ctx->geo.halo[2]) {
     set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
@@ -1310,6 +1374,9 @@ void cgks_destroy(cgks_ctx* ctx) {
   for (int c = 0; c < 2; ++c)
     if (ctx->graph[c]) cudaGraphExecDestroy(ctx->graph[c]);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
   if (g_const_owner == ctx) g_const_owner = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],

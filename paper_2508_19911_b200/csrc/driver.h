@@ -48,6 +48,10 @@ struct StageArgs {
   const CUtensorMap* tm_rec = nullptr;
   const CUtensorMap* tm_U = nullptr;
   int use_tma = 0;
+  // stage parts (halo overlap of z-slab ranks): 0 = the whole stage; 1 = the reconstruction of the
+  // extended z planes [rz0, rz1) only (offsets from the first extended plane); 3 = fluxes + update only
+  int part = 0;
+  int rz0 = 0, rz1 = -1;
 };
 
 struct DimOps {

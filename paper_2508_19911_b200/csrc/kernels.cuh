@@ -271,7 +271,8 @@ template <int DIM, bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
 __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double* __restrict__ U,
                                                                     double* __restrict__ coef,
                                                                     const ErrState* __restrict__ err,
-                                                                    const double* __restrict__ Lin = nullptr) {
+                                                                    const double* __restrict__ Lin = nullptr,
+                                                                    int zb = 0, int ze = 1 << 30) {
   using S = Sten<DIM>;
   using RT = ReconTile<DIM>;
   constexpr int NCO = S::NB * 5;
@@ -281,10 +282,11 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
   // block origin in the extended (reconstruction) index range
   const int x0 = blockIdx.x * RT::TX + c_geo.elo[0];
   const int y0 = blockIdx.y * RT::TY + c_geo.elo[1];
-  const int z0 = blockIdx.z * RT::TZ + c_geo.elo[2];
+  // (z planes [zb, ze) of the extended range: a part of it when the halo exchange is overlapped)
+  const int z0 = zb + blockIdx.z * RT::TZ + c_geo.elo[2];
   const int i = x0 + tx, j = y0 + ty, k = z0 + tz;
   const bool valid = (i < c_geo.elo[0] + c_geo.en[0]) && (j < c_geo.elo[1] + c_geo.en[1]) &&
-                     (k < c_geo.elo[2] + c_geo.en[2]);
+                     (k < c_geo.elo[2] + min(c_geo.en[2], ze));
   const int own = (DIM == 3 ? (tz + 1) * RT::HX * RT::HY : 0) + (DIM >= 2 ? (ty + 1) * RT::HX : 0) + tx + 1;
   const ReconStageMap<DIM> map{reinterpret_cast<unsigned*>(rsm + 2 * RT::NFS * RT::HALO)};
   if (!BOX) {
@@ -422,11 +424,12 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
 // ---------------------------------------------------------------------------
 template <int DIM, bool NONLIN, bool BOX>
 __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, double* __restrict__ slope,
-                                                 const ErrState* __restrict__ err) {
+                                                 const ErrState* __restrict__ err, int zb = 0, int ze = 1 << 30) {
   constexpr int NV = 5;
   if (err->code) return;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long ntot = (long long)c_geo.en[0] * c_geo.en[1] * c_geo.en[2];
+  // extended z planes [zb, ze) (a part of the range when the halo exchange is overlapped)
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x + (long long)zb * c_geo.en[0] * c_geo.en[1];
+  const long long ntot = (long long)c_geo.en[0] * c_geo.en[1] * min(c_geo.en[2], ze);
   if (t >= ntot) return;
   const int i = (int)(t % c_geo.en[0]) + c_geo.elo[0];
   const int j = (int)((t / c_geo.en[0]) % c_geo.en[1]) + c_geo.elo[1];

@@ -54,15 +54,17 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
     attr = true;
   }
+  const int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+  if (z1 <= z0) return 0;
   const dim3 grid((unsigned)((a.en[0] + RT::TX - 1) / RT::TX), (unsigned)((a.en[1] + RT::TY - 1) / RT::TY),
-                  (unsigned)((a.en[2] + RT::TZ - 1) / RT::TZ));
+                  (unsigned)((z1 - z0 + RT::TZ - 1) / RT::TZ));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (env.prof) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, env.stream);
   }
-  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err, a.Lin);
+  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err, a.Lin, z0, z1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of recon5 failed: %s", cudaGetErrorString(e));
@@ -114,11 +116,17 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
 
 template <bool COMPACT, bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
 int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
-  if (COMPACT) {
-    int rc = recon5_launch<NONLIN, BOX, LINES, STR>(env, a);
-    if (rc) return rc;
-  } else {
-    LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  if (a.part != 3) {
+    if (COMPACT) {
+      int rc = recon5_launch<NONLIN, BOX, LINES, STR>(env, a);
+      if (rc) return rc;
+    } else {
+      const int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+      if (z1 > z0)
+        LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), (long long)a.en[0] * a.en[1] * (z1 - z0), 256, a.Uin, a.rec,
+               a.err, z0, z1);
+    }
+    if (a.part == 1) return 0;
   }
   {
     int rc = flux_launch<COMPACT, BOX, 0, LINES, STR>(env, "flux_x", a, stage);
@@ -183,7 +191,7 @@ int recon_any(LaunchEnv& env, const StageArgs& a) {
     if (a.stretched) return recon5_launch<NONLIN, BOX, false, true>(env, a);
     return recon5_launch<NONLIN, BOX>(env, a);
   }
-  LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err);
+  LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), a.necell, 256, a.Uin, a.rec, a.err, 0, 1 << 30);
   return 0;
 }
 

@@ -1,0 +1,54 @@
+"""The NCCL slab path on one GPU: a single rank given an ncclUniqueId runs the z-slab machinery with
+itself as both z neighbours (ghost planes, NCCL send/recv halo exchange = the periodic wrap, dt
+allreduce, the exchange overlapped with the interior reconstruction on a second stream, all captured
+in the step graph).  Same kernels and per-cell arithmetic as the periodic single-rank context, so
+the two runs agree bit for bit."""
+import numpy as np
+import pytest
+
+from cgks_inputs import random_smooth
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, scheme, nl, steps, nccl, L=None, **kw):
+    import torch  # noqa: F401  (loads the libnccl.so.2 the library binds at run time)
+    from paper_2508_19911_b200 import Solver, nccl_unique_id
+    S = Solver.from_case(case, scheme=scheme, nonlinear=nl, nccl_id=nccl_unique_id() if nccl else None, **kw)
+    S.set_state(case.Q, case.G)
+    if L is not None:
+        S.set_lines(L)
+    S.step(steps)
+    Q, G = S.get_state()
+    t = S.get_time()
+    Lo = S.get_lines() if L is not None else None
+    S.close()
+    return Q, G, t, Lo
+
+
+@pytest.mark.parametrize("overlap", [1, 0])
+@pytest.mark.parametrize("graph", [1, 0])
+@pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 1)])
+def test_nccl_self_halo_bitwise(scheme, nl, overlap, graph, monkeypatch):
+    if not overlap:
+        monkeypatch.setenv("CGKS_NO_OVERLAP", "1")
+    if not graph:
+        monkeypatch.setenv("CGKS_NO_GRAPH", "1")
+    case = random_smooth((16, 12, 10), seed=4, jump=0.4 if nl else 0.0)
+    kw = dict(mu=1e-3, Pr=0.72)
+    Q1, G1, t1, _ = _run(case, scheme, nl, 4, False, **kw)
+    Q2, G2, t2, _ = _run(case, scheme, nl, 4, True, **kw)
+    assert t1 == t2
+    assert np.array_equal(Q1, Q2)
+    if scheme == 1:
+        assert np.array_equal(G1, G2)
+
+
+def test_nccl_self_halo_lines_bitwise():
+    case = random_smooth((16, 12, 10), seed=6)
+    rng = np.random.default_rng(2)
+    L = case.G[np.array([0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2])] + 0.01 * rng.standard_normal((12, 5) + tuple(case.n[::-1]))
+    kw = dict(mu=1e-3, Pr=0.72, lines=1)
+    Q1, G1, t1, L1 = _run(case, 1, 0, 3, False, L=L, **kw)
+    Q2, G2, t2, L2 = _run(case, 1, 0, 3, True, L=L, **kw)
+    assert t1 == t2 and np.array_equal(Q1, Q2) and np.array_equal(G1, G2) and np.array_equal(L1, L2)
