@@ -3,7 +3,7 @@
 cell-updates/s and the fraction of the FP64/HBM roofline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload tgv128|tgv64|hit128|shock_vortex|vortex40|tgv_ss116] [--scheme cgks5|gks2]
+                  [--workload tgv<N>|hit<N>|tgv_ss<N>|shock_vortex|vortex40] [--scheme cgks5|gks2]
 
 A step is one full S2O4 time step of CGKS-5th (dt min-reduction + two stages of
 reconstruction, fluxes and update) over the whole grid.  Default workload: the
@@ -35,15 +35,14 @@ METRIC = "CGKS-5th FP64 cell-updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline
 
 
 def make_case(name):
+    """tgv<N> (TGV, BASELINE configs[1]), tgv_ss<N> (high-speed TGV with Sutherland viscosity, nonlinear,
+    P:455-474, NEXT-2: the paper's meshes are 116^3 and 384^3), hit<N>, shock_vortex, vortex40."""
+    import re
     from cgks_inputs import hit, shock_vortex, tgv, tgv_supersonic, vortex
-    if name == "tgv_ss116":  # high-speed TGV, the paper's CGKS-5th mesh (NEXT-2), nonlinear
-        return tgv_supersonic(116)
-    if name == "tgv128":
-        return tgv(128)
-    if name == "tgv64":
-        return tgv(64)
-    if name == "hit128":
-        return hit(128)
+    m = re.fullmatch(r"(tgv_ss|tgv|hit)(\d+)", name)
+    if m:
+        n = int(m.group(2))
+        return {"tgv_ss": tgv_supersonic, "tgv": tgv, "hit": hit}[m.group(1)](n)
     if name == "shock_vortex":
         return shock_vortex()
     if name == "vortex40":
@@ -137,7 +136,7 @@ def cpu_baseline(case_name, scheme, budget_s=20.0):
         c = tgv_supersonic(32)
     else:
         c = tgv(32) if case_name.startswith("tgv") else make_case(case_name)
-    if case_name in ("hit128",):
+    if case_name.startswith("hit"):
         from cgks_inputs import hit
         c = hit(32)
     prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if scheme == "cgks5" else 0,
@@ -236,6 +235,10 @@ def run_ours(args, rank, ws, lr):
     Gd = torch.from_numpy(np.ascontiguousarray(case.G)).cuda()
     S.set_state(Qd, Gd if scheme_id == 1 else None)
     torch.cuda.synchronize()
+    del Qd, Gd  # the library holds the state; free HBM for the large meshes (384^3 uses ~165 GB)
+    torch.cuda.empty_cache()
+    free_b, total_b = torch.cuda.mem_get_info()
+    hbm_used_gb = (total_b - free_b) / 1e9
     for _ in range(args.warmup):
         S.step(1)
     torch.cuda.synchronize()
@@ -278,7 +281,7 @@ def run_ours(args, rank, ws, lr):
     nbytes = Qh.nbytes + (Gh.nbytes if scheme_id == 1 else 0)
 
     # roofline of the dominant kernel: per-kernel CUDA-event durations on the library stream
-    S.set_state(Qd, Gd if scheme_id == 1 else None)
+    S.set_state(Qh, Gh if scheme_id == 1 else None)
     prof = S.profile(max(2, min(args.steps, 4)))
     flops, per_cell = S.algorithmic_flops()
     dom = max(prof, key=lambda k: prof[k][0])
@@ -327,7 +330,8 @@ def run_ours(args, rank, ws, lr):
                        "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
                        "parallelism": f"zslab{ws} (NCCL halo + allreduce-min)" if ws > 1 else (
                            "zslab1 (NCCL self halo, overlapped)" if args.nccl_self else "1gpu"),
-                       "l2": "state larger than L2 (no flush)"},
+                       "l2": "state larger than L2 (no flush)",
+                       "hbm_used_gb": round(hbm_used_gb, 1)},
             "roofline": roof,
             "algorithmic_flops_per_cell_update": per_cell,
             "per_kernel": per_kernel,
