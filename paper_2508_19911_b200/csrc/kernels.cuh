@@ -678,17 +678,35 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
         }
       }
       const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);  // derivative along tA / tB flips that parity
+      // point g2 = (sA, sB) = (bit 0, bit 1) takes S0 + sA S1 + sB S2 + sA sB S3 = a_sA + sB b_sA with
+      // a+- = S0 +- S1, b+- = S2 +- S3 (8 additions for the 4 points), times chi = sA and / or sB for
+      // the transverse derivatives, applied as a sign-bit flip (integer pipe, no multiplication)
+      unsigned neg[NG];
 #pragma unroll
-      for (int g2 = 0; g2 < NG; ++g2) {
-        const double sA = (g2 & 1) ? 1.0 : -1.0, sB = (g2 & 2) ? 1.0 : -1.0;
-        const double chi = ((flip & 1) ? sA : 1.0) * ((flip & 2) ? sB : 1.0);
-        double* dst = xs + (lane - 2 * gp + 2 * g2);
+      for (int g2 = 0; g2 < NG; ++g2)
+        neg[g2] = (((flip & 1) && !(g2 & 1)) ? 1u : 0u) ^ (((flip & 2) && !(g2 & 2)) ? 1u : 0u);
 #pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          double val = S[v][0];
-          if (NG > 1) val = fma(sA, S[v][1], val);
-          if (NG > 2) val = fma(sB, S[v][2], fma(sA * sB, S[v][3], val));
-          dst[(q * 5 + v) * 128] = chi * val;
+      for (int v = 0; v < 5; ++v) {
+        double r[NG];
+        if constexpr (NG == 1) {
+          r[0] = S[v][0];
+        } else {
+          const double ap = S[v][0] + S[v][1], am = S[v][0] - S[v][1];
+          if constexpr (NG == 2) {
+            r[0] = am;
+            r[1] = ap;
+          } else {
+            const double bp = S[v][2] + S[v][3], bm = S[v][2] - S[v][3];
+            r[0] = am - bm;
+            r[1] = ap - bp;
+            r[2] = am + bm;
+            r[3] = ap + bp;
+          }
+        }
+#pragma unroll
+        for (int g2 = 0; g2 < NG; ++g2) {
+          const long long bits = __double_as_longlong(r[g2]) ^ ((long long)neg[g2] << 63);
+          xs[(lane - 2 * gp + 2 * g2) + (q * 5 + v) * 128] = __longlong_as_double(bits);
         }
       }
     }
