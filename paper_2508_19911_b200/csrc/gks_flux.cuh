@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <type_traits>
+
 #define HD __host__ __device__ __forceinline__
 
 namespace cgks {
@@ -557,6 +559,18 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const
     const T rC = fc.relax_C * jump;
     const T ee = (rC > 1.0 / 700.0) ? exp(-1.0 / fmax(rC, T(1.0 / 700.0))) : T(0.0);
     const T w = 1.0 - ee;
+#ifdef __CUDA_ARCH__
+    if constexpr (std::is_same<T, double>::value) {
+      if (__all_sync(0xffffffffu, ee == 0.0)) {  // smooth flow in the whole warp: the interface values
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          o.QLn[i] = acc[10 + i];
+          o.QLt[i] = acc[15 + i];
+        }
+        return good;
+      }
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       o.QLn[i] = w * acc[10 + i] + ee * Wown[i];
