@@ -488,6 +488,9 @@ struct XchgDev {
   __device__ __forceinline__ bool flag(bool b) const { return __shfl_xor_sync(0xffffffffu, (int)b, 1) != 0; }
 };
 
+#ifndef CGKS_FYZ
+#define CGKS_FYZ 4
+#endif
 #ifndef CGKS_FLUX_MINB
 #define CGKS_FLUX_MINB 3
 #endif
@@ -501,7 +504,7 @@ struct FluxTile {
   static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
   static constexpr int LPF = 2 * NG;                         // lanes per face
   static constexpr int FPB = 128 / LPF;                      // faces per block
-  static constexpr int FY = AX == 0 ? 1 : 4;                 // faces along the normal axis
+  static constexpr int FY = AX == 0 ? 1 : (AX == 2 ? CGKS_FYZ : 4);  // faces along the normal axis
   static constexpr int FX = FPB / FY;                        // faces along x
   // tile cells (x-faces: cells i0 - 2 .. i0 + FPB - 1, of which the first feeds no face: TMA rows
   // start at an even cell and span a multiple of 16 bytes)
