@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
   using RT = ReconTile<DIM>;
   constexpr int NCO = S::NB * 5;
   extern __shared__ double rsm[];
-  if (err->code) return;
+  if (__syncthreads_or(err->code != 0)) return;  // block-uniform (the staging pipeline synchronises)
   const int tx = threadIdx.x % RT::TX, ty = (threadIdx.x / RT::TX) % RT::TY, tz = threadIdx.x / (RT::TX * RT::TY);
   // block origin in the extended (reconstruction) index range
   const int x0 = blockIdx.x * RT::TX + c_geo.elo[0];
@@ -548,7 +548,9 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
   double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
   uint64_t* bar = reinterpret_cast<uint64_t*>(scratch + 20 * 128);  // TMA completion barrier
-  if (err->code) return;
+  // block-uniform early exit: the flag can be raised by another block while this one starts, and a
+  // thread that went on alone would wait on a barrier its thread 0 never initialised
+  if (__syncthreads_or(err->code != 0)) return;
   constexpr int FX = FT::FX, FY = FT::FY;
   const int fn0 = c_geo.fn[AX][0];
   // block origin: face (i0, j0, k0); y-/z-faces cover FY faces along their normal axis
@@ -991,7 +993,7 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV, TimeState* __restrict__ ts,
                                              ErrState* __restrict__ err) {
   __shared__ double red[8];
-  if (err->code) return;
+  if (__syncthreads_or(err->code != 0)) return;  // block-uniform (block reduction below)
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
   double cand = 1e300;

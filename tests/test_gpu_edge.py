@@ -88,3 +88,26 @@ def test_zero_steps_leave_the_state():
     t, steps, _ = S.get_time()
     S.close()
     assert steps == 0 and t == 0.0 and np.array_equal(Q, c.Q) and np.array_equal(G, c.G)
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_positivity_failure_in_large_run_is_clean(graph, monkeypatch):
+    """A positivity failure raised mid-kernel on a large grid (high-speed TGV 116^3 without the
+    collision-time jump term fails near step 470) is reported as CGKS_ERR_POSITIVITY with the state
+    of the last completed step -- blocks that start after the flag is raised exit as a whole (a
+    thread-divergent exit used to leave threads waiting on an uninitialised TMA barrier: launch
+    failure)."""
+    if not graph:
+        monkeypatch.setenv("CGKS_NO_GRAPH", "1")
+    from cgks_inputs import tgv_supersonic
+    Solver, CgksError = _S()
+    case = tgv_supersonic(116)
+    S = Solver.from_case(case, scheme=1, tau_C=0.0)
+    S.set_state(case.Q, case.G)
+    S.step(455)
+    with pytest.raises(CgksError) as e:
+        S.step(40)
+    assert e.value.code == 3, str(e.value)
+    Q, _ = S.get_state()
+    assert np.isfinite(Q).all() and Q[0].min() > 0
+    S.close()

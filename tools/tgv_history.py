@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--nonlinear", type=int, default=None)
     ap.add_argument("--t-end", type=float, default=1.0)
     ap.add_argument("--every", type=int, default=10)
+    ap.add_argument("--lines", type=int, default=0, help="CGKS-5th with line-averaged derivative DOFs (NEXT-1)")
+    ap.add_argument("--chi-c", type=float, default=None, help="GENO chi constant (reading R8; default 0.01)")
+    ap.add_argument("--param", action="append", default=[], help="scheme parameter override k=v (tau_C, relax_C, ...)")
     args = ap.parse_args()
     import torch
     from cgks_inputs import tgv, tgv_supersonic
@@ -41,7 +44,11 @@ def main():
     scheme = CGKS_CGKS5 if args.scheme == "cgks5" else CGKS_GKS2
     nl = case.nonlinear if args.nonlinear is None else args.nonlinear
     stream = torch.cuda.current_stream()
-    S = Solver.from_case(case, scheme=scheme, nonlinear=nl, stream=stream.cuda_stream)
+    kw = {} if args.chi_c is None else {"chi_c": args.chi_c}
+    for kv in args.param:
+        k, v = kv.split("=", 1)
+        kw[k] = float(v)
+    S = Solver.from_case(case, scheme=scheme, nonlinear=nl, stream=stream.cuda_stream, lines=args.lines, **kw)
     S.set_state(case.Q, case.G if scheme == CGKS_CGKS5 else None)
     ms = 0.0
     t = 0.0
@@ -58,7 +65,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         ms += e0.elapsed_time(e1)
-    print(json.dumps({"case": case.name, "n": args.n, "scheme": args.scheme, "nonlinear": nl, "t_end": t,
+    print(json.dumps({"case": case.name, "n": args.n, "scheme": args.scheme, "nonlinear": nl, "lines": args.lines,
+                      "chi_c": args.chi_c, "params": args.param, "t_end": t,
                       "steps": steps, "device_seconds_stepping": ms * 1e-3}), flush=True)
     S.close()
 
