@@ -824,6 +824,10 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0);
 int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
   if (!ctxs || n < 1 || nsteps < 0) return CGKS_ERR_CONFIG;
   cgks_ctx* c0 = ctxs[0];
+  if (c0 && c0->geo.stretched && n > 1) {  // one constant upload serves the group: per-rank width tables differ
+    set_msg(c0, "cgks_step_group: stretched meshes need one process per rank (NCCL), not an in-process group");
+    return CGKS_ERR_CONFIG;
+  }
   for (int r = 0; r < n; ++r) {
     if (!ctxs[r] || ctxs[r]->rank != r || ctxs[r]->nranks != n || ctxs[r]->comm_mode == 1 ||
         std::memcmp(&ctxs[r]->geo, &c0->geo, sizeof(Geo)) != 0 || ctxs[r]->device != c0->device ||

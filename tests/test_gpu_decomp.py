@@ -87,3 +87,16 @@ def test_single_step_refused_for_group_member():
     with pytest.raises(CgksError):
         S.step(1)
     S.close()
+
+
+def test_group_refuses_stretched_meshes():
+    from paper_2508_19911_b200 import CgksError, Solver, step_group
+    from cgks_inputs import stretched_nodes
+    case = random_smooth((8, 8, 8), seed=1)
+    nodes = (stretched_nodes(8, 0.0, 1.0, 0.2), None, None)
+    S = [Solver.from_case(case, scheme=1, nproc=(1, 1, 2), rank=r, nodes=nodes) for r in range(2)]
+    with pytest.raises(CgksError) as e:
+        step_group(S, 1)
+    assert e.value.code == 2 and "stretched" in str(e.value)
+    for s in S:
+        s.close()

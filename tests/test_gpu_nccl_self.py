@@ -52,3 +52,16 @@ def test_nccl_self_halo_lines_bitwise():
     Q1, G1, t1, L1 = _run(case, 1, 0, 3, False, L=L, **kw)
     Q2, G2, t2, L2 = _run(case, 1, 0, 3, True, L=L, **kw)
     assert t1 == t2 and np.array_equal(Q1, Q2) and np.array_equal(G1, G2) and np.array_equal(L1, L2)
+
+
+def test_nccl_self_halo_stretched_bitwise():
+    # stretched nodes on all three axes: the slab path's ghost-plane widths come from the global
+    # node arrays (periodic images), so the result equals the plain periodic context bit for bit
+    from cgks_inputs import stretched_nodes
+    case = random_smooth((16, 12, 10), seed=7, jump=0.3)
+    nodes = (stretched_nodes(16, case.lo[0], case.hi[0], 0.2), stretched_nodes(12, case.lo[1], case.hi[1], 0.15),
+             stretched_nodes(10, case.lo[2], case.hi[2], 0.25))
+    kw = dict(mu=1e-3, Pr=0.72, nodes=nodes)
+    Q1, G1, t1, _ = _run(case, 1, 1, 3, False, **kw)
+    Q2, G2, t2, _ = _run(case, 1, 1, 3, True, **kw)
+    assert t1 == t2 and np.array_equal(Q1, Q2) and np.array_equal(G1, G2)
