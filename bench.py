@@ -267,17 +267,38 @@ def run_ours(args, rank, ws, lr):
     Gh_pin = torch.from_numpy(Gh).pin_memory()
     Qo_pin = torch.empty(Qh.shape, dtype=torch.float64).pin_memory()
     Go_pin = torch.empty(Gh.shape, dtype=torch.float64).pin_memory()
-    e2e_steps = max(1, min(args.steps, 5))
+    # (a) the pipelined public calls: set_state_async / step_async / get_state_async, one cgks_sync at
+    # the end; every step still copies its whole input in and its whole result out, the copies run
+    # on the library's copy streams and overlap the neighbouring steps
+    e2e_steps = max(1, args.steps)
+    e2e_mode = "pipelined (cgks_set_state_async / cgks_step_async / cgks_get_state_async, copy streams)"
     torch.cuda.synchronize()
     barrier(ws)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    try:
+        for _ in range(e2e_steps):
+            S.set_state_async(Qh_pin, Gh_pin if scheme_id == 1 else None)
+            S.step_async(1)
+            S.get_state_async(Qo_pin, Go_pin if scheme_id == 1 else None)
+        S.sync()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
+    except Exception as ex:  # staging buffers do not fit next to a very large state: serial calls only
+        e2e_s, e2e_mode = None, f"serial only ({ex})"
+        S.sync()
+    # (b) the synchronous calls, one after the other (no overlap)
+    ser_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(ser_steps):
         S.set_state(Qh_pin.numpy(), Gh_pin.numpy() if scheme_id == 1 else None)
         S.step(1)
         S.get_state(Qo_pin.numpy(), Go_pin.numpy() if scheme_id == 1 else None, with_grad=scheme_id == 1)
     torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
-    e2e_val = cells * e2e_steps / e2e_s
+    ser_s = max_over_ranks(time.perf_counter() - t0, ws)
+    ser_val = cells * ser_steps / ser_s
+    e2e_val = cells * e2e_steps / e2e_s if e2e_s else ser_val
     nbytes = Qh.nbytes + (Gh.nbytes if scheme_id == 1 else 0)
 
     # roofline of the dominant kernel: per-kernel CUDA-event durations on the library stream
@@ -337,7 +358,9 @@ def run_ours(args, rank, ws, lr):
             "per_kernel": per_kernel,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_val, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes,
-                    "d2h_bytes_per_step": nbytes},
+                    "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "mode": e2e_mode,
+                    "serial_value": ser_val, "serial_steps": ser_steps,
+                    "host_buffers": "pinned (torch pin_memory)"},
             "gpu_launches": S.launches_per_step() * args.steps if S.ctx else None}
     line["gpu_launches"] = int(sum(v[1] for v in prof.values()) / max(2, min(args.steps, 4)) * args.steps)
     if not args.no_cpu_baseline and ws == 1:

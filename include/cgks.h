@@ -148,6 +148,21 @@ int cgks_step(cgks_ctx* ctx, int nsteps);
 /* Copy the state out (user layout).  gradQ may be NULL. */
 int cgks_get_state(const cgks_ctx* ctx, double* Q, double* gradQ);
 
+/* Asynchronous variants (pipelined host I/O): they enqueue and return.  set_state_async copies host
+ * inputs on an input copy stream into a staging buffer and converts them on the compute stream;
+ * get_state_async converts on the compute stream and copies out on an output copy stream; both
+ * wait for the previous use of their staging buffer, so set_state_async(n+1) overlaps step(n) and
+ * get_state_async(n) overlaps step(n+1).  Host buffers must stay valid and unmodified (inputs) or
+ * unread (outputs) until cgks_sync; pinned host memory makes the copies truly asynchronous.
+ * cgks_step_async defers its error check to cgks_sync, which waits for everything enqueued and
+ * returns what cgks_step would have returned (the state is then the last completed step).  Every
+ * synchronous call first performs cgks_sync.  The staging buffers (2 x 160 B per cell) are
+ * allocated on first use; CGKS_ERR_CUDA if they do not fit. */
+int cgks_set_state_async(cgks_ctx* ctx, const double* Q, const double* gradQ);
+int cgks_step_async(cgks_ctx* ctx, int nsteps);
+int cgks_get_state_async(const cgks_ctx* ctx, double* Q, double* gradQ);
+int cgks_sync(cgks_ctx* ctx);
+
 /* Simulated time, completed steps, and the last time step used. */
 int cgks_get_time(const cgks_ctx* ctx, double* t, int64_t* steps, double* last_dt);
 

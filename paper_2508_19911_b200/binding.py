@@ -62,7 +62,7 @@ _lib = None
 EXPORTS = ["cgks_scheme_defaults", "cgks_create", "cgks_local_extent", "cgks_set_state", "cgks_step",
            "cgks_get_state", "cgks_get_time", "cgks_last_error", "cgks_launches_per_step", "cgks_profile",
            "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group",
-           "cgks_destroy"]
+           "cgks_set_state_async", "cgks_step_async", "cgks_get_state_async", "cgks_sync", "cgks_destroy"]
 
 
 def load(path: str = LIB_PATH):
@@ -82,6 +82,10 @@ def load(path: str = LIB_PATH):
     L.cgks_set_state.argtypes = [vp, vp, vp]
     L.cgks_step.argtypes = [vp, ctypes.c_int]
     L.cgks_get_state.argtypes = [vp, vp, vp]
+    L.cgks_set_state_async.argtypes = [vp, vp, vp]
+    L.cgks_step_async.argtypes = [vp, ctypes.c_int]
+    L.cgks_get_state_async.argtypes = [vp, vp, vp]
+    L.cgks_sync.argtypes = [vp]
     L.cgks_get_time.argtypes = [vp, dp, ctypes.POINTER(ctypes.c_int64), dp]
     L.cgks_diagnostics.argtypes = [vp, dp]
     L.cgks_set_lines.argtypes = [vp, vp]
@@ -213,6 +217,7 @@ class Solver:
             raise CgksError(rc, "cgks_create failed (see stderr)")
         self._L = L
         self.ctx = ctx
+        self._async_refs = []
         self.n = tuple(int(x) for x in n)
         self.scheme = scheme
 
@@ -247,6 +252,24 @@ class Solver:
             G = np.zeros((3, 5) + shp)
         self._check(self._L.cgks_get_state(self.ctx, _ptr(Q), _ptr(G)))
         return Q, G
+
+    # -- asynchronous host I/O (cgks_*_async, cgks_sync): the arrays are kept alive until sync()
+    def set_state_async(self, Q, G=None):
+        self._async_refs.append((Q, G))
+        self._check(self._L.cgks_set_state_async(self.ctx, _ptr(Q), _ptr(G)))
+
+    def step_async(self, nsteps=1):
+        self._check(self._L.cgks_step_async(self.ctx, int(nsteps)))
+
+    def get_state_async(self, Q, G=None):
+        """Enqueue the copy-out into the caller's buffers (valid after sync())."""
+        self._async_refs.append((Q, G))
+        self._check(self._L.cgks_get_state_async(self.ctx, _ptr(Q), _ptr(G)))
+
+    def sync(self):
+        rc = self._L.cgks_sync(self.ctx)
+        self._async_refs.clear()
+        self._check(rc)
 
     def get_time(self):
         t = ctypes.c_double()

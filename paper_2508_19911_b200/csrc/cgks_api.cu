@@ -143,6 +143,19 @@ struct cgks_ctx {
   bool overlap = false;
   cudaStream_t halo_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // asynchronous host I/O (cgks_set_state_async / cgks_step_async / cgks_get_state_async / cgks_sync):
+  // staging buffers of the 20 user-layout fields, one copy stream per direction, ordering events
+  double* stage_in = nullptr;
+  double* stage_out = nullptr;
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t ev_in_free = nullptr, ev_in_ready = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
+  bool async_pending = false;     // work enqueued by the async calls, not yet synchronised
+  bool async_steps = false;       // ... including steps whose errors cgks_sync reports
+  int async_cur0 = 0;             // buffer index and step count before the first deferred step
+  long long async_steps0 = 0;
+  long long host_steps = 0;       // steps completed or enqueued since cgks_set_state(_async)
+  TimeState* ts0 = nullptr;       // device copy of the reset time state (a pageable source would
+                                  // make the async reset wait for the compute stream)
 };
 
 static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
@@ -933,8 +946,14 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+extern "C" int cgks_sync(cgks_ctx* ctx);
+// the synchronous calls first complete (and report) what the asynchronous ones enqueued
+static int drain_async(cgks_ctx* ctx) { return ctx->async_pending ? cgks_sync(ctx) : CGKS_OK; }
+
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
+  ctx->host_steps = 0;
   int rc = upload_constants(ctx);
   if (rc) return rc;
   const long long nc = ctx->ncell;
@@ -976,6 +995,7 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
 
 int cgks_set_lines(cgks_ctx* ctx, const double* L) {
   if (!ctx || !L) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   if (!ctx->lines) {
     set_msg(ctx, "cgks_set_lines: the context has no line DOFs (scheme.lines = 0)");
     return CGKS_ERR_CONFIG;
@@ -997,6 +1017,7 @@ int cgks_set_lines(cgks_ctx* ctx, const double* L) {
 int cgks_get_lines(const cgks_ctx* cctx, double* L) {
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx || !L) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   if (!ctx->lines) return CGKS_ERR_CONFIG;
   int rc = upload_constants(ctx);
   if (rc) return rc;
@@ -1016,6 +1037,7 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0) {
   CK(cudaMemcpyAsync(&e, ctx->err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->host_steps = t.steps;
   if (e.code) {
     // kernels after the failure were no-ops; the last completed step sits in the input buffer of step e.step
     long long done = t.steps - steps0;
@@ -1058,6 +1080,7 @@ static int capture_step(cgks_ctx* ctx, int c) {
 
 int cgks_step(cgks_ctx* ctx, int nsteps) {
   if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   if (ctx->comm_mode == 2) {
     set_msg(ctx, "context belongs to an in-process decomposition: use cgks_step_group");
     return CGKS_ERR_CONFIG;
@@ -1087,6 +1110,7 @@ int cgks_step(cgks_ctx* ctx, int nsteps) {
 int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   int rc = upload_constants(ctx);
   if (rc) return rc;
   const long long nc = ctx->ncell;
@@ -1116,9 +1140,145 @@ int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
   return CGKS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Asynchronous host I/O: copies on their own streams, ordered against the compute stream by
+// events, so a pipeline of set_state_async / step_async / get_state_async overlaps the input copy
+// of the next state and the output copy of the previous one with the current steps.
+// ---------------------------------------------------------------------------
+static int ensure_async(cgks_ctx* ctx) {
+  if (ctx->cin) return CGKS_OK;
+  const size_t bytes = sizeof(double) * (size_t)ctx->ncell * 20;
+  if (cudaMalloc((void**)&ctx->stage_in, bytes) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->stage_out, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    set_msg(ctx, "asynchronous staging buffers (2 x %zu bytes) do not fit", bytes);
+    return CGKS_ERR_CUDA;
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->cin, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->cout, cudaStreamNonBlocking));
+  for (cudaEvent_t* ev : {&ctx->ev_in_free, &ctx->ev_in_ready, &ctx->ev_out_ready, &ctx->ev_out_free})
+    CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->ev_in_free, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_out_free, ctx->stream));
+  TimeState t0;
+  std::memset(&t0, 0, sizeof(TimeState));
+  const double big = 1e300;
+  std::memcpy(&t0.dtmin_bits, &big, sizeof(big));
+  CK(cudaMalloc((void**)&ctx->ts0, sizeof(TimeState)));
+  CK(cudaMemcpy(ctx->ts0, &t0, sizeof(TimeState), cudaMemcpyHostToDevice));
+  return CGKS_OK;
+}
+
+int cgks_set_state_async(cgks_ctx* ctx, const double* Q, const double* gradQ) {
+  if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  if (ctx->comm_mode == 2) return cgks_set_state(ctx, Q, gradQ);
+  int rc = upload_constants(ctx);
+  if (!rc) rc = ensure_async(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  const int ng = ctx->NV == 20 ? 15 : 0;
+  const bool dq = is_device_ptr(Q), dg = gradQ && is_device_ptr(gradQ);
+  // host inputs: copy into stage_in once the previous upload has been consumed
+  CK(cudaStreamWaitEvent(ctx->cin, ctx->ev_in_free, 0));
+  if (!dq) CK(cudaMemcpyAsync(ctx->stage_in, Q, sizeof(double) * nc * 5, cudaMemcpyHostToDevice, ctx->cin));
+  if (ng && gradQ && !dg)
+    CK(cudaMemcpyAsync(ctx->stage_in + nc * 5, gradQ, sizeof(double) * nc * ng, cudaMemcpyHostToDevice, ctx->cin));
+  CK(cudaEventRecord(ctx->ev_in_ready, ctx->cin));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready, 0));
+  double* U = ctx->U[0];
+  ctx->cur = 0;
+  if (ctx->ops->pack(ctx->stream, dq ? Q : ctx->stage_in, U, ctx->NV, 0, 5, nc)) CK(cudaGetLastError());
+  if (ng && ctx->ops->pack(ctx->stream, gradQ ? (dg ? gradQ : ctx->stage_in + nc * 5) : nullptr, U, ctx->NV, 5, ng, nc))
+    CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_in_free, ctx->stream));
+  if (ctx->lines && ctx->ops->lines_init(ctx->stream, U, ctx->Lb[0], nc)) CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->ts, ctx->ts0, sizeof(TimeState), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->err, 0, sizeof(ErrState), ctx->stream));
+  ctx->host_steps = 0;
+  ctx->async_pending = true;
+  return CGKS_OK;
+}
+
+int cgks_step_async(cgks_ctx* ctx, int nsteps) {
+  if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
+  if (ctx->comm_mode == 2) {
+    set_msg(ctx, "context belongs to an in-process decomposition: use cgks_step_group");
+    return CGKS_ERR_CONFIG;
+  }
+  int rc = upload_constants(ctx);
+  if (rc) return rc;
+  if (!ctx->async_steps) {
+    ctx->async_cur0 = ctx->cur;
+    ctx->async_steps0 = ctx->host_steps;
+  }
+  if (ctx->use_graph && nsteps > 0) {
+    for (int c = 0; c < 2 && ctx->use_graph; ++c)
+      if (!ctx->graph[c] && capture_step(ctx, c)) ctx->use_graph = false;
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    if (ctx->use_graph) {
+      CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
+      ctx->cur = 1 - ctx->cur;
+    } else {
+      rc = one_step(ctx);
+      if (rc) return rc;
+    }
+  }
+  ctx->host_steps += nsteps;
+  ctx->async_steps = ctx->async_steps || nsteps > 0;
+  ctx->async_pending = true;
+  return CGKS_OK;
+}
+
+int cgks_get_state_async(const cgks_ctx* cctx, double* Q, double* gradQ) {
+  cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
+  if (!ctx || !Q) return CGKS_ERR_CONFIG;
+  int rc = upload_constants(ctx);
+  if (!rc) rc = ensure_async(ctx);
+  if (rc) return rc;
+  const long long nc = ctx->ncell;
+  const int ng = ctx->NV == 20 ? 15 : 0;
+  const bool dq = is_device_ptr(Q), dg = gradQ && is_device_ptr(gradQ);
+  const double* U = ctx->U[ctx->cur];
+  // stage_out is refilled once the previous download has drained it
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_out_free, 0));
+  if (ctx->ops->unpack(ctx->stream, U, dq ? Q : ctx->stage_out, ctx->NV, 0, 5, nc)) CK(cudaGetLastError());
+  if (gradQ && ng &&
+      ctx->ops->unpack(ctx->stream, U, dg ? gradQ : ctx->stage_out + nc * 5, ctx->NV, 5, ng, nc))
+    CK(cudaGetLastError());
+  if (gradQ && !ng) {
+    if (dg)
+      CK(cudaMemsetAsync(gradQ, 0, sizeof(double) * nc * 15, ctx->stream));
+    else
+      std::memset(gradQ, 0, sizeof(double) * nc * 15);
+  }
+  CK(cudaEventRecord(ctx->ev_out_ready, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->cout, ctx->ev_out_ready, 0));
+  if (!dq) CK(cudaMemcpyAsync(Q, ctx->stage_out, sizeof(double) * nc * 5, cudaMemcpyDeviceToHost, ctx->cout));
+  if (gradQ && ng && !dg)
+    CK(cudaMemcpyAsync(gradQ, ctx->stage_out + nc * 5, sizeof(double) * nc * ng, cudaMemcpyDeviceToHost, ctx->cout));
+  CK(cudaEventRecord(ctx->ev_out_free, ctx->cout));
+  ctx->async_pending = true;
+  return CGKS_OK;
+}
+
+int cgks_sync(cgks_ctx* ctx) {
+  if (!ctx) return CGKS_ERR_CONFIG;
+  if (ctx->cin) CK(cudaStreamSynchronize(ctx->cin));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->cout) CK(cudaStreamSynchronize(ctx->cout));
+  ctx->async_pending = false;
+  if (ctx->async_steps) {
+    ctx->async_steps = false;
+    return finish_steps(ctx, ctx->async_cur0, ctx->async_steps0);
+  }
+  return CGKS_OK;
+}
+
 int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_dt) {
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   TimeState ts;
   CK(cudaMemcpy(&ts, ctx->ts, sizeof(ts), cudaMemcpyDeviceToHost));
   if (t) *t = ts.t;
@@ -1129,6 +1289,7 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
     set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
@@ -1169,6 +1330,7 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
     set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
@@ -1379,6 +1541,13 @@ void cgks_destroy(cgks_ctx* ctx) {
     if (ctx->graph[c]) cudaGraphExecDestroy(ctx->graph[c]);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
+  if (ctx->cin) cudaStreamDestroy(ctx->cin);
+  if (ctx->cout) cudaStreamDestroy(ctx->cout);
+  for (cudaEvent_t ev : {ctx->ev_in_free, ctx->ev_in_ready, ctx->ev_out_ready, ctx->ev_out_free})
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stage_in) cudaFree(ctx->stage_in);
+  if (ctx->stage_out) cudaFree(ctx->stage_out);
+  if (ctx->ts0) cudaFree(ctx->ts0);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
