@@ -1,0 +1,53 @@
+"""Host-side tools: the equal-resolution comparison (tools/tgv_compare.py) and the bench workload
+names (bench.make_case)."""
+import json
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _write(path, ts, ek, es, meta):
+    with open(path, "w") as f:
+        for t, a, b in zip(ts, ek, es):
+            f.write(json.dumps({"t": t, "steps": 0, "E_k": a, "eps_S": b, "eps_D": 0.0, "eps_T": b}) + "\n")
+        f.write(json.dumps(meta) + "\n")
+
+
+def test_tgv_compare_deviations_and_svg(tmp_path):
+    t = np.linspace(0.0, 10.0, 101)
+    ek = 0.125 * np.exp(-0.2 * t)
+    es = 0.01 * np.sin(np.pi * t / 10.0) + 0.001
+    ref = tmp_path / "ref.jsonl"
+    run = tmp_path / "run.jsonl"
+    _write(ref, t, ek, es, {"scheme": "cgks5", "n": 64, "device_seconds_stepping": 10.0, "steps": 100})
+    t2 = np.linspace(0.0, 10.0, 37)  # other sample times: the reference is interpolated
+    _write(run, t2, np.interp(t2, t, ek) * 1.02, np.interp(t2, t, es) - 0.001,
+           {"scheme": "gks2", "n": 128, "device_seconds_stepping": 25.0, "steps": 300})
+    svg = tmp_path / "h.svg"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tgv_compare.py"), str(ref), str(run),
+                          "--svg", str(svg)], capture_output=True, text=True, check=True).stdout
+    d = json.loads(out)
+    r = d["runs"][0]
+    assert r["run"] == "GKS-2nd 128^3" and d["reference"]["run"] == "CGKS-5th 64^3"
+    assert r["E_k_max_abs_dev_rel"] == pytest.approx(0.02, rel=1e-3)  # 2 % of E_k(0) = max E_k
+    assert r["eps_S_max_abs_dev_rel"] == pytest.approx(0.001 / es.max(), rel=1e-6)
+    assert r["time_ratio_to_first_run"] == 1.0 and r["device_seconds"] == 25.0
+    root = ET.parse(svg).getroot()
+    assert sum(1 for e in root.iter() if e.tag.endswith("polyline")) == 4  # 2 runs x 2 panels
+
+
+def test_bench_workload_names():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.make_case("tgv24").n == (24, 24, 24)
+    c = bench.make_case("tgv_ss12")
+    assert c.n == (12, 12, 12) and c.sutherland_S > 0 and c.nonlinear
+    assert bench.make_case("hit16").n == (16, 16, 16)
+    with pytest.raises(ValueError):
+        bench.make_case("tgv")
