@@ -65,3 +65,22 @@ def test_nccl_self_halo_stretched_bitwise():
     Q1, G1, t1, _ = _run(case, 1, 1, 3, False, **kw)
     Q2, G2, t2, _ = _run(case, 1, 1, 3, True, **kw)
     assert t1 == t2 and np.array_equal(Q1, Q2) and np.array_equal(G1, G2)
+
+
+def test_nccl_self_halo_async_pipeline():
+    # the asynchronous calls on the NCCL slab path (exchange on the halo stream, copies on the copy
+    # streams) give the synchronous results bit for bit
+    import torch
+    from paper_2508_19911_b200 import Solver, nccl_unique_id
+    case = random_smooth((16, 12, 10), seed=5, jump=0.3)
+    kw = dict(mu=1e-3, Pr=0.72)
+    Q1, G1, _, _ = _run(case, 1, 1, 4, False, **kw)
+    S = Solver.from_case(case, scheme=1, nonlinear=1, nccl_id=nccl_unique_id(), **kw)
+    qi, gi = torch.from_numpy(case.Q).pin_memory(), torch.from_numpy(case.G).pin_memory()
+    qo, go = torch.zeros_like(qi).pin_memory(), torch.zeros_like(gi).pin_memory()
+    S.set_state_async(qi, gi)
+    S.step_async(4)
+    S.get_state_async(qo, go)
+    S.sync()
+    S.close()
+    assert np.array_equal(qo.numpy(), Q1) and np.array_equal(go.numpy(), G1)
