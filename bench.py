@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -32,6 +33,16 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "CGKS-5th FP64 cell-updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline"
+
+
+def slab512(ws, rank):
+    """BASELINE configs[4] per-GPU block: 512 x 512 x 64 planes of the 512^3 TGV,
+    z-planes [64 rank, 64 rank + 64); N ranks hold a 512 x 512 x 64N grid (N = 8: the 512^3 run)."""
+    from cgks_inputs import tgv
+    c = tgv(512, z0=64 * rank, nzb=64)
+    c.n = (512, 512, 64 * ws)
+    c.hi = (c.hi[0], c.hi[1], c.lo[2] + 2 * math.pi * 64 * ws / 512)
+    return c
 
 
 def make_case(name):
@@ -201,14 +212,17 @@ def run_ours(args, rank, ws, lr):
     if ws > 1:
         # weak scaling (BASELINE configs[4] strategy): each GPU owns a 128^3 z-slab of the TGV on
         # [-pi,pi]^2 x [-pi, -pi + 2 pi N]; halo exchange and dt allreduce over NCCL inside cgks_step
-        if not args.workload.startswith("tgv"):
+        if not args.workload.startswith("tgv") or args.workload.startswith("tgv_ss"):
             raise SystemExit("multi-GPU runs use the TGV workload")
         import torch.distributed as dist
 
         from cgks_inputs import tgv
         from paper_2508_19911_b200 import nccl_unique_id
-        nb = int(args.workload[3:])
-        case = tgv(nb, zrep=ws, z0=rank * nb, nzb=nb)
+        if args.workload == "tgv512slab":
+            case = slab512(ws, rank)
+        else:
+            nb = int(args.workload[3:])
+            case = tgv(nb, zrep=ws, z0=rank * nb, nzb=nb)
         if args.nonlinear is not None:
             case.nonlinear = args.nonlinear
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -216,7 +230,11 @@ def run_ours(args, rank, ws, lr):
         S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, nproc=(1, 1, ws), rank=rank,
                              nccl_id=obj[0])
     else:
-        case = make_case(args.workload)
+        if args.workload == "tgv512slab":  # the block of one rank of the 512^3 run, with the periodic self halo
+            case = slab512(1, 0)
+            args.nccl_self = True
+        else:
+            case = make_case(args.workload)
         if args.nonlinear is not None:
             case.nonlinear = args.nonlinear
         nodes = None

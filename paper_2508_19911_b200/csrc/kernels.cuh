@@ -108,7 +108,9 @@ __device__ __forceinline__ double ld_state(const double* __restrict__ U, int NV,
   return __ldg(U + sidx(NV, f, idx[0], idx[1], idx[2]));
 }
 
-// index into an extended-range per-cell buffer (coefficients / slopes)
+// index into an extended-range per-cell buffer (coefficients / slopes), layout [z][y][field][x]:
+// the NF fields of one x-row are contiguous (field stride en0), so a tile of a few rows spans a few
+// contiguous blocks instead of one memory page per field and plane
 __device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
   // periodic axes wrap; bounded axes are stored from elo = -1
   int ii = c_geo.bounded[0] ? i : wrapi(i, c_geo.n[0]);
@@ -117,7 +119,7 @@ __device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
   ii -= c_geo.elo[0];
   jj -= c_geo.elo[1];
   kk -= c_geo.elo[2];
-  return ((long long)kk * NF + f) * c_geo.eplane + (long long)jj * c_geo.en[0] + ii;
+  return (((long long)kk * c_geo.en[1] + jj) * NF + f) * c_geo.en[0] + ii;
 }
 
 // stretched meshes (R37): width / inverse width of cell index c along a (c in -2 .. n+1)
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
   }
   // coefficient q of component v at cb[(q * 5 + v) * eplane]
   double* cb = coef + (valid ? eidx(NCO, 0, i, j, k) : 0);
-  const long long ep = c_geo.eplane;
+  const long long ep = c_geo.en[0];  // field stride
   recon_stage<DIM, BOX>(U, rsm, 0, x0, y0, z0, map);
 #pragma unroll 1
   for (int v = 0; v < 5; ++v) {
@@ -519,13 +521,17 @@ struct FluxTile {
   // and conflict-free across the 8 rows a warp reads
   static constexpr int TS = ((NB / 2) % 2 == 1) ? NB : NB + 2;
   static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
-  // Tile layout = the TMA box layout of the [z][field][y][x] arrays: reconstruction fields, then the
-  // cell averages.  x- and y-faces: [field][cell] (field stride NT); z-faces: [cz][field][cx]
-  // (field stride FX).  cbase(c) = offset of cell c = (normal index) * TX + x index.
-  static constexpr int FS = AX == 2 ? FX : NT;
+  // Tile layout = the TMA box layouts: reconstruction fields, then the cell averages; cell c =
+  // (normal index) * TX + x index.
+  // reconstruction fields ([z][y][field][x] arrays): x-faces [field][cell], y- and z-faces
+  // [normal index][field][x index] (field stride FX); cell averages ([z][field][y][x] arrays): x- and
+  // y-faces [field][cell] (field stride NT), z-faces [cz][field][cx]
+  static constexpr int FS = AX == 0 ? NT : FX;
   __host__ __device__ static constexpr int cbase(int c, int nfield) {
-    return AX == 2 ? (c / FX) * nfield * FX + c % FX : c;
+    return AX == 0 ? c : (c / FX) * nfield * FX + c % FX;
   }
+  static constexpr int FSU = AX == 2 ? FX : NT;
+  __host__ __device__ static constexpr int cbaseU(int c) { return AX == 2 ? (c / FX) * 5 * FX + c % FX : c; }
   static constexpr int STILE = (NREC * NT + 15) / 16 * 16;   // start of the cell-average tile (128-byte aligned)
   // the tile region is reused for parking slots 20..39 after the evaluation
   static constexpr int TILE = STILE + 5 * NT > 20 * 128 ? STILE + 5 * NT : 20 * 128;
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     if (threadIdx.x == 0) {
       mbar_init(bar, 1);
       mbar_expect_tx(bar, (unsigned)(sizeof(double) * (FT::NREC + 5) * NT));
-      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], y0 - c_geo.elo[1], 0, z0 - c_geo.elo[2]);
+      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2]);  // (x, field, y, z)
       tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
     }
   } else {
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
         const int kmax = c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0);
         if (ck > kmax) ck = kmax;
       }
-      const long long st = c_geo.eplane;
+      const long long st = c_geo.en[0];  // field stride of the reconstruction array
       // asynchronous global -> shared copies (LDGSTS): all in flight at once; running addresses
       const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
       unsigned dst = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NREC) + fsub * FT::FS);
@@ -610,12 +616,12 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
         src += TPC * st;
         dst += TPC * FT::FS * (unsigned)sizeof(double);
       }
-      double* sdst = tile + FT::STILE + FT::cbase(c, 5);
+      double* sdst = tile + FT::STILE + FT::cbaseU(c);
       if (BOX) {
-        for (int v = fsub; v < 5; v += TPC) sdst[v * FT::FS] = ld_state<BOX>(U, NV, v, ci, cj, ck);
+        for (int v = fsub; v < 5; v += TPC) sdst[v * FT::FSU] = ld_state<BOX>(U, NV, v, ci, cj, ck);
       } else {
         const double* ub = U + sidx(NV, 0, wrap_ax(0, ci), wrap_ax(1, cj), wrap_ax(2, ck));
-        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FS, ub + v * c_geo.plane);
+        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FSU, ub + v * c_geo.plane);
       }
     }
   }
@@ -639,7 +645,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   // tile column of this lane's cell
   const int c = AX == 0 ? fl + side + 1 : (fy + side) * FX + fx;
   const double* tc = tile + FT::cbase(c, FT::NREC);           // field f at tc[f * FS]
-  const double* sc = tile + FT::STILE + FT::cbase(c, 5);      // cell average v at sc[v * FS]
+  const double* sc = tile + FT::STILE + FT::cbaseU(c);        // cell average v at sc[v * FSU]
 
   // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)
   constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
@@ -719,7 +725,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     double W[5], dW[NQ][5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      W[v] = sc[v * FT::FS] + xs[v * 128 + lane];
+      W[v] = sc[v * FT::FSU] + xs[v * 128 + lane];
 #pragma unroll
       for (int q = 1; q < NQ; ++q) dW[q][v] = xs[(q * 5 + v) * 128 + lane];
     }
@@ -748,7 +754,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
     const double hs = side ? -0.5 : 0.5;
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      const double q = sc[v * FT::FS];
+      const double q = sc[v * FT::FSU];
       W[v] = q + hs * tc[(AX * 5 + v) * FT::FS];
 #pragma unroll
       for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * FT::FS] * (STR ? ihc[a] : c_geo.ih[a]);
@@ -1129,7 +1135,7 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
     double W[5], dW[3][5];
     if (COMPACT) {
       const double* cb = rec + eidx(NB * 5, 0, i, j, k);
-      const long long ep = c_geo.eplane;
+      const long long ep = c_geo.en[0];  // field stride
       const double* wv = wt + p * 4 * NB;
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
