@@ -84,7 +84,7 @@ typedef struct {
                        /* (S = 0.4042); used in the collision time and the viscous dt bound */
   int lines;           /* CGKS-5th: 1 = line-averaged derivatives of the own cell as reconstruction data  */
                        /* (SURVEY 8(f) NEXT-1), carried as extra DOFs per cell;    */
-                       /* 0 = the cell-averaged gradient (R1, default).  Single-rank contexts only.      */
+                       /* 0 = the cell-averaged gradient (R1, default).                                  */
 } cgks_scheme;
 
 /* Fill a cgks_scheme with the paper defaults for scheme id (CGKS_GKS2 / CGKS_CGKS5). */
@@ -95,7 +95,9 @@ void cgks_scheme_defaults(int id, cgks_scheme* s);
  * (mu == 0: inviscid collision time P:344); Pr > 0 the Prandtl number (R20).
  * Builds the CGKS-5th constrained-least-squares matrix (R1-R4) on the
  * host in long double and checks its rank (CGKS_ERR_CONFIG when deficient).
- * Allocates all device memory on the current device.  *out is NULL on failure.
+ * Allocates all device memory on the current device, which the context keeps: every later call
+ * on it makes that device current for its duration (and restores the caller's), so contexts on
+ * different GPUs can be used from one thread.  *out is NULL on failure.
  */
 int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const cgks_scheme* scheme,
                 cgks_ctx** out);

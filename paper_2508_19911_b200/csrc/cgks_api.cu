@@ -158,7 +158,24 @@ struct cgks_ctx {
                                   // make the async reset wait for the compute stream)
 };
 
-static cgks_ctx* g_const_owner = nullptr;  // context whose parameters are in constant memory
+// context whose parameters are in the constant memory, per device (each context runs on the device
+// current at its creation; every entry point makes that device current for its duration)
+static const int kMaxDev = 64;
+static cgks_ctx* g_owner[kMaxDev] = {nullptr};
+
+// makes the context's device current for the duration of an entry point (restores the caller's)
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const cgks_ctx* c);
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+DevGuard::DevGuard(const cgks_ctx* c) {
+  int cur = 0;
+  if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+}
 
 static void set_msg(cgks_ctx* c, const char* fmt, ...) {
   if (!c) return;
@@ -179,12 +196,13 @@ static void set_msg(cgks_ctx* c, const char* fmt, ...) {
   } while (0)
 
 static int upload_constants(cgks_ctx* ctx) {
-  if (g_const_owner == ctx) return CGKS_OK;
+  cgks_ctx*& owner = g_owner[ctx->device & (kMaxDev - 1)];
+  if (owner == ctx) return CGKS_OK;
   if (ctx->ops->upload(ctx->geo, ctx->fc, ctx->Rp, ctx->scheme_id == CGKS_CGKS5 ? ctx->nnz : 0, ctx->stream)) {
     set_msg(ctx, "constant upload failed: %s", cudaGetErrorString(cudaGetLastError()));
     return CGKS_ERR_CUDA;
   }
-  g_const_owner = ctx;
+  owner = ctx;
   return CGKS_OK;
 }
 
@@ -837,6 +855,7 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0);
 // In-process group of slab contexts on one device, stepped in lock-step: one shared time state,
 // all work on the first context's stream, halos copied between the contexts' buffers.
 int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
+  DevGuard dg_(ctxs && n > 0 ? ctxs[0] : nullptr);
   if (!ctxs || n < 1 || nsteps < 0) return CGKS_ERR_CONFIG;
   cgks_ctx* c0 = ctxs[0];
   if (c0 && c0->geo.stretched && n > 1) {  // one constant upload serves the group: per-rank width tables differ
@@ -865,7 +884,7 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
     ctxs[r]->stream = c0->stream;
     ctxs[r]->ts = c0->ts;
     ctxs[r]->err = c0->err;
-    g_const_owner = c0;  // identical geometry: one upload serves all
+    g_owner[c0->device & (kMaxDev - 1)] = c0;  // identical geometry: one upload serves all
   }
   TimeState t;
   CK(cudaMemcpyAsync(&t, c0->ts, sizeof(t), cudaMemcpyDeviceToHost, c0->stream));
@@ -953,6 +972,7 @@ extern "C" int cgks_sync(cgks_ctx* ctx);
 static int drain_async(cgks_ctx* ctx) { return ctx->async_pending ? cgks_sync(ctx) : CGKS_OK; }
 
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
+  DevGuard dg_(ctx);
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   ctx->host_steps = 0;
@@ -996,6 +1016,7 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
 }
 
 int cgks_set_lines(cgks_ctx* ctx, const double* L) {
+  DevGuard dg_(ctx);
   if (!ctx || !L) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (!ctx->lines) {
@@ -1017,6 +1038,7 @@ int cgks_set_lines(cgks_ctx* ctx, const double* L) {
 }
 
 int cgks_get_lines(const cgks_ctx* cctx, double* L) {
+  DevGuard dg_(cctx);
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx || !L) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
@@ -1081,6 +1103,7 @@ static int capture_step(cgks_ctx* ctx, int c) {
 }
 
 int cgks_step(cgks_ctx* ctx, int nsteps) {
+  DevGuard dg_(ctx);
   if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (ctx->comm_mode == 2) {
@@ -1110,6 +1133,7 @@ int cgks_step(cgks_ctx* ctx, int nsteps) {
 }
 
 int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
+  DevGuard dg_(cctx);
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
@@ -1172,6 +1196,7 @@ static int ensure_async(cgks_ctx* ctx) {
 }
 
 int cgks_set_state_async(cgks_ctx* ctx, const double* Q, const double* gradQ) {
+  DevGuard dg_(ctx);
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
   if (ctx->comm_mode == 2) return cgks_set_state(ctx, Q, gradQ);
   int rc = upload_constants(ctx);
@@ -1202,6 +1227,7 @@ int cgks_set_state_async(cgks_ctx* ctx, const double* Q, const double* gradQ) {
 }
 
 int cgks_step_async(cgks_ctx* ctx, int nsteps) {
+  DevGuard dg_(ctx);
   if (!ctx || nsteps < 0) return CGKS_ERR_CONFIG;
   if (ctx->comm_mode == 2) {
     set_msg(ctx, "context belongs to an in-process decomposition: use cgks_step_group");
@@ -1233,6 +1259,7 @@ int cgks_step_async(cgks_ctx* ctx, int nsteps) {
 }
 
 int cgks_get_state_async(const cgks_ctx* cctx, double* Q, double* gradQ) {
+  DevGuard dg_(cctx);
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx || !Q) return CGKS_ERR_CONFIG;
   int rc = upload_constants(ctx);
@@ -1265,6 +1292,7 @@ int cgks_get_state_async(const cgks_ctx* cctx, double* Q, double* gradQ) {
 }
 
 int cgks_sync(cgks_ctx* ctx) {
+  DevGuard dg_(ctx);
   if (!ctx) return CGKS_ERR_CONFIG;
   if (ctx->cin) CK(cudaStreamSynchronize(ctx->cin));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1278,6 +1306,7 @@ int cgks_sync(cgks_ctx* ctx) {
 }
 
 int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_dt) {
+  DevGuard dg_(cctx);
   cgks_ctx* ctx = const_cast<cgks_ctx*>(cctx);
   if (!ctx) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
@@ -1290,6 +1319,7 @@ int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_
 }
 
 int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
+  DevGuard dg_(ctx);
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
@@ -1331,6 +1361,7 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
 }
 
 int cgks_qcriterion(cgks_ctx* ctx, double* out) {
+  DevGuard dg_(ctx);
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
@@ -1355,6 +1386,7 @@ const char* cgks_last_error(const cgks_ctx* ctx) { return ctx ? ctx->msg : "null
 int cgks_launches_per_step(const cgks_ctx* ctx) { return ctx ? ctx->launches_per_step : 0; }
 
 int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_ms, int64_t* launches, int* n_out) {
+  DevGuard dg_(ctx);
   if (!ctx) return CGKS_ERR_CONFIG;
   int rc = upload_constants(ctx);
   if (rc) return rc;
@@ -1538,6 +1570,7 @@ extern "C" int cgks_fp64_peak(double* tflops, double* ms_out) {
 }
 
 void cgks_destroy(cgks_ctx* ctx) {
+  DevGuard dg_(ctx);
   if (!ctx) return;
   for (int c = 0; c < 2; ++c)
     if (ctx->graph[c]) cudaGraphExecDestroy(ctx->graph[c]);
@@ -1553,7 +1586,7 @@ void cgks_destroy(cgks_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->comm && nccl::g_api.CommDestroy) nccl::g_api.CommDestroy(ctx->comm);
-  if (g_const_owner == ctx) g_const_owner = nullptr;
+  if (g_owner[ctx->device & (kMaxDev - 1)] == ctx) g_owner[ctx->device & (kMaxDev - 1)] = nullptr;
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
                     ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart,
                     ctx->ctab, ctx->Lb[0], ctx->Lb[1], ctx->Ls, ctx->Lc,
