@@ -85,6 +85,9 @@ typedef struct {
   int lines;           /* CGKS-5th: 1 = line-averaged derivatives of the own cell as reconstruction data  */
                        /* (SURVEY 8(f) NEXT-1), carried as extra DOFs per cell;    */
                        /* 0 = the cell-averaged gradient (R1, default).                                  */
+  double chi_scale;    /* GENO: zeta of R8 divided by chi_scale before chi = 1/(1 + zeta^4); 1 = R8 as    */
+                       /* read (default); larger values keep the quartic at larger sub-stencil contrasts  */
+                       /* (the paper defers chi to its references; DESIGN.md section 8 measures 1 / 4 / 8) */
 } cgks_scheme;
 
 /* Fill a cgks_scheme with the paper defaults for scheme id (CGKS_GKS2 / CGKS_CGKS5). */

@@ -52,6 +52,7 @@ class OrcParams(ctypes.Structure):
         ("sutherland_S", ctypes.c_double),
         ("lines", ctypes.c_int),
         ("nodes", ctypes.POINTER(ctypes.c_double) * 3),
+        ("chi_scale", ctypes.c_double),
     ]
 
 
@@ -126,6 +127,7 @@ class Problem:
     relax_C: float = 10.0
     k_venkat: float = 0.3
     chi_c: float = 0.01
+    chi_scale: float = 1.0     # GENO: zeta (R8) divided by chi_scale
     sutherland_S: float = 0.0  # 0: constant mu; 0.4042: the paper's Sutherland law
     lines: int = 0             # CGKS-5th: 1 = line-averaged derivatives as the own-cell data (NEXT-1)
     nodes: tuple = None        # stretched tensor-product mesh (NEXT-4): per-axis node coordinates (n_a + 1) or None
@@ -147,6 +149,7 @@ class Problem:
         p.cfl, p.fixed_dt = self.cfl, self.fixed_dt
         p.tau_eps, p.tau_C, p.relax_C = self.tau_eps, self.tau_C, self.relax_C
         p.k_venkat, p.chi_c = self.k_venkat, self.chi_c
+        p.chi_scale = float(self.chi_scale)
         p.sutherland_S = self.sutherland_S
         p.lines = int(self.lines)
         self._keep = []

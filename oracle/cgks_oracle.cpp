@@ -51,6 +51,7 @@ typedef struct {
                             // P:197-203), 0 = the own cell-averaged gradient (R1)
   const double* nodes[3];   // stretched tensor-product mesh (NEXT-4): node coordinates x_a[0..n_a] per axis, or
                             // NULL for the uniform spacing (hi - lo) / n
+  double chi_scale;         // GENO: zeta (R8) divided by chi_scale (1 = R8 as read)
 } orc_params;
 
 }  // extern "C"
@@ -940,7 +941,7 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
       ismax = std::max(ismax, IS[m]);
       ismin = std::min(ismin, IS[m]);
     }
-    double zeta = (ismax - ismin) / (ismin + 1e-15 + S.P.chi_c * ismax);
+    double zeta = (ismax - ismin) / (ismin + 1e-15 + S.P.chi_c * ismax) / (S.P.chi_scale > 0.0 ? S.P.chi_scale : 1.0);
     cr.chi[v] = 1.0 / (1.0 + std::pow(zeta, 4));
   }
 }

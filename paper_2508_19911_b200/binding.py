@@ -48,6 +48,7 @@ class cgks_scheme(ctypes.Structure):
         ("chi_c", ctypes.c_double),
         ("sutherland_S", ctypes.c_double),
         ("lines", ctypes.c_int),
+        ("chi_scale", ctypes.c_double),
     ]
 
 
@@ -172,7 +173,7 @@ class Solver:
 
     def __init__(self, n, lo, hi, gamma=1.4, mu=0.0, Pr=1.0, scheme=CGKS_CGKS5, nonlinear=0,
                  time_scheme=CGKS_TIME_DEFAULT, cfl=None, fixed_dt=0.0, tau_eps=0.05, tau_C=10.0, relax_C=10.0,
-                 k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, lines=0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
+                 k_venkat=0.3, chi_c=0.01, sutherland_S=0.0, lines=0, chi_scale=1.0, bc=((0, 0), (0, 0), (0, 0)), bc_state=None,
                  stream=None, nodes=None,
                  nproc=(1, 1, 1), rank=0, nccl_id=None):
         L = load()
@@ -211,6 +212,7 @@ class Solver:
         sc.k_venkat, sc.chi_c = float(k_venkat), float(chi_c)
         sc.sutherland_S = float(sutherland_S)
         sc.lines = int(lines)
+        sc.chi_scale = float(chi_scale)
         ctx = ctypes.c_void_p()
         rc = L.cgks_create(ctypes.byref(g), float(gamma), float(mu), float(Pr), ctypes.byref(sc), ctypes.byref(ctx))
         if rc != CGKS_OK:

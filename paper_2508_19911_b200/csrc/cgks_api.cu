@@ -415,6 +415,7 @@ void cgks_scheme_defaults(int id, cgks_scheme* s) {
   s->relax_C = 10.0;
   s->k_venkat = 0.3;
   s->chi_c = 0.01;
+  s->chi_scale = 1.0;
   s->sutherland_S = 0.0;
   s->lines = 0;
 }
@@ -442,6 +443,10 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   }
   if (scheme->lines && scheme->id != CGKS_CGKS5) {
     set_msg(ctx, "line DOFs need CGKS-5th");
+    return fail(CGKS_ERR_CONFIG);
+  }
+  if (!(scheme->chi_scale > 0.0)) {
+    set_msg(ctx, "invalid GENO chi scale %g", scheme->chi_scale);
     return fail(CGKS_ERR_CONFIG);
   }
   if (!(scheme->sutherland_S >= 0.0)) {
@@ -527,6 +532,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   g.gamma = gamma;
   g.k_venkat = scheme->k_venkat;
   g.chi_c = scheme->chi_c;
+  g.chi_is = 1.0 / scheme->chi_scale;
   g.suth = scheme->sutherland_S;
   {
     const int ngl = dim == 3 ? 4 : (dim == 2 ? 2 : 1);

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double*
 #pragma unroll
         for (int a = 0; a < DIM; ++a) lin[a] = fma(w, bm[m][a], lin[a]);
       }
-      const double zeta = (ismax - ismin) / (ismin + eps + c_geo.chi_c * ismax);
+      const double zeta = (ismax - ismin) / (ismin + eps + c_geo.chi_c * ismax) * c_geo.chi_is;
       const double z2 = zeta * zeta;
       const double chi = 1.0 / (1.0 + z2 * z2);
 #pragma unroll

@@ -25,6 +25,7 @@ struct Geo {
   double bc_state[3][2][5];
   double cfl, fixed_dt, mu, gamma;
   double k_venkat, chi_c, eps_venkat2;
+  double chi_is;  // 1 / chi_scale (GENO)
   double suth;  // Sutherland constant S (0: constant mu)
   int lines;    // CGKS-5th line-DOF variant
   int ngl;      // lines per axis (transverse face Gauss points: 4 / 2 / 1)

@@ -231,6 +231,17 @@ def test_parity_hit_config3_geno_10_steps():
     _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
 
 
+@pytest.mark.parametrize("chi_scale", [4.0, 8.0])
+def test_parity_geno_chi_scale(chi_scale):
+    # GENO with zeta scaled by 1/chi_scale (DESIGN R8 discussion): same on both sides
+    case = hit(24)
+    Qg, Gg, Qo, Go = _run_both(case, 1, 10, chi_scale=chi_scale)
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+    # and it differs from the default chi (the parameter reaches the kernel)
+    Qd, _, _, _ = _run_both(case, 1, 10)
+    assert np.abs(Qd - Qg).max() > 1e-12
+
+
 @pytest.mark.slow
 def test_parity_shock_vortex_config4_100_steps():
     """configs[3] geometry at 64x32, nonlinear CGKS-5th with inflow/outflow, 100 steps.

@@ -168,3 +168,43 @@ def test_venkat_extremum_and_constant():
     W, dW, phi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[0.5, 0, 0]]))
     assert phi[0] < 1.0
     assert phi[0] >= 0.0
+
+
+def test_geno_chi_scale_closed_form():
+    # chi_scale C divides zeta (R8): chi_C = 1 / (1 + (zeta_1 / C)^4), zeta_1 = (1/chi_1 - 1)^(1/4),
+    # checked on a curved field where the sub-stencil contrast gives an intermediate chi
+    n = 5
+    ax = np.arange(n) - 2.0
+    Z, Y, X = np.meshgrid(ax, ax, ax, indexing="ij")
+    Q = np.zeros((5, n, n, n))
+    Q[0] = 1.0 + 0.05 * X + 0.01 * X ** 2 + 0.01 * Y
+    Q[4] = 2.5 + 0.1 * Z ** 2
+    G = np.zeros((3, 5, n, n, n))
+    G[0, 0] = 0.05 + 0.02 * X
+    G[1, 0] = 0.01
+    G[2, 4] = 0.2 * Z
+    x = np.array([[0.5, 0.0, 0.0]])
+    chis = {}
+    for C in (1.0, 4.0, 8.0):
+        prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(n, n, n), scheme=1, nonlinear=1, chi_scale=C)
+        _, _, chi = oracle.recon_eval(prob, Q, G, (2, 2, 2), x)
+        chis[C] = chi
+    c1 = chis[1.0][0]
+    assert 0.01 < c1 < 0.99, c1
+    z1 = (1.0 / c1 - 1.0) ** 0.25
+    for C in (4.0, 8.0):
+        assert chis[C][0] == pytest.approx(1.0 / (1.0 + (z1 / C) ** 4), rel=1e-12)
+        assert chis[C][0] > c1
+
+
+def test_geno_chi_scale_keeps_eno_at_a_jump():
+    n = 5
+    Q = np.zeros((5, n, n, n))
+    Q[0] = 1.0
+    Q[4] = 2.5
+    Q[0][:, :, 2:] = 2.0
+    Q[4][:, :, 2:] = 5.0
+    G = np.zeros((3, 5, n, n, n))
+    prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(1, 1, 1), scheme=1, nonlinear=1, chi_scale=8.0)
+    _, _, chi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[-0.5, 0.0, 0.0]]))
+    assert chi[0] < 1e-4 and chi[4] < 1e-4
