@@ -220,6 +220,11 @@ def run_ours(args, rank, ws, lr):
         from paper_2508_19911_b200 import nccl_unique_id
         if args.workload == "tgv512slab":
             case = slab512(ws, rank)
+        elif args.strong:  # strong scaling: the global n^3 TGV split into N z-slabs
+            nb = int(args.workload[3:])
+            if nb % ws or nb // ws < 4:
+                raise SystemExit(f"strong scaling needs n divisible by N with >= 4 planes per rank ({nb}, {ws})")
+            case = tgv(nb, z0=rank * (nb // ws), nzb=nb // ws)
         else:
             nb = int(args.workload[3:])
             case = tgv(nb, zrep=ws, z0=rank * nb, nzb=nb)
@@ -361,9 +366,9 @@ def run_ours(args, rank, ws, lr):
         return 0
     line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if args.strong and ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{case.name} {case.n[0]}x{case.n[1]}x{case.n[2]}"
-                                   + (f" ({case.n[0]}^3 per GPU)" if ws > 1 else ""),
+                                   + (("" if args.strong else f" ({case.n[0]}^2 x {len(case.Q[0])} per GPU)") if ws > 1 else ""),
                        "scheme": args.scheme + ("-geno" if case.nonlinear else "-linear")
                        + ("-lines" if args.lines else "") + (f"-stretched{args.stretch:g}" if args.stretch else ""),
                        "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
@@ -400,6 +405,8 @@ def main():
     ap.add_argument("--stretch", type=float, default=0.0,
                     help="sine-stretched tensor-product mesh with this amplitude (NEXT-4; timing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: split the global tgv<n> grid over the ranks (strong scaling) instead of n^3 per GPU")
     ap.add_argument("--nccl-self", action="store_true",
                     help="1 GPU through the z-slab path: ghost planes + NCCL halo exchange with itself")
     args = ap.parse_args()

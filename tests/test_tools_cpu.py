@@ -51,3 +51,19 @@ def test_bench_workload_names():
     assert bench.make_case("hit16").n == (16, 16, 16)
     with pytest.raises(ValueError):
         bench.make_case("tgv")
+
+
+def test_slab_inputs_tile_the_global_grid():
+    # the per-rank inputs of the decomposed bench runs: slabs of tgv(n) concatenate to tgv(n)
+    # (strong scaling), and the 512 x 512 x 64 blocks are the z-planes of the 512^3 TGV
+    from cgks_inputs import tgv
+    full = tgv(16)
+    parts = [tgv(16, z0=4 * r, nzb=4) for r in range(4)]
+    assert np.array_equal(np.concatenate([p.Q for p in parts], axis=1), full.Q)
+    assert np.array_equal(np.concatenate([p.G for p in parts], axis=2), full.G)
+    sys.path.insert(0, ROOT)
+    import bench
+    b = bench.slab512(8, 3)
+    assert b.n == (512, 512, 512) and b.Q.shape == (5, 64, 512, 512)
+    b1 = bench.slab512(1, 0)
+    assert b1.n == (512, 512, 64) and b1.hi[2] - b1.lo[2] == pytest.approx(2 * np.pi / 8)
