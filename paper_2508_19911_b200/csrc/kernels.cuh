@@ -554,9 +554,6 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
   double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
   uint64_t* bar = reinterpret_cast<uint64_t*>(scratch + 20 * 128);  // TMA completion barrier
-  // block-uniform early exit: the flag can be raised by another block while this one starts, and a
-  // thread that went on alone would wait on a barrier its thread 0 never initialised
-  if (__syncthreads_or(err->code != 0)) return;
   constexpr int FX = FT::FX, FY = FT::FY;
   const int fn0 = c_geo.fn[AX][0];
   // block origin: face (i0, j0, k0); y-/z-faces cover FY faces along their normal axis
@@ -627,11 +624,12 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   }
   if (COMPACT)
     for (int q = threadIdx.x; q < 2 * FT::NQ * FT::TS; q += blockDim.x) cp_async8(tab + q, gtab + q);  // padded rows
+  // block-uniform early exit (the flag can be raised by another block while this one starts); the
+  // copies are issued first so that they overlap this barrier, and are drained before an exit
+  const bool stop = __syncthreads_or(err->code != 0);  // also orders the barrier init before the waits
   cp_async_wait_all();
-  if (tma) {
-    __syncthreads();  // the barrier is initialised before anyone waits on it
-    mbar_wait(bar, 0);
-  }
+  if (tma) mbar_wait(bar, 0);
+  if (stop) return;
   __syncthreads();
 
   const double dt = ts->dt;
