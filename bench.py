@@ -168,17 +168,23 @@ def cpu_baseline(case_name, scheme, budget_s=20.0):
 
 
 def run_reference(args, rank, ws):
+    """The reference arm: the oracle as it stands, W untimed + K timed steps of a bounded sample
+    (the same flow at 24^3) of our arm's workload, on the host cores; the line carries our arm's
+    config (metric, unit and workload), the sample is named in cpu_baseline."""
     if rank != 0:
         return 0
-    cb = cpu_baseline(args.workload, args.scheme, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
-    # the reference arm: W untimed + K timed oracle steps on the bounded sample
     import oracle
-    from cgks_inputs import tgv
+    from cgks_inputs import hit, tgv, tgv_supersonic
+    oracle.build()
+    full = make_case(args.workload)
     if args.workload.startswith("tgv_ss"):
-        from cgks_inputs import tgv_supersonic
         c = tgv_supersonic(24)
+    elif args.workload.startswith("tgv"):
+        c = tgv(24)
+    elif args.workload.startswith("hit"):
+        c = hit(24)
     else:
-        c = tgv(24) if args.workload.startswith("tgv") else make_case(args.workload)
+        c = full
     prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if args.scheme == "cgks5" else 0,
                           time_scheme=2 if args.scheme == "cgks5" else 1)
     Q, G = c.Q, c.G
@@ -188,14 +194,18 @@ def run_reference(args, rank, ws):
     Q, G, _, _, _ = oracle.run(prob, Q, G, args.steps)
     dt = time.perf_counter() - t0
     value = c.ncell * args.steps / dt
+    cores = oracle.max_threads()
     line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.workload} bounded sample {c.n[0]}^3 on host cores",
-                       "scheme": args.scheme, "global_cells": c.ncell},
-            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cb["cores"], "kind": "oracle",
-                             "sample": f"{c.name} {c.n[0]}^3, {args.steps} timed steps"},
+            "config": {"workload": f"{full.name} {full.n[0]}x{full.n[1]}x{full.n[2]}",
+                       "scheme": args.scheme + ("-geno" if full.nonlinear else "-linear"),
+                       "time_scheme": "S2O4" if args.scheme == "cgks5" else "S1O2", "global_cells": full.ncell,
+                       "parallelism": "host cores (CPU oracle)"},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{c.name} {c.n[0]}x{c.n[1]}x{c.n[2]} (bounded sample of the workload), "
+                                       f"{args.warmup} untimed + {args.steps} timed steps, OpenMP threads={cores}"},
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0

@@ -67,3 +67,16 @@ def test_slab_inputs_tile_the_global_grid():
     assert b.n == (512, 512, 512) and b.Q.shape == (5, 64, 512, 512)
     b1 = bench.slab512(1, 0)
     assert b1.n == (512, 512, 64) and b1.hi[2] - b1.lo[2] == pytest.approx(2 * np.pi / 8)
+
+
+def test_bench_reference_arm_line():
+    # the reference arm (CPU oracle on a bounded sample) prints one JSON line with our arm's config
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "cell-updates/s" and line["higher_is_better"]
+    assert line["config"]["workload"] == "tgv 128x128x128" and line["config"]["global_cells"] == 128 ** 3
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
