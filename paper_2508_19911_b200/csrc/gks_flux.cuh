@@ -59,10 +59,13 @@ HD T erfc_e(T z, T e) {
     // per lane (not per warp): the value of a face must not depend on which faces share its warp,
     // so that decomposed runs stay bit-identical; at low Mach the branch is uniform anyway
     if (fabs(z) < 0.5) {
-      const double x = z * z;
-      double s = c_erf_small[11];
-#pragma unroll
-      for (int n = 10; n >= 0; --n) s = fma(s, x, c_erf_small[n]);
+      // Estrin form (dependency depth 5 instead of Horner's 11): pairs in x, quads in x^2, x^4, x^8
+      const double* c = c_erf_small;
+      const double x = z * z, x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
+      const double p0 = fma(c[1], x, c[0]), p1 = fma(c[3], x, c[2]), p2 = fma(c[5], x, c[4]);
+      const double p3 = fma(c[7], x, c[6]), p4 = fma(c[9], x, c[8]), p5 = fma(c[11], x, c[10]);
+      const double q0 = fma(p1, x2, p0), q1 = fma(p3, x2, p2), q2 = fma(p5, x2, p4);
+      const double s = fma(q2, x8, fma(q1, x4, q0));
       return fma(-z, s, 1.0);
     }
   }
