@@ -80,6 +80,8 @@ def lib():
         L.orc_recon5_matrix.restype = ctypes.c_int
         L.orc_recon_eval.argtypes = [pp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp]
         L.orc_recon_eval.restype = ctypes.c_int
+        L.orc_geno_cell.argtypes = [pp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]
+        L.orc_geno_cell.restype = ctypes.c_int
         L.orc_stage_residual.argtypes = [pp, dp, dp, ctypes.c_double, dp, dp, dp, dp]
         L.orc_stage_residual.restype = ctypes.c_int
         L.orc_recon_eval_l.argtypes = [pp, dp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp,
@@ -268,6 +270,20 @@ def recon_eval_lines(prob: Problem, Q, G, L, ijk, x):
     if rc:
         raise ValueError(f"recon_eval rc={rc}")
     return out[:, :5], out[:, 5:].reshape(-1, 3, 5), chi
+
+
+def geno_cell(prob: Problem, Q, G, ijk):
+    """GENO internals of cell ijk (CGKS-5th, nonlinear): IS (6,5), omega (6,5), bsub (6,3,5), chi (5,);
+    sub-stencil m = 2 axis + side (0 minus, 1 plus); only the first 2*dim rows are meaningful."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    IS, om, bs, chi = np.zeros((6, 5)), np.zeros((6, 5)), np.zeros((6, 3, 5)), np.zeros(5)
+    p = prob.to_c()
+    rc = lib().orc_geno_cell(ctypes.byref(p), _ptr(Q), _ptr(G), int(ijk[0]), int(ijk[1]), int(ijk[2]),
+                             _ptr(IS), _ptr(om), _ptr(bs), _ptr(chi))
+    if rc:
+        raise ValueError(f"geno_cell rc={rc}")
+    return IS, om, bs, chi
 
 
 def recon_eval(prob: Problem, Q, G, ijk, x):

@@ -863,6 +863,7 @@ struct CellRecon {
   double chi[5];
   double omega[6][5];
   double bsub[6][3][5];    // sub-stencil linear coefficients (reference units)
+  double IS[6][5];         // smoothness indicators of the sub-stencils (R7)
   // GKS-2nd: linear coefficients b[a][v] (reference units) and limiter phi0[v]
   double b[3][5];
   double phi[5];
@@ -926,6 +927,7 @@ void recon5_cell(const Solver& S, const std::vector<CellState>& F, int i, int j,
         }
       IS[m] = 0.0;  // R7
       for (int a = 0; a < 3; ++a) IS[m] += cr.bsub[m][a][v] * cr.bsub[m][a][v];
+      cr.IS[m][v] = IS[m];
     }
     // nonlinear weights: wbar_m = d_m/(IS_m+eps)^5, normalised
     const double eps = 1e-15;
@@ -1579,6 +1581,28 @@ int orc_recon_eval_l(const orc_params* p, const double* Q, const double* G, cons
   }
   if (chi_out)
     for (int v = 0; v < 5; ++v) chi_out[v] = p->scheme == 1 ? cr.chi[v] : cr.phi[v];
+  return 0;
+}
+
+// GENO internals of cell (i,j,k) (R6-R9): sub-stencil smoothness indicators IS[m][v],
+// normalised nonlinear weights omega[m][v], sub-stencil linear coefficients bsub[m][a][v] (reference
+// units) and chi[v]; m = 2 axis + (0: minus side, 1: plus side), 2*dim sub-stencils.  Test
+// infrastructure for the weight pins (tests/test_oracle_recon.py).  Returns 2 unless CGKS-5th GENO.
+int orc_geno_cell(const orc_params* p, const double* Q, const double* G, int i, int j, int k, double* IS,
+                  double* omega, double* bsub, double* chi) {
+  if (p->scheme != 1 || !p->nonlinear) return 2;
+  Solver S(*p);
+  if (!build_recon5(S.dim, S.rc, p->lines)) return 2;
+  load_state(S, Q, G, nullptr);
+  CellRecon cr;
+  recon5_cell(S, S.U, i, j, k, cr);
+  for (int m = 0; m < 2 * S.dim; ++m)
+    for (int v = 0; v < 5; ++v) {
+      IS[m * 5 + v] = cr.IS[m][v];
+      omega[m * 5 + v] = cr.omega[m][v];
+      for (int a = 0; a < 3; ++a) bsub[(m * 3 + a) * 5 + v] = cr.bsub[m][a][v];
+    }
+  for (int v = 0; v < 5; ++v) chi[v] = cr.chi[v];
   return 0;
 }
 

@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 from cgks_inputs import random_smooth, uniform
-from parity_util import rel_linf, worst
+from parity_util import hmin, rel_linf, worst
 
 pytestmark = pytest.mark.gpu
 
@@ -48,8 +48,7 @@ def test_tiny_grids_match_oracle(n, scheme):
     S.step(3)
     Qg, Gg = S.get_state()
     S.close()
-    L = max(c.hi[a] - c.lo[a] for a in range(c.dim))
-    k, v = worst(rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, L=L))
+    k, v = worst(rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, h=hmin(c), nsteps=3))
     assert v <= 1e-10, (k, v)
 
 

@@ -11,7 +11,7 @@ import pytest
 import oracle
 from cgks_inputs import line_derivatives, vortex
 from cgks_inputs.cases import _vortex_prim, gl_average
-from parity_util import floors, rel_linf, worst
+from parity_util import floors, hmin, rel_linf, worst
 
 pytestmark = pytest.mark.gpu
 
@@ -31,11 +31,11 @@ def _smooth3d():
     return n, lo, hi, Q, G, L
 
 
-def _compare(Qg, Gg, Lg, Qo, Go, Lo, Lbox, tol):
-    r = rel_linf(Qg, Qo, Gg, Go, L=Lbox)
+def _compare(Qg, Gg, Lg, Qo, Go, Lo, h, tol, nsteps=10):
+    r = rel_linf(Qg, Qo, Gg, Go, h=h, nsteps=nsteps, tol=tol)
     k, v = worst(r)
     assert v <= tol, (k, v)
-    qs, gs = floors(Qo, Go, Lbox)
+    qs, gs = floors(Qo, Go, h, nsteps, tol)
     el = np.abs(Lg - Lo).max(axis=(0, 2, 3, 4)) / gs
     assert el.max() <= tol, el
 
@@ -57,7 +57,7 @@ def test_lines_parity_3d(nl):
     tg, _, _ = S.get_time()
     S.close()
     assert abs(tg - to) <= 1e-13 * to
-    _compare(Qg, Gg, Lg, Qo, Go, Lo, 2 * math.pi, 1e-10)
+    _compare(Qg, Gg, Lg, Qo, Go, Lo, hmin(n, lo, hi), 1e-10)
 
 
 def test_lines_parity_vortex_2d():
@@ -75,7 +75,7 @@ def test_lines_parity_vortex_2d():
     Qg, Gg = S.get_state()
     Lg = S.get_lines()
     S.close()
-    _compare(Qg, Gg, Lg, Qo, Go, Lo, 10.0, 1e-10)
+    _compare(Qg, Gg, Lg, Qo, Go, Lo, hmin(c), 1e-10, 20)
 
 
 def test_lines_default_from_gradients():
@@ -90,7 +90,7 @@ def test_lines_default_from_gradients():
     S.step(5)
     Qg, Gg = S.get_state()
     S.close()
-    k, v = worst(rel_linf(Qg, Qo, Gg, Go, L=2 * math.pi))
+    k, v = worst(rel_linf(Qg, Qo, Gg, Go, h=hmin(n, lo, hi), nsteps=5))
     assert v <= 1e-10, (k, v)
 
 
@@ -135,4 +135,4 @@ def test_lines_parity_box(nl, bc):
     tg, _, _ = S.get_time()
     S.close()
     assert abs(tg - to) <= 1e-13 * to
-    _compare(Qg, Gg, Lg, Qo, Go, Lo, 2 * math.pi, 1e-10)
+    _compare(Qg, Gg, Lg, Qo, Go, Lo, hmin(n, lo, hi), 1e-10)

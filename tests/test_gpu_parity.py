@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 from cgks_inputs import double_sod, hit, random_smooth, shock_vortex, tgv, tgv_supersonic, uniform, vortex
-from parity_util import floors, rel_linf, worst
+from parity_util import floors, hmin, rel_linf, worst
 
 pytestmark = pytest.mark.gpu
 
@@ -39,8 +39,9 @@ def _L(case):
     return max(case.hi[a] - case.lo[a] for a in range(case.dim))
 
 
-def _check(Qg, Gg, Qo, Go, scheme, tol, L=1.0):
-    r = rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, L=L)
+def _check(Qg, Gg, Qo, Go, scheme, tol, case, nsteps):
+    r = rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, h=hmin(case), nsteps=nsteps,
+                 tol=tol)
     k, v = worst(r)
     assert v <= tol, (k, v, r)
     return r
@@ -61,7 +62,7 @@ def test_parity_3d_ragged_10_steps(name, scheme, nl, ts, kw):
     case = random_smooth((37, 11, 9), seed=21, jump=0.4 if nl else 0.0)
     case.nonlinear = nl
     Qg, Gg, Qo, Go = _run_both(case, scheme, 10, time_scheme=ts, **kw)
-    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, case, 10)
 
 
 @pytest.mark.parametrize("scheme,ts", [(1, 2), (0, 1), (0, 2)])
@@ -70,14 +71,14 @@ def test_parity_vortex_config1(scheme, ts):
     case = vortex(40)
     for n, tol in [(10, 1e-10), (20, 1e-10)]:
         Qg, Gg, Qo, Go = _run_both(case, scheme, n, time_scheme=ts)
-        _check(Qg, Gg, Qo, Go, scheme, tol, _L(case))
+        _check(Qg, Gg, Qo, Go, scheme, tol, case, n)
 
 
 @pytest.mark.parametrize("scheme", [1, 0])
 def test_parity_100_steps(scheme):
     case = random_smooth((12, 10, 8), seed=5)
     Qg, Gg, Qo, Go = _run_both(case, scheme, 100, mu=1e-3, Pr=0.72)
-    _check(Qg, Gg, Qo, Go, scheme, 1e-8, _L(case))
+    _check(Qg, Gg, Qo, Go, scheme, 1e-8, case, 100)
 
 
 @pytest.mark.parametrize("scheme", [1, 0])
@@ -85,14 +86,14 @@ def test_parity_shock_vortex_box_bc(scheme):
     # config 4 geometry at reduced size: inflow/outflow in x, periodic y, nonlinear (R29)
     case = shock_vortex(nx=96, ny=48)
     Qg, Gg, Qo, Go = _run_both(case, scheme, 10)
-    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, case, 10)
 
 
 @pytest.mark.parametrize("scheme", [1, 0])
 def test_parity_double_sod_1d(scheme):
     case = double_sod(100)
     Qg, Gg, Qo, Go = _run_both(case, scheme, 20)
-    _check(Qg, Gg, Qo, Go, scheme, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, scheme, 1e-10, case, 20)
 
 
 @pytest.mark.parametrize("scheme,nl", [(1, 0), (1, 1), (0, 1)])
@@ -174,7 +175,7 @@ def _sampled_one_step(case, scheme, samples, seed=0, nonlinear=None):
         cc = tuple(r if a < dim else 0 for a in range(3))
         qo = Qo[:, cc[2], cc[1], cc[0]]
         qg = Qg[:, c[2], c[1], c[0]]
-        qs, gs = floors(Qg, Gg if scheme == 1 else None, _L(case))  # R34 floors of the stepped field
+        qs, gs = floors(Qg, Gg if scheme == 1 else None, hmin(case), 1, 1e-10)  # R34 floors of the stepped field
         errs.append(np.abs(qg - qo) / qs)
         if scheme == 1:
             go = Go[:, :, cc[2], cc[1], cc[0]]
@@ -213,7 +214,7 @@ def test_parity_tgv_config2_cgks5_10_steps():
     # configs[1] flow (TGV, Ma 0.1, Re 1600, Pr 0.72) at 24^3, CGKS-5th linear, 10 steps
     case = tgv(24)
     Qg, Gg, Qo, Go = _run_both(case, 1, 10)
-    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, case, 10)
 
 
 @pytest.mark.slow
@@ -221,14 +222,14 @@ def test_parity_tgv_config2_gks2_100_steps():
     # GKS-2nd (S1O2) on the TGV, 100 steps: relative Linf <= 1e-8 (north_star)
     case = tgv(24)
     Qg, Gg, Qo, Go = _run_both(case, 0, 100)
-    _check(Qg, Gg, Qo, Go, 0, 1e-8, _L(case))
+    _check(Qg, Gg, Qo, Go, 0, 1e-8, case, 100)
 
 
 def test_parity_hit_config3_geno_10_steps():
     # configs[2] flow (decaying isotropic turbulence, Ma_t 0.5, Re_lambda 72) at 24^3, nonlinear CGKS-5th
     case = hit(24)
     Qg, Gg, Qo, Go = _run_both(case, 1, 10)
-    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, case, 10)
 
 
 @pytest.mark.parametrize("chi_scale", [4.0, 8.0])
@@ -236,7 +237,7 @@ def test_parity_geno_chi_scale(chi_scale):
     # GENO with zeta scaled by 1/chi_scale (DESIGN R8 discussion): same on both sides
     case = hit(24)
     Qg, Gg, Qo, Go = _run_both(case, 1, 10, chi_scale=chi_scale)
-    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, case, 10)
     # and it differs from the default chi (the parameter reaches the kernel)
     Qd, _, _, _ = _run_both(case, 1, 10)
     assert np.abs(Qd - Qg).max() > 1e-12
@@ -256,8 +257,8 @@ def test_parity_shock_vortex_config4_100_steps():
     Qp = case.Q * (1.0 + 1e-15 * rng.standard_normal(case.Q.shape))
     Qs, Gs, _, _, rc = oracle.run(prob, Qp, case.G, 100)
     assert rc == 0
-    sens = worst(rel_linf(Qs, Qo, Gs, Go, _L(case)))[1]
-    err = worst(rel_linf(Qg, Qo, Gg, Go, _L(case)))
+    sens = worst(rel_linf(Qs, Qo, Gs, Go, hmin(case), 100, 1e-8))[1]
+    err = worst(rel_linf(Qg, Qo, Gg, Go, hmin(case), 100, 1e-8))
     assert err[1] <= max(1e-8, 20.0 * sens), (err, sens)
 
 
@@ -266,14 +267,14 @@ def test_parity_supersonic_tgv_geno_10_steps():
     # P:455-474 at 20^3: nonlinear CGKS-5th (GENO), mu(T) by the Sutherland law, 10 S2O4 steps
     case = tgv_supersonic(20)
     Qg, Gg, Qo, Go = _run_both(case, 1, 10)
-    _check(Qg, Gg, Qo, Go, 1, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, 1, 1e-10, case, 10)
 
 
 def test_parity_supersonic_tgv_gks2_venkat_10_steps():
     # the paper's GKS-2nd comparison run: Venkatakrishnan-limited GKS-2nd, S1O2, Sutherland viscosity
     case = tgv_supersonic(20)
     Qg, Gg, Qo, Go = _run_both(case, 0, 10)
-    _check(Qg, Gg, Qo, Go, 0, 1e-10, _L(case))
+    _check(Qg, Gg, Qo, Go, 0, 1e-10, case, 10)
 
 
 def test_full_size_supersonic_tgv116_sampled():

@@ -12,6 +12,14 @@ from cgks_inputs import gl_average, stretched_nodes, vortex
 from cgks_inputs.cases import _vortex_prim
 from parity_util import rel_linf, worst
 
+
+def _hmin_nodes(nodes, n, lo, hi):
+    hs = []
+    for a in range(3):
+        if n[a] > 1:
+            hs.append(np.diff(nodes[a]).min() if nodes[a] is not None else (hi[a] - lo[a]) / n[a])
+    return min(hs)
+
 pytestmark = pytest.mark.gpu
 
 
@@ -42,7 +50,8 @@ def test_stretched_vortex_2d(scheme, nl):
     Q, G = gl_average(_vortex_prim(0.0), (n, n, 1), (0, 0, 0), (10, 10, 1), 1.4, nq=5, mesh_nodes=nodes)
     Qg, Gg, Qo, Go = _both((n, n, 1), (0, 0, 0), (10, 10, 1), nodes, Q, G, scheme, 10, mu=1e-3, Pr=0.72,
                            nonlinear=nl, cfl=0.3)
-    k, v = worst(rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None, L=10.0))
+    k, v = worst(rel_linf(Qg, Qo, Gg if scheme == 1 else None, Go if scheme == 1 else None,
+                          h=_hmin_nodes(nodes, (n, n, 1), (0, 0, 0), (10, 10, 1))))
     assert v <= 1e-10, (k, v)
 
 
@@ -60,7 +69,7 @@ def test_stretched_3d(box):
     Q, G = gl_average(prim, n, lo, hi, 1.4, nq=4, mesh_nodes=(nodes[0], nodes[1], zn))
     bc = ((2, 2), (0, 0), (0, 0)) if box else ((0, 0), (0, 0), (0, 0))
     Qg, Gg, Qo, Go = _both(n, lo, hi, nodes, Q, G, 1, 10, mu=2e-3, Pr=0.72, nonlinear=1, cfl=0.3, bc=bc)
-    k, v = worst(rel_linf(Qg, Qo, Gg, Go, L=2 * math.pi))
+    k, v = worst(rel_linf(Qg, Qo, Gg, Go, h=_hmin_nodes(nodes, n, lo, hi)))
     assert v <= 1e-10, (k, v)
 
 
@@ -124,10 +133,10 @@ def test_stretched_lines_3d(nl, box):
     tg, _, _ = S.get_time()
     S.close()
     assert abs(tg - to) <= 1e-13 * to
-    k, v = worst(rel_linf(Qg, Qo, Gg, Go, L=2 * math.pi))
+    k, v = worst(rel_linf(Qg, Qo, Gg, Go, h=_hmin_nodes(nodes, n, lo, hi)))
     assert v <= 1e-10, (k, v)
     from parity_util import floors
-    _, gs = floors(Qo, Go, 2 * math.pi)
+    _, gs = floors(Qo, Go, _hmin_nodes(nodes, n, lo, hi))
     el = np.abs(Lg - Lo).max(axis=(0, 2, 3, 4)) / gs
     assert el.max() <= 1e-10, el
 

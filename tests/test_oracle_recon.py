@@ -208,3 +208,109 @@ def test_geno_chi_scale_keeps_eno_at_a_jump():
     prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(1, 1, 1), scheme=1, nonlinear=1, chi_scale=8.0)
     _, _, chi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[-0.5, 0.0, 0.0]]))
     assert chi[0] < 1e-4 and chi[4] < 1e-4
+
+
+# ---- GENO nonlinear weights: omega_m = wbar_m / sum_k wbar_k, wbar_m = d_m / (IS_m + eps)^5,
+# d_m = 1/6, eps = 1e-15 (SPEC S:374-376 lists the pins: equal IS => 1/6, power-5 suppression) --------
+def _geno_block(slopes_minus, slopes_plus, own_grad, h=1.0, n=5):
+    """3-D n^3 periodic block, centre cell c = (2,2,2): the six face neighbours differ from Q_0 by the
+    given reference-unit slopes (minus side: Q_0 - Q_{-a} = slopes_minus[a]; plus side: Q_{+a} - Q_0 =
+    slopes_plus[a]), own cell-averaged gradient own_grad (physical units, h = 1 so reference = physical).
+    The same numbers in all five components (scaled), rho and rho E kept positive."""
+    Q = np.zeros((5, n, n, n))
+    G = np.zeros((3, 5, n, n, n))
+    c = n // 2
+    base = np.array([2.0, 0.3, -0.2, 0.1, 9.0])
+    Q[:] = base[:, None, None, None]
+    scale = np.array([1.0, 0.5, 0.25, 0.125, 2.0])
+    for a in range(3):
+        lo = [c, c, c]
+        hi = [c, c, c]
+        lo[a] -= 1
+        hi[a] += 1
+        Q[(slice(None), lo[2], lo[1], lo[0])] = base - scale * slopes_minus[a]
+        Q[(slice(None), hi[2], hi[1], hi[0])] = base + scale * slopes_plus[a]
+        G[a, :, c, c, c] = scale * own_grad[a] / h
+    prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(n * h,) * 3, scheme=1, nonlinear=1)
+    return prob, Q, G, (c, c, c)
+
+
+def test_geno_weights_equal_is_give_one_sixth():
+    # linear data with equal reference slopes on every axis: all six IS_m equal => omega_m = d_m = 1/6
+    prob, Q, G, c = _geno_block([0.3] * 3, [0.3] * 3, [0.3] * 3)
+    IS, om, _, chi = oracle.geno_cell(prob, Q, G, c)
+    assert np.allclose(IS, IS[0, 0] * np.array([1.0, 0.5, 0.25, 0.125, 2.0]) ** 2 / 1.0, rtol=1e-14)
+    assert np.all(np.abs(om - 1.0 / 6.0) <= 4e-16), om
+    assert np.all(chi == 1.0)
+
+
+def test_geno_weights_power5_suppression():
+    # one sub-stencil (plus side of x) with IS ~1.3e6 x the others: its weight is below 1e-29
+    # (d/(r IS)^5 against five of d/IS^5: (1/r^5) / 5 ~ 5e-32), the other five share the rest equally
+    prob, Q, G, c = _geno_block([0.3] * 3, [600.0, 0.3, 0.3], [0.3] * 3)
+    IS, om, _, _ = oracle.geno_cell(prob, Q, G, c)
+    ratio = IS[1] / IS[0]
+    assert np.all(ratio > 1e6)
+    assert np.all(om[1] < 1e-29), om[1]
+    others = om[[0, 2, 3, 4, 5]]
+    assert np.allclose(others, 0.2, rtol=1e-14, atol=0.0)
+
+
+@pytest.mark.parametrize("r", [2.0, 4.0, 10.0])
+def test_geno_weights_known_ratios(r):
+    """IS ratios fixed by the data: the minus-x sub-stencil has IS_0 = 3 s^2 r, the other five IS = 3 s^2
+    (plus its own transverse slopes), so omega_0 = r^-5 / (r^-5 + 5) and omega_m = 1 / (r^-5 + 5) --
+    the exponent 5 of P:268 decides the values (exponent 1 would give 1/(5 r + 1))."""
+    s = 0.3
+    # minus-x slope b with b^2 + 2 s^2 = 3 s^2 r  =>  b = s sqrt(3 r - 2)
+    b = s * np.sqrt(3.0 * r - 2.0)
+    prob, Q, G, c = _geno_block([b, s, s], [s, s, s], [s, s, s])
+    IS, om, _, _ = oracle.geno_cell(prob, Q, G, c)
+    assert np.allclose(IS[0] / IS[1], r, rtol=1e-13)
+    w0 = r ** -5 / (r ** -5 + 5.0)
+    assert np.allclose(om[0], w0, rtol=1e-13), (om[0], w0)
+    assert np.allclose(om[1:], 1.0 / (r ** -5 + 5.0), rtol=1e-13)
+
+
+def test_geno_blend_value_1d_known_ratio():
+    """The blended face value of P:259-263 in 1-D: Q(x_G) = chi P^4(x_G) + (1 - chi) sum_m omega_m P_m^1(x_G).
+    Data (Q_{-1}, Q_0, Q_{+1}) = (Q_0 - c, Q_0, Q_0 + 2c): sub-stencil slopes c and 2c, IS ratio 4, so
+    omega = (1024/1025, 1/1025) and sum_m omega_m P_m^1(1/2) = Q_0 + (1026/1025) c / 2.  P^4 is the linear
+    scheme's value of the same data (nonlinear = 0); chi is the oracle's (R8, parity unpinned)."""
+    n = 7
+    h = 0.5
+    c = 0.04
+    Q = np.zeros((5, 1, 1, n))
+    base = np.array([1.0, 0.2, 0.0, 0.0, 2.5])
+    Q[:] = base[:, None, None, None]
+    i0 = 3
+    Q[:, 0, 0, i0 - 1] = base - c
+    Q[:, 0, 0, i0 + 1] = base + 2 * c
+    Q[2:4] = 0.0
+    G = np.zeros((3,) + Q.shape)
+    G[0, :, 0, 0, i0] = 1.5 * c / h
+    G[0, 2:4] = 0.0
+    kw = dict(n=(n, 1, 1), lo=(0, 0, 0), hi=(n * h, 1, 1), scheme=1)
+    x = np.array([[0.5, 0.0, 0.0], [-0.5, 0.0, 0.0]])
+    Wl, dWl, _ = oracle.recon_eval(oracle.Problem(**kw, nonlinear=0), Q, G, (i0, 0, 0), x)
+    Wn, dWn, chi = oracle.recon_eval(oracle.Problem(**kw, nonlinear=1), Q, G, (i0, 0, 0), x)
+    assert np.all((chi[[0, 1, 4]] > 0.0) & (chi[[0, 1, 4]] < 1.0))
+    slope = 1026.0 / 1025.0 * c  # reference units
+    for v in (0, 1, 4):
+        for p, xr in enumerate((0.5, -0.5)):
+            lin = base[v] + slope * xr
+            want = chi[v] * Wl[p, v] + (1.0 - chi[v]) * lin
+            assert abs(Wn[p, v] - want) <= 1e-14 * abs(want), (v, p, Wn[p, v], want)
+            dwant = chi[v] * dWl[p, 0, v] + (1.0 - chi[v]) * slope / h
+            assert abs(dWn[p, 0, v] - dwant) <= 1e-13 * abs(dwant), (v, p, dWn[p, 0, v], dwant)
+
+
+def test_geno_weights_epsilon():
+    """eps = 1e-15 of P:270 enters as (IS_m + eps): five flat sub-stencils (IS = 0) and one with IS = eps
+    give omega = (2 eps)^-5 / ((2 eps)^-5 + 5 eps^-5) = 1/161 for that one (a dropped eps would give 0)."""
+    s = np.sqrt(1e-15)
+    prob, Q, G, c = _geno_block([0.0] * 3, [s, 0.0, 0.0], [0.0] * 3)
+    IS, om, _, _ = oracle.geno_cell(prob, Q, G, c)
+    assert abs(IS[1, 0] - 1e-15) <= 1e-22 and np.all(IS[[0, 2, 3, 4, 5], 0] == 0.0)
+    assert abs(om[1, 0] - 1.0 / 161.0) <= 1e-6 / 161.0, om[1, 0]
+    assert np.allclose(om[[0, 2, 3, 4, 5], 0], 32.0 / 161.0, rtol=1e-6)
