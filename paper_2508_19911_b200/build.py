@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcgks.so")
 SOURCES = ["cgks_api.cu", "cls_build.cpp", "stage_d1.cu", "stage_d2.cu", "stage_d3.cu"]
-HEADERS = ["kernels.cuh", "gks_flux.cuh", "cls_build.h", "flop_count.h", "recon_gen.cuh", "types.h", "driver.h",
+HEADERS = ["kernels.cuh", "flux1.cuh", "gks_flux.cuh", "cls_build.h", "flop_count.h", "recon_gen.cuh", "types.h", "driver.h",
            "stage_impl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -1443,9 +1443,14 @@ struct ParkHost {
   void mark(int m) const { marks[m] = fc::tally().flops; }
 };
 
-// flops of one Gauss point: both cooperating lanes, with the part both lanes compute identically to
-// stay convergent (the exchange sums and the whole interface phase up to the side relaxation, marks
-// 1 to 5) counted once
+// flops of one Gauss point in the formulation k_flux1 runs (one lane per Gauss point): both sides'
+// half-range terms (side_terms), their sum (25 additions), the interface phase once (interface_terms)
+// and, for CGKS-5th, the relaxation weight and the two sides' relaxed interface values
+struct ParkCount {
+  fc::CD* slots;
+  void put(int s, const fc::CD& v) const { slots[s] = v; }
+  fc::CD get(int s) const { return slots[s]; }
+};
 static double flux_point_flops(const FluxConst& f, bool compact) {
   using fc::CD;
   CD W[2][5], dW[2][3][5];
@@ -1458,19 +1463,27 @@ static double flux_point_flops(const FluxConst& f, bool compact) {
       dW[1][d][i] = CD::run(-0.02 * (i + 1) + 0.01 * d);
     }
   }
-  double total = 0.0;
-  for (int side = 0; side < 2; ++side) {
-    GPOutT<CD> o;
-    CD slots[40];
-    double marks[6] = {0, 0, 0, 0, 0, 0};
-    fc::tally() = fc::Tally();
-    if (compact)
-      gks_flux_side<true>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
-    else
-      gks_flux_side<false>(side, W[side], dW[side], CD::run(1e-3), CD::run(1e3), f, XchgMirror(), ParkHost{slots, marks}, o);
-    total += fc::tally().flops - (side == 1 ? marks[5] - marks[1] : 0.0);
+  fc::tally() = fc::Tally();
+  CD x1[45], slots[25], p[2], dtw[2][5], acc[20], jump;
+  for (int q = 0; q < 45; ++q) x1[q] = CD::run(0.0);
+  for (int s = 0; s < 2; ++s) {
+    side_terms<CD>(s ? -1.0 : 1.0, W[s], dW[s], f, x1, p[s], dtw[s]);
+    for (int q = 0; q < 25; ++q) {
+      slots[q] = s ? slots[q] + x1[20 + q] : x1[20 + q];
+      x1[20 + q] = CD::run(0.0);
+    }
   }
-  return total;
+  interface_terms<CD>(x1, p[0], p[1], CD::run(1e-3), CD::run(1e3), f, ParkCount{slots}, acc, jump);
+  if (compact) {
+    CD ee = relax_ee<CD>(jump, f);
+    CD w = CD::run(1.0) - ee;
+    for (int s = 0; s < 2; ++s)
+      for (int i = 0; i < 5; ++i) {
+        acc[10 + i] = w * acc[10 + i] + ee * W[s][i];
+        acc[15 + i] = w * acc[15 + i] + ee * dtw[s][i];
+      }
+  }
+  return fc::tally().flops;
 }
 
 extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names, double* flops_per_launch,

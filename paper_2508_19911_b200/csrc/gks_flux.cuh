@@ -602,4 +602,197 @@ HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const
   return good;
 }
 
+
+// ---------------------------------------------------------------------------
+// One lane per Gauss point (k_flux1): the same interface solver as gks_flux_side, with both sides'
+// half-range terms computed by one lane (no lane exchange, the interface phase executed once).
+// side_terms adds one side's half-range contributions into x1[0..44] (layout of gks_flux_side:
+// 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3, 25-29 MF4, 30-34 MF5, 35-39 MQ4, 40-44 MQ5) and
+// returns the side's pressure, positivity and Euler time derivative dW/dt (R23).
+// ---------------------------------------------------------------------------
+template <typename T>
+HD bool side_terms(double sgn, const T* W, const T (*dW)[5], const FluxConst& fc, T* x1, T& p_out, T* dtw) {
+  const T gm1 = fc.gamma - 1.0;
+  const T rho = W[0], ir = 1.0 / rho;
+  const T U = W[1] * ir, V = W[2] * ir, Ww = W[3] * ir;
+  const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
+  const T p = gm1 * (W[4] - rho * uu2s);
+  const bool ok = (rho > 0.0) && (p > 0.0);
+  const T ip = ok ? T(1.0) / p : T(1.0);
+  const T lam = ok ? T(0.5) * rho * ip : T(1.0);
+  const T sv = ok ? p * ir : T(0.5);  // variance 1/(2 lam)
+  const T Uv[3] = {U, V, Ww};
+  p_out = p;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) dtw[i] = 0.0;
+  {
+    const Dprim<T> q0 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[0]);
+    jvp_flux<0>(rho, Uv, p, W[4], dW[0], q0, -1.0, dtw);
+    const Dprim<T> q1 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[1]);
+    jvp_flux<1>(rho, Uv, p, W[4], dW[1], q1, -1.0, dtw);
+    const Dprim<T> q2 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[2]);
+    jvp_flux<2>(rho, Uv, p, W[4], dW[2], q2, -1.0, dtw);
+  }
+  T M[7];
+  half_moments(U, lam, sv, sgn, M);  // H(u) or 1-H(u)
+  Tg<T> tg;
+  tg_value(V, Ww, sv, fc.N, tg);
+  const RW<T> G00 = rw_value<0, 0>(tg, rho), G10 = rw_value<1, 0>(tg, rho), G01 = rw_value<0, 1>(tg, rho);
+  col_value<0>(M, G00, x1 + 0);
+  col_value<1>(M, G00, x1 + 20);
+#pragma unroll
+  for (int dir = 0; dir < 4; ++dir) {
+    const T* d = dir < 3 ? dW[dir] : dtw;
+    const Dprim<T> q = dprim(ir, Uv, uu2s, fc.gamma - 1.0, d);
+    const T dlam = lam * (q.dr * ir - q.dp * ip);
+    const T ds = -2.0 * sv * sv * dlam;
+    T dM[5];
+    moments_deriv(M, U, lam, sv, q.du[0], dlam, dM);
+    Tg<T> dt;
+    tg_deriv(V, Ww, sv, fc.N, q.du[1], q.du[2], ds, dt);
+    const RW<T> H00 = rw_deriv<0, 0>(tg, dt, rho, q.dr);
+    if (dir == 0) {
+      col_deriv<0>(M, dM, G00, H00, x1 + 5);
+      col_deriv<1>(M, dM, G00, H00, x1 + 35);
+      col_deriv<2>(M, dM, G00, H00, x1 + 25);
+    } else if (dir == 1) {
+      const RW<T> H10 = rw_deriv<1, 0>(tg, dt, rho, q.dr);
+      col_deriv<0>(M, dM, G00, H00, x1 + 10);
+      col_deriv<0>(M, dM, G10, H10, x1 + 35);
+      col_deriv<1>(M, dM, G10, H10, x1 + 25);
+    } else if (dir == 2) {
+      const RW<T> H01 = rw_deriv<0, 1>(tg, dt, rho, q.dr);
+      col_deriv<0>(M, dM, G00, H00, x1 + 15);
+      col_deriv<0>(M, dM, G01, H01, x1 + 35);
+      col_deriv<1>(M, dM, G01, H01, x1 + 25);
+    } else {
+      col_deriv<0>(M, dM, G00, H00, x1 + 40);
+      col_deriv<1>(M, dM, G00, H00, x1 + 30);
+    }
+  }
+  return ok;
+}
+
+// Interface phase (G) of gks_flux_side from the summed half-range terms: x1[0..19] in registers, the
+// half-range vectors x1[20..44] in parking slots 0..24 (get(i)).  Writes acc[0..9] = F^n, F_t^n
+// (Prandtl fix applied) and acc[10..19] = Q^n, Q_t^n of the interface, and the relative pressure jump
+// |pL - pR| / (pL + pR) for the side relaxation.  Returns the positivity of the equilibrium state.
+template <typename T, typename P>
+HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& fc, const P& park, T* acc, T& jump_out) {
+  const T gm1 = fc.gamma - 1.0;
+  const T r0 = x1[0], i0 = 1.0 / r0;
+  const T U0 = x1[1] * i0, V0 = x1[2] * i0, Ww0 = x1[3] * i0;
+  const T uu2 = 0.5 * (U0 * U0 + V0 * V0 + Ww0 * Ww0);
+  const T p0 = gm1 * (x1[4] - r0 * uu2);
+  const bool good = (r0 > 0.0) && (p0 > 0.0);
+  const T rpp = 1.0 / (p0 * (pL + pR));
+  const T jump = fabs(pL - pR) * (p0 * rpp);
+  jump_out = jump;
+  T mu_p0 = fc.mu * ((pL + pR) * rpp);
+  if (fc.suth > 0.0) {
+    const T T0 = p0 * i0;
+    mu_p0 = fc.mu * (1.0 + fc.suth) * sqrt(T0) * i0 / (T0 + fc.suth);
+  }
+  const T tau = (fc.mu > 0.0) ? (mu_p0 + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
+  T al[6], be[6];
+  T a20, a21;  // heat-flux scalars of the Prandtl fix (R20)
+  {
+    const T U0v[3] = {U0, V0, Ww0};
+    const T uu0 = 2.0 * uu2;
+    const double K5 = fc.N + 5.0, K7 = fc.N + 7.0;
+    T MQa[5], MF1[5], MF2[5], MF0[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) MQa[i] = MF1[i] = MF2[i] = 0.0;
+    {
+      const T* d0 = x1 + 5;
+      const Dprim<T> q0 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d0);
+      jvp_flux<0>(r0, U0v, p0, x1[4], d0, q0, 1.0, MQa);
+      jvp_flux2<0>(r0, i0, U0v, p0, uu0, K5, K7, q0, MF1);
+      const T* d1 = x1 + 10;
+      const Dprim<T> q1 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d1);
+      jvp_flux<1>(r0, U0v, p0, x1[4], d1, q1, 1.0, MQa);
+      jvp_flux2<1>(r0, i0, U0v, p0, uu0, K5, K7, q1, MF1);
+      const T* d2 = x1 + 15;
+      const Dprim<T> q2 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d2);
+      jvp_flux<2>(r0, U0v, p0, x1[4], d2, q2, 1.0, MQa);
+      jvp_flux2<2>(r0, i0, U0v, p0, uu0, K5, K7, q2, MF1);
+      const Dprim<T> qa = dprim(i0, U0v, uu2, fc.gamma - 1.0, MQa);
+      jvp_flux<0>(r0, U0v, p0, x1[4], MQa, qa, -1.0, MF2);
+    }
+    {
+      const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation
+      const T E2 = 1.0 - m2;
+      const T c3 = tau * m2 * (3.0 - E2) * idt;
+      const T qq = 4.0 * tau * m2 * m2 * idt * idt;
+      al[0] = 1.0 - c3;
+      be[0] = qq;
+      al[1] = 2.0 * tau * c3 - tau * (1.0 + 2.0 * E2 - E2 * E2);
+      be[1] = 4.0 * tau * m2 * (dt * E2 - 2.0 * tau * m2) * idt * idt;
+      al[2] = -tau + tau * c3;
+      be[2] = 1.0 - tau * qq;
+      al[3] = c3;
+      be[3] = -qq;
+      al[4] = -2.0 * tau * c3 + tau * E2 * (2.0 - E2);
+      be[4] = -be[1];
+      al[5] = -tau * c3;
+      be[5] = tau * qq;
+    }
+    MF0[0] = r0 * U0;
+    MF0[1] = r0 * U0 * U0 + p0;
+    MF0[2] = r0 * U0 * V0;
+    MF0[3] = r0 * U0 * Ww0;
+    MF0[4] = U0 * (x1[4] + p0);
+    const T sMF0 = qF(MF0, U0, V0, Ww0, uu2), sMF1 = qF(MF1, U0, V0, Ww0, uu2), sMF2 = qF(MF2, U0, V0, Ww0, uu2),
+            sMQa = qF(MQa, U0, V0, Ww0, uu2);
+    const T sW = qF(x1, U0, V0, Ww0, uu2);  // qF(W0); MQ0 = MQ3 = W0
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const T mf0 = MF0[i], mf1 = MF1[i], mf2 = MF2[i], mqa = MQa[i];
+      acc[i] = al[0] * mf0 + al[1] * mf1 + al[2] * mf2;
+      acc[5 + i] = be[0] * mf0 + be[1] * mf1 + be[2] * mf2;
+      acc[10 + i] = (al[0] + al[3]) * x1[i] + (al[1] - al[2]) * mqa;  // MQ1 = MQa, MQ2 = -MQa (compatibility)
+      acc[15 + i] = (be[0] + be[3]) * x1[i] + (be[1] - be[2]) * mqa;
+    }
+    a20 = -U0 * sW * (al[0] - 1.0 + al[3]) + (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) +
+          al[2] * (sMF2 + U0 * sMQa);
+    a21 = -U0 * sW * (be[0] + be[3]) + be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
+  }
+  {
+    T v3[5], v4[5], v5[5], q4[5], q5[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      v3[i] = park.get(i);
+      v4[i] = park.get(5 + i);
+      v5[i] = park.get(10 + i);
+      q4[i] = park.get(15 + i);
+      q5[i] = park.get(20 + i);
+    }
+    const T s3 = qF(v3, U0, V0, Ww0, uu2);
+    const T s4 = qF(v4, U0, V0, Ww0, uu2) - U0 * qF(q4, U0, V0, Ww0, uu2);
+    const T s5 = qF(v5, U0, V0, Ww0, uu2) - U0 * qF(q5, U0, V0, Ww0, uu2);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
+      acc[5 + i] += be[3] * v3[i] + be[4] * v4[i] + be[5] * v5[i];
+      acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
+      acc[15 + i] += be[4] * q4[i] + be[5] * q5[i];
+    }
+    a20 += al[3] * s3 + al[4] * s4 + al[5] * s5;
+    a21 += be[3] * s3 + be[4] * s4 + be[5] * s5;
+  }
+  if (fc.Pr != 1.0) {  // Prandtl fix (R20)
+    acc[4] += fc.pfix * a20;
+    acc[9] += fc.pfix * a21;
+  }
+  return good;
+}
+
+// side-state relaxation weight (R23): ee = exp(-dt / tau0), tau0 = C |pL - pR| / (pL + pR) dt,
+// taken as 0 below 1e-304 (smooth flow; see gks_flux_side)
+template <typename T>
+HD T relax_ee(T jump, const FluxConst& fc) {
+  const T rC = fc.relax_C * jump;
+  return (rC > 1.0 / 700.0) ? exp(-1.0 / fmax(rC, T(1.0 / 700.0))) : T(0.0);
+}
+
 }  // namespace cgks

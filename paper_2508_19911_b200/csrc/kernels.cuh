@@ -848,6 +848,10 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __re
   }
 }
 
+}  // namespace cgks
+#include "flux1.cuh"
+
+namespace cgks {
 // ---------------------------------------------------------------------------
 // K3: residual, Gauss-theorem gradients and stage update
 //   MODE 0: S2O4 stage 1  (Uin = U^n -> Uout = U*, carry)

@@ -78,10 +78,25 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 }
 
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
+#ifndef CGKS_FLUX1
+#define CGKS_FLUX1 1  // 1: k_flux1 (one lane per Gauss point), 0: k_flux (two lanes per Gauss point)
+#endif
+#if CGKS_FLUX1
+template <int AX, bool COMPACT>
+using FluxTileSel = FluxTile1<D, AX, COMPACT>;
+#else
+template <int AX, bool COMPACT>
+using FluxTileSel = FluxTile<D, AX, COMPACT>;
+#endif
+
 template <bool COMPACT, bool BOX, int AX, bool LINES = false, bool STR = false>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
-  using FT = FluxTile<D, AX, COMPACT>;
+  using FT = FluxTileSel<AX, COMPACT>;
+#if CGKS_FLUX1
+  auto kern = k_flux1<D, AX, COMPACT, BOX, LINES, STR>;
+#else
   auto kern = k_flux<D, AX, COMPACT, BOX, LINES, STR>;
+#endif
   static bool attr = false;
   const size_t smem = FT::smem_bytes();
   if (!attr) {
@@ -245,14 +260,14 @@ int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part
 template <bool C>
 void flux_tile_t(int ax, int* tx, int* tn) {
   if (ax == 0) {
-    *tx = FluxTile<D, 0, C>::TX;
-    *tn = FluxTile<D, 0, C>::TN;
+    *tx = FluxTileSel<0, C>::TX;
+    *tn = FluxTileSel<0, C>::TN;
   } else if (ax == 1) {
-    *tx = FluxTile<D, (D > 1 ? 1 : 0), C>::TX;
-    *tn = FluxTile<D, (D > 1 ? 1 : 0), C>::TN;
+    *tx = FluxTileSel<(D > 1 ? 1 : 0), C>::TX;
+    *tn = FluxTileSel<(D > 1 ? 1 : 0), C>::TN;
   } else {
-    *tx = FluxTile<D, (D > 2 ? 2 : 0), C>::TX;
-    *tn = FluxTile<D, (D > 2 ? 2 : 0), C>::TN;
+    *tx = FluxTileSel<(D > 2 ? 2 : 0), C>::TX;
+    *tn = FluxTileSel<(D > 2 ? 2 : 0), C>::TN;
   }
 }
 
