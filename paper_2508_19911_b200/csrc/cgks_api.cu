@@ -116,6 +116,10 @@ struct cgks_ctx {
   double* staging = nullptr;
   TimeState* ts = nullptr;
   ErrState* err = nullptr;
+  ErrState* err_sticky = nullptr;  // first error of an earlier pipelined batch (async calls), cleared by cgks_sync
+  bool async_latched = false;      // a batch's error record was latched into err_sticky
+  cudaEvent_t ev_const = nullptr;  // end of this context's enqueued work when another takes the constants
+  long long test_peer_fail = -1;   // CGKS_TEST_PEER_FAIL_STEP (NCCL ranks): emulated peer failure (tests only)
   int cur = 0;
   ClsTables cls;
   double Rp[ReconGen<3>::NNZ > ReconGenL<3>::NNZ ? ReconGen<3>::NNZ : ReconGenL<3>::NNZ];  // packed CLS matrix
@@ -198,6 +202,15 @@ static void set_msg(cgks_ctx* c, const char* fmt, ...) {
 static int upload_constants(cgks_ctx* ctx) {
   cgks_ctx*& owner = g_owner[ctx->device & (kMaxDev - 1)];
   if (owner == ctx) return CGKS_OK;
+  // the previous owner's enqueued kernels (asynchronous calls, graphs) read the constants until they
+  // finish: the upload waits for them
+  if (owner && owner->ev_const && owner->stream) {
+    if (cudaEventRecord(owner->ev_const, owner->stream) != cudaSuccess ||
+        cudaStreamWaitEvent(ctx->stream, owner->ev_const, 0) != cudaSuccess) {
+      set_msg(ctx, "cannot order the constant upload after the previous context's work");
+      return CGKS_ERR_CUDA;
+    }
+  }
   if (ctx->ops->upload(ctx->geo, ctx->fc, ctx->Rp, ctx->scheme_id == CGKS_CGKS5 ? ctx->nnz : 0, ctx->stream)) {
     set_msg(ctx, "constant upload failed: %s", cudaGetErrorString(cudaGetLastError()));
     return CGKS_ERR_CUDA;
@@ -371,15 +384,27 @@ static int dt_reduce(cgks_ctx* ctx) {
   return nccl_check(ctx, e, "allreduce(min) of dt");
 }
 
-// one full time step from U[cur] into U[1-cur]
+// dt of the first step of a call: k_dt on U[cur] (local min), allreduce-min over the ranks, dt.  Later
+// steps take theirs from the final update's fused CFL min (k_step_end).
+static int initial_dt(cgks_ctx* ctx) {
+  LaunchEnv env = env_of(ctx);
+  if (ctx->ops->dt(env, ctx->U[ctx->cur], ctx->NV, ctx->ts, ctx->err, ctx->ncell)) return CGKS_ERR_CUDA;
+  if (ctx->comm_mode == 1) {
+    if (ctx->ops->err_poison(env, ctx->ts, ctx->err, ctx->test_peer_fail)) return CGKS_ERR_CUDA;
+    int rc = dt_reduce(ctx);
+    if (rc) return rc;
+  }
+  if (ctx->ops->dt_final(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
+  return CGKS_OK;
+}
+
+// one full time step from U[cur] into U[1-cur]: the stages (the final update forms the next dt's CFL
+// candidates), then -- NCCL ranks -- the error poison and the allreduce-min, then the step end
 static int one_step(cgks_ctx* ctx) {
   double* Un = ctx->U[ctx->cur];
   double* Unext = ctx->U[1 - ctx->cur];
   LaunchEnv env = env_of(ctx);
-  if (ctx->ops->dt(env, Un, ctx->NV, ctx->ts, ctx->err, ctx->ncell)) return CGKS_ERR_CUDA;
-  int rc = dt_reduce(ctx);
-  if (rc) return rc;
-  if (ctx->ops->dt_final(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
+  int rc;
   if (ctx->time_scheme == CGKS_TIME_S1O2) {
     rc = halo_stage(ctx, Un, Unext, 2, 1);
   } else {
@@ -387,6 +412,11 @@ static int one_step(cgks_ctx* ctx) {
     if (!rc) rc = halo_stage(ctx, ctx->Us, Unext, 1, 2);
   }
   if (rc) return rc;
+  if (ctx->comm_mode == 1) {
+    if (ctx->ops->err_poison(env, ctx->ts, ctx->err, ctx->test_peer_fail)) return CGKS_ERR_CUDA;
+    rc = dt_reduce(ctx);
+    if (rc) return rc;
+  }
   if (ctx->ops->step_end(env, ctx->ts, ctx->err)) return CGKS_ERR_CUDA;
   ctx->cur = 1 - ctx->cur;
   return CGKS_OK;
@@ -395,7 +425,7 @@ static int one_step(cgks_ctx* ctx) {
 static int count_launches(cgks_ctx* c) {
   int per_stage = (c->overlap ? 3 : 1) + c->dim + 1;  // overlapped halo: the reconstruction in 3 launches
   int stages = (c->time_scheme == CGKS_TIME_S1O2) ? 1 : 2;
-  return 2 + stages * per_stage + 1;
+  return stages * per_stage + 1 + (c->comm_mode == 1 ? 1 : 0);  // + step end (+ error poison)
 }
 
 // ---------------------------------------------------------------------------
@@ -633,7 +663,9 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   for (int a = 0; a < dim && ok; ++a)
     ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] * g.fn[a][2] * nff);
   if (!ok || cudaMalloc((void**)&ctx->ts, sizeof(TimeState)) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->err, sizeof(ErrState)) != cudaSuccess) {
+      cudaMalloc((void**)&ctx->err, sizeof(ErrState)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->err_sticky, sizeof(ErrState)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_const, cudaEventDisableTiming) != cudaSuccess) {
     set_msg(ctx, "device allocation failed (%lld cells)", ctx->ncell);
     return fail(CGKS_ERR_CUDA);
   }
@@ -797,6 +829,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       }
       ctx->comm_mode = 1;
       ctx->overlap = std::getenv("CGKS_NO_OVERLAP") == nullptr;
+      if (const char* tp = std::getenv("CGKS_TEST_PEER_FAIL_STEP")) ctx->test_peer_fail = std::atoll(tp);
       if (cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -808,6 +841,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     }
   }
   cudaMemset(ctx->err, 0, sizeof(ErrState));
+  cudaMemset(ctx->err_sticky, 0, sizeof(ErrState));
   TimeState t0;
   std::memset(&t0, 0, sizeof(t0));
   double big = 1e300;
@@ -857,6 +891,9 @@ int cgks_nccl_unique_id(void* out128) {
 }
 
 static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0);
+extern "C" int cgks_sync(cgks_ctx* ctx);
+// the synchronous calls first complete (and report) what the asynchronous ones enqueued
+static int drain_async(cgks_ctx* ctx) { return ctx->async_pending ? cgks_sync(ctx) : CGKS_OK; }
 
 // In-process group of slab contexts on one device, stepped in lock-step: one shared time state,
 // all work on the first context's stream, halos copied between the contexts' buffers.
@@ -868,6 +905,9 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
     set_msg(c0, "cgks_step_group: stretched meshes need one process per rank (NCCL), not an in-process group");
     return CGKS_ERR_CONFIG;
   }
+  for (int r = 0; r < n; ++r)
+    if (ctxs[r])
+      if (int e = drain_async(ctxs[r])) return e;
   for (int r = 0; r < n; ++r) {
     if (!ctxs[r] || ctxs[r]->rank != r || ctxs[r]->nranks != n || ctxs[r]->comm_mode == 1 ||
         std::memcmp(&ctxs[r]->geo, &c0->geo, sizeof(Geo)) != 0 || ctxs[r]->device != c0->device ||
@@ -918,12 +958,15 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
     }
     return CGKS_OK;
   };
-  for (int s = 0; s < nsteps && !rc; ++s) {
+  if (nsteps > 0) {  // dt of the first step: min over the members' states (later: fused in the final update)
     LaunchEnv env = env_of(c0);
     for (int r = 0; r < n && !rc; ++r)
       if (ctxs[r]->ops->dt(env, ctxs[r]->U[ctxs[r]->cur], ctxs[r]->NV, c0->ts, c0->err, ctxs[r]->ncell))
         rc = CGKS_ERR_CUDA;
     if (!rc && c0->ops->dt_final(env, c0->ts, c0->err)) rc = CGKS_ERR_CUDA;
+  }
+  for (int s = 0; s < nsteps && !rc; ++s) {
+    LaunchEnv env = env_of(c0);
     // each stage in the two halves of the NCCL ranks' overlapped schedule (interior reconstruction,
     // exchange, the rest), so the split stage is covered on one device
     auto stage_all = [&](int which, int mode, int stg) -> int {
@@ -964,6 +1007,11 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
   return rc;
 }
 
+// keep the first error of a pipelined batch before the next cgks_set_state_async resets the flag
+static __global__ void k_err_latch(const ErrState* err, ErrState* sticky) {
+  if (err->code != 0 && sticky->code == 0) *sticky = *err;
+}
+
 static bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -973,9 +1021,6 @@ static bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-extern "C" int cgks_sync(cgks_ctx* ctx);
-// the synchronous calls first complete (and report) what the asynchronous ones enqueued
-static int drain_async(cgks_ctx* ctx) { return ctx->async_pending ? cgks_sync(ctx) : CGKS_OK; }
 
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
   DevGuard dg_(ctx);
@@ -1071,11 +1116,11 @@ static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0) {
   if (e.code) {
     // kernels after the failure were no-ops; the last completed step sits in the input buffer of step e.step
     long long done = t.steps - steps0;
-    ctx->cur = (int)((cur0 + done) % 2);
-    static const char* kn[] = {"?", "flux", "update", "dt"};
+    ctx->cur = (int)((((cur0 + done) % 2) + 2) % 2);
+    static const char* kn[] = {"?", "flux", "update", "dt", "another rank (its error code, via the dt allreduce)"};
     set_msg(ctx, "%s at cell (%d,%d,%d), step %lld, stage %d (kernel %s)",
             e.code == 3 ? "positivity failure (rho<=0 or p<=0)" : "non-finite time step", e.cell[0], e.cell[1],
-            e.cell[2], e.step, e.stage, kn[e.kernel & 3]);
+            e.cell[2], e.step, e.stage, kn[(unsigned)e.kernel % 5]);
     return e.code == 3 ? CGKS_ERR_POSITIVITY : CGKS_ERR_NUMERICAL;
   }
   return CGKS_OK;
@@ -1126,6 +1171,7 @@ int cgks_step(cgks_ctx* ctx, int nsteps) {
     for (int c = 0; c < 2 && ctx->use_graph; ++c)
       if (!ctx->graph[c] && capture_step(ctx, c)) ctx->use_graph = false;  // fall back to direct launches
   }
+  if (nsteps > 0 && (rc = initial_dt(ctx))) return rc;
   for (int s = 0; s < nsteps; ++s) {
     if (ctx->use_graph) {
       CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
@@ -1226,6 +1272,12 @@ int cgks_set_state_async(cgks_ctx* ctx, const double* Q, const double* gradQ) {
   CK(cudaEventRecord(ctx->ev_in_free, ctx->stream));
   if (ctx->lines && ctx->ops->lines_init(ctx->stream, U, ctx->Lb[0], nc)) CK(cudaGetLastError());
   CK(cudaMemcpyAsync(ctx->ts, ctx->ts0, sizeof(TimeState), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->async_steps) {  // the previous batch's steps: keep their first error for cgks_sync
+    k_err_latch<<<1, 1, 0, ctx->stream>>>(ctx->err, ctx->err_sticky);
+    CK(cudaGetLastError());
+    ctx->async_latched = true;
+    ctx->async_steps = false;  // the next cgks_step_async starts a new batch from U[0], step 0
+  }
   CK(cudaMemsetAsync(ctx->err, 0, sizeof(ErrState), ctx->stream));
   ctx->host_steps = 0;
   ctx->async_pending = true;
@@ -1249,6 +1301,7 @@ int cgks_step_async(cgks_ctx* ctx, int nsteps) {
     for (int c = 0; c < 2 && ctx->use_graph; ++c)
       if (!ctx->graph[c] && capture_step(ctx, c)) ctx->use_graph = false;
   }
+  if (nsteps > 0 && (rc = initial_dt(ctx))) return rc;
   for (int s = 0; s < nsteps; ++s) {
     if (ctx->use_graph) {
       CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
@@ -1304,11 +1357,26 @@ int cgks_sync(cgks_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->cout) CK(cudaStreamSynchronize(ctx->cout));
   ctx->async_pending = false;
+  int rc = CGKS_OK;
   if (ctx->async_steps) {
     ctx->async_steps = false;
-    return finish_steps(ctx, ctx->async_cur0, ctx->async_steps0);
+    rc = finish_steps(ctx, ctx->async_cur0, ctx->async_steps0);
   }
-  return CGKS_OK;
+  if (ctx->async_latched) {  // an earlier batch of the pipeline failed: report its (first) error
+    ctx->async_latched = false;
+    ErrState e;
+    CK(cudaMemcpy(&e, ctx->err_sticky, sizeof(e), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->err_sticky, 0, sizeof(ErrState)));
+    if (e.code) {
+      static const char* kn[] = {"?", "flux", "update", "dt", "another rank"};
+      set_msg(ctx, "%s at cell (%d,%d,%d), step %lld, stage %d (kernel %s) in an earlier pipelined batch "
+                   "(cgks_set_state_async reset the state after it; its outputs are not valid)",
+              e.code == 3 ? "positivity failure (rho<=0 or p<=0)" : "non-finite time step", e.cell[0], e.cell[1],
+              e.cell[2], e.step, e.stage, kn[(unsigned)e.kernel % 5]);
+      return e.code == 3 ? CGKS_ERR_POSITIVITY : CGKS_ERR_NUMERICAL;
+    }
+  }
+  return rc;
 }
 
 int cgks_get_time(const cgks_ctx* cctx, double* t, int64_t* steps, double* last_dt) {
@@ -1394,13 +1462,16 @@ int cgks_launches_per_step(const cgks_ctx* ctx) { return ctx ? ctx->launches_per
 int cgks_profile(cgks_ctx* ctx, int nsteps, int max, char* names, double* total_ms, int64_t* launches, int* n_out) {
   DevGuard dg_(ctx);
   if (!ctx) return CGKS_ERR_CONFIG;
+  if (int r = drain_async(ctx)) return r;
   int rc = upload_constants(ctx);
   if (rc) return rc;
   ctx->prof = true;
   ctx->ptimes.clear();
   TimeState t;
-  CK(cudaMemcpy(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(&t, ctx->ts, sizeof(t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   int cur0 = ctx->cur;
+  if (nsteps > 0) rc = initial_dt(ctx);
   for (int s = 0; s < nsteps && !rc; ++s) rc = one_step(ctx);
   ctx->prof = false;
   cudaStreamSynchronize(ctx->stream);
@@ -1614,6 +1685,8 @@ void cgks_destroy(cgks_ctx* ctx) {
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);
   if (ctx->err) cudaFree(ctx->err);
+  if (ctx->err_sticky) cudaFree(ctx->err_sticky);
+  if (ctx->ev_const) cudaEventDestroy(ctx->ev_const);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

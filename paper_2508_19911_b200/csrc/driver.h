@@ -60,7 +60,11 @@ struct DimOps {
   int (*stage)(LaunchEnv& env, const StageArgs& a, int mode, int stage);
   int (*dt)(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err, long long ncell);  // local min
   int (*dt_final)(LaunchEnv& env, TimeState* ts, ErrState* err);  // dt = CFL * (global) min
+  // end of a step: t, steps += 1 and the next dt from the final update's fused CFL min (rank-reduced)
   int (*step_end)(LaunchEnv& env, TimeState* ts, ErrState* err);
+  // NCCL slab runs: a failing rank posts its error code into the dt min before the allreduce
+  // (test_step >= 0: test hook emulating a peer rank's failure in that step, CGKS_TEST_PEER_FAIL_STEP)
+  int (*err_poison)(LaunchEnv& env, TimeState* ts, ErrState* err, long long test_step);
   int (*pack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   int (*unpack)(cudaStream_t s, const double* src, double* dst, int NV, int f0, int nf, long long ncell);
   // flow diagnostics of a.Uin (reconstruction + quadrature); *nblk = number of 4-double block partials

@@ -90,10 +90,12 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
   const bool tma = !BOX && use_tma && !wraps;
   if (tma) {
     if (threadIdx.x == 0) {
+      // tile boxes and the evaluation tables (one 1-D bulk copy) complete on one mbarrier
       mbar_init(bar, 1);
-      mbar_expect_tx(bar, (unsigned)(sizeof(double) * (FT::NREC + 5) * NT));
+      mbar_expect_tx(bar, (unsigned)(sizeof(double) * ((FT::NREC + 5) * NT + FT::TAB)));
       tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2]);
       tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
+      if (COMPACT) bulk_load(tab, gtab, (unsigned)(sizeof(double) * FT::TAB), bar);
     }
   } else {
     // cp.async: TPC threads per tile cell (index math once per cell), a strided subset of its fields each
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
       }
     }
   }
-  if (COMPACT)
+  if (COMPACT && !tma)
     for (int q = threadIdx.x; q < FT::TAB; q += blockDim.x) cp_async8(tab + q, gtab + q);
   const bool stop = __syncthreads_or(err->code != 0);
   cp_async_wait_all();

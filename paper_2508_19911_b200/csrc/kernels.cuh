@@ -169,6 +169,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (bytes a multiple of 16, both addresses 16-byte aligned) on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
                                            int j, int k) {
   if (atomicCAS(&err->code, 0, code) == 0) {
@@ -858,19 +867,67 @@ namespace cgks {
 //   MODE 1: S2O4 stage 2  (carry -> Uout = U^{n+1})
 //   MODE 2: S1O2          (Uin = U^n -> Uout = U^{n+1})
 // ---------------------------------------------------------------------------
+// per-cell CFL candidate (R25): CFL-free min over the active axes of min(h_a / (|U_a| + c), h_a^2 / (3 nu));
+// ok = false if the state is not positive (the candidate is then 1e300)
+template <int DIM>
+__device__ __forceinline__ double cfl_candidate(const double* q, int i, int j, int k, bool& ok) {
+  const double ir = 1.0 / q[0];
+  const double u[3] = {q[1] * ir, q[2] * ir, q[3] * ir};
+  const double p = (c_geo.gamma - 1.0) * (q[4] - 0.5 * q[0] * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
+  ok = (q[0] > 0.0) && (p > 0.0);
+  double cand = 1e300;
+  if (ok) {
+    const double c = sqrt(c_geo.gamma * p * ir);
+    double mu_T = c_geo.mu;
+    if (c_geo.suth > 0.0) {  // Sutherland law, T = p / rho
+      const double Tc = p * ir;
+      mu_T = c_geo.mu * (1.0 + c_geo.suth) * Tc * sqrt(Tc) / (Tc + c_geo.suth);
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double ha = c_geo.stretched ? cw(a, a == 0 ? i : (a == 1 ? j : k)) : c_geo.h[a];
+      double d = ha / (fabs(u[a]) + c);
+      if (c_geo.mu > 0.0) d = fmin(d, ha * ha / (3.0 * mu_T * ir));  // nu = mu(T) / rho (R25)
+      cand = fmin(cand, d);
+    }
+  }
+  return cand;
+}
+
+// block min of a candidate (all threads of the block call it), atomicMin of the bit pattern by thread 0
+// (order-preserving for positive doubles; NaN bits are above every finite positive value)
+__device__ __forceinline__ void block_min_atomic(double cand, unsigned long long* dst) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = cand;
+  __syncthreads();
+  if (w == 0) {
+    cand = l < (int)(blockDim.x >> 5) ? red[l] : 1e300;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
+    if (l == 0) atomicMin(dst, (unsigned long long)__double_as_longlong(cand));
+  }
+}
+
 template <int DIM, bool COMPACT, int MODE, bool LINES = false>
 __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, const double* __restrict__ fx,
                                                  const double* __restrict__ fy, const double* __restrict__ fz,
                                                  double* __restrict__ Uout, double* __restrict__ carry,
-                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
+                                                 TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                  double* __restrict__ Lout = nullptr,
                                                  double* __restrict__ Lcarry = nullptr) {
   constexpr int NV = COMPACT ? 20 : 5;
   constexpr int NF = COMPACT ? (LINES ? 30 + 2 * (DIM == 3 ? 4 : (DIM == 2 ? 2 : 1)) * 10 : 30) : 10;
-  if (err->code) return;
+  // the final update of a step (MODE 1, 2) also forms the next step's CFL candidates (fused):
+  // block min, atomicMin into ts->dtmin_bits; k_step_end turns the (global) min into dt
+  constexpr bool DT = MODE != 0;
+  if (__syncthreads_or(err->code != 0)) return;  // block-uniform (block reduction below)
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
-  if (t >= nc) return;
+  double cand = 1e300;
+  if (t < nc) {
   const int i = (int)(t % c_geo.n[0]);
   const int j = (int)((t / c_geo.n[0]) % c_geo.n[1]);
   const int k = (int)(t / c_geo.plane);
@@ -991,6 +1048,13 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
   const double ke = 0.5 * (Qo[1] * Qo[1] + Qo[2] * Qo[2] + Qo[3] * Qo[3]) / Qo[0];
   const double p = (c_geo.gamma - 1.0) * (Qo[4] - ke);
   if (!(Qo[0] > 0.0) || !(p > 0.0)) flag_error(err, 3, 2, MODE == 0 ? 1 : 2, ts->steps, i, j, k);
+  if (DT) {
+    bool ok;
+    cand = cfl_candidate<DIM>(Qo, i, j, k, ok);
+    if (ok && !(cand == cand)) flag_error(err, 4, 2, 2, ts->steps, i, j, k);
+  }
+  }
+  if (DT) block_min_atomic(cand, &ts->dtmin_bits);
 }
 
 // ---------------------------------------------------------------------------
@@ -1000,7 +1064,6 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV, TimeState* __restrict__ ts,
                                              ErrState* __restrict__ err) {
-  __shared__ double red[8];
   if (__syncthreads_or(err->code != 0)) return;  // block-uniform (block reduction below)
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
@@ -1012,43 +1075,23 @@ __global__ void __launch_bounds__(256) k_dt(const double* __restrict__ U, int NV
     double q[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) q[v] = __ldg(U + sidx(NV, v, i, j, k));
-    const double ir = 1.0 / q[0];
-    const double u[3] = {q[1] * ir, q[2] * ir, q[3] * ir};
-    const double p = (c_geo.gamma - 1.0) * (q[4] - 0.5 * q[0] * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
-    if (!(q[0] > 0.0) || !(p > 0.0)) {
+    bool ok;
+    cand = cfl_candidate<DIM>(q, i, j, k, ok);
+    if (!ok)
       flag_error(err, 3, 3, 0, ts->steps, i, j, k);
-    } else {
-      const double c = sqrt(c_geo.gamma * p * ir);
-      double mu_T = c_geo.mu;
-      if (c_geo.suth > 0.0) {  // Sutherland law, T = p / rho
-        const double Tc = p * ir;
-        mu_T = c_geo.mu * (1.0 + c_geo.suth) * Tc * sqrt(Tc) / (Tc + c_geo.suth);
-      }
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) {
-        const double ha = c_geo.stretched ? cw(a, a == 0 ? i : (a == 1 ? j : k)) : c_geo.h[a];
-        double d = ha / (fabs(u[a]) + c);
-        if (c_geo.mu > 0.0) d = fmin(d, ha * ha / (3.0 * mu_T * ir));  // nu = mu(T) / rho (R25)
-        cand = fmin(cand, d);
-      }
-      if (!(cand == cand)) flag_error(err, 4, 3, 0, ts->steps, i, j, k);
-    }
+    else if (!(cand == cand))
+      flag_error(err, 4, 3, 0, ts->steps, i, j, k);
   }
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = cand;
-  __syncthreads();
-  if (w == 0) {
-    cand = l < (blockDim.x >> 5) ? red[l] : 1e300;
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) cand = fmin(cand, __shfl_xor_sync(0xffffffffu, cand, m));
-    if (l == 0) atomicMin(&ts->dtmin_bits, (unsigned long long)__double_as_longlong(cand));
-  }
+  block_min_atomic(cand, &ts->dtmin_bits);
 }
 
-static __global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
+// dt of the first step of a cgks_step call from the k_dt min (rank-reduced; poison as in k_step_end)
+static __global__ void k_dt_finalize(TimeState* ts, ErrState* err) {
   if (err->code) return;
+  if (ts->dtmin_bits < 16ull) {
+    flag_error(err, (int)ts->dtmin_bits, 4, 0, ts->steps, -1, -1, -1);
+    return;
+  }
   const double m = __longlong_as_double((long long)ts->dtmin_bits);
   const double dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
   ts->dt = dt;
@@ -1056,10 +1099,32 @@ static __global__ void k_dt_finalize(TimeState* ts, const ErrState* err) {
   ts->dtmin_bits = (unsigned long long)__double_as_longlong(1e300);
 }
 
-static __global__ void k_step_end(TimeState* ts, const ErrState* err) {
+// end of a step: advance t and the step count, and turn the (rank-reduced) min of the final update's
+// CFL candidates into the next dt.  A bit pattern below 16 is an error code posted by a failing rank
+// (k_err_poison) through the allreduce-min: this rank then fails the same step with the same code
+// (kernel 4 = peer), so that every rank stops at the same step with the same state.
+static __global__ void k_step_end(TimeState* ts, ErrState* err) {
   if (err->code) return;
+  const unsigned long long b = ts->dtmin_bits;
+  if (b < 16ull) {
+    flag_error(err, (int)b, 4, 2, ts->steps, -1, -1, -1);
+    return;
+  }
   ts->t += ts->dt;
   ts->steps += 1;
+  const double m = __longlong_as_double((long long)b);
+  const double dt = c_geo.fixed_dt > 0.0 ? c_geo.fixed_dt : c_geo.cfl * m;
+  ts->dt = dt;
+  ts->idt = 1.0 / dt;
+  ts->dtmin_bits = (unsigned long long)__double_as_longlong(1e300);
+}
+
+// a failing rank posts its error code as its dt candidate bits (below every positive double) before the
+// allreduce-min of the NCCL slab runs, so that every rank sees it (k_step_end, k_dt_finalize)
+// (test_step >= 0: test hook of tests/test_gpu_nccl_self.py -- a peer rank's positivity failure in that step)
+static __global__ void k_err_poison(TimeState* ts, const ErrState* err, long long test_step) {
+  if (err->code) ts->dtmin_bits = (unsigned long long)err->code;
+  else if (test_step >= 0 && ts->steps == test_step) ts->dtmin_bits = 3ull;
 }
 
 // user layout [f][z][y][x]  <->  internal [z][f][y][x]

@@ -297,12 +297,17 @@ int dt_fn(LaunchEnv& env, const double* U, int NV, TimeState* ts, ErrState* err,
 }
 
 int dt_final_fn(LaunchEnv& env, TimeState* ts, ErrState* err) {
-  LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ts, (const ErrState*)err);
+  LAUNCH("dt_finalize", k_dt_finalize, 1, 32, ts, err);
   return 0;
 }
 
 int step_end_fn(LaunchEnv& env, TimeState* ts, ErrState* err) {
-  LAUNCH("step_end", k_step_end, 1, 32, ts, (const ErrState*)err);
+  LAUNCH("step_end", k_step_end, 1, 32, ts, err);
+  return 0;
+}
+
+int err_poison_fn(LaunchEnv& env, TimeState* ts, ErrState* err, long long test_step) {
+  LAUNCH("err_poison", k_err_poison, 1, 32, ts, (const ErrState*)err, test_step);
   return 0;
 }
 

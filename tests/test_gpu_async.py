@@ -70,3 +70,78 @@ def test_async_deferred_positivity_error():
     assert np.array_equal(Q3, Qb)
     assert S.get_time()[1] == 0
     S.close()
+
+
+def test_async_error_of_first_batch_is_not_wiped():
+    # a failure in batch n must survive cgks_set_state_async of batch n+1 (sticky record)
+    from paper_2508_19911_b200 import CgksError, Solver
+    case = random_smooth((16, 8, 6), seed=2)
+    good = [random_smooth((16, 8, 6), seed=s) for s in (3, 4)]
+    S = Solver.from_case(case, scheme=1)
+    Qb = case.Q.copy()
+    Qb[0, 2, 3, 4] = -1.0
+    outs = [(_pinned(np.zeros_like(case.Q)), _pinned(np.zeros_like(case.G))) for _ in range(3)]
+    for (Q, G), (qo, go) in zip([(Qb, case.G)] + [(c.Q, c.G) for c in good], outs):
+        S.set_state_async(Q, G)
+        S.step_async(2)
+        S.get_state_async(qo, go)
+    with pytest.raises(CgksError) as e:
+        S.sync()
+    assert e.value.code == 3
+    assert "earlier pipelined batch" in S.last_error()
+    # the later batches ran normally
+    R = Solver.from_case(case, scheme=1)
+    for c, (qo, go) in zip(good, outs[1:]):
+        R.set_state(c.Q, c.G)
+        R.step(2)
+        Qr, Gr = R.get_state()
+        assert np.array_equal(qo.numpy(), Qr) and np.array_equal(go.numpy(), Gr)
+    R.close()
+    # the record is cleared by the sync that reported it
+    S.set_state(good[0].Q, good[0].G)
+    S.step(1)
+    S.close()
+
+
+def test_async_after_sync_steps_bookkeeping():
+    # sync steps, then async steps, then a new batch that fails: the buffer index must stay valid
+    from paper_2508_19911_b200 import CgksError, Solver
+    case = random_smooth((16, 8, 6), seed=2)
+    S = Solver.from_case(case, scheme=1)
+    S.set_state(case.Q, case.G)
+    S.step(4)
+    S.step_async(1)
+    Qb = case.Q.copy()
+    Qb[0, 1, 1, 1] = -1.0
+    S.set_state_async(Qb, case.G)
+    S.step_async(5)
+    with pytest.raises(CgksError) as e:
+        S.sync()
+    assert e.value.code == 3
+    Q3, _ = S.get_state()
+    assert np.array_equal(Q3, Qb)
+    S.close()
+
+
+def test_two_contexts_constants_ordered():
+    # context B's constant upload must wait for context A's enqueued asynchronous steps
+    from paper_2508_19911_b200 import Solver
+    a = random_smooth((20, 12, 10), seed=1)
+    b = random_smooth((12, 10, 8), seed=2)
+    R = Solver.from_case(a, scheme=1, mu=1e-3, Pr=0.72)
+    R.set_state(a.Q, a.G)
+    R.step(4)
+    Qr, Gr = R.get_state()
+    R.close()
+    A = Solver.from_case(a, scheme=1, mu=1e-3, Pr=0.72)
+    B = Solver.from_case(b, scheme=1, nonlinear=1, mu=5e-3, Pr=1.0)
+    qo, go = _pinned(np.zeros_like(a.Q)), _pinned(np.zeros_like(a.G))
+    A.set_state_async(a.Q, a.G)
+    A.step_async(4)
+    A.get_state_async(qo, go)
+    B.set_state(b.Q, b.G)  # takes the constants while A's steps may still be queued
+    B.step(2)
+    A.sync()
+    assert np.array_equal(qo.numpy(), Qr) and np.array_equal(go.numpy(), Gr)
+    A.close()
+    B.close()

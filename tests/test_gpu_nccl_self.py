@@ -84,3 +84,29 @@ def test_nccl_self_halo_async_pipeline():
     S.sync()
     S.close()
     assert np.array_equal(qo.numpy(), Q1) and np.array_equal(go.numpy(), G1)
+
+
+@pytest.mark.parametrize("graph", [1, 0])
+def test_nccl_peer_failure_stops_at_the_same_step(graph, monkeypatch):
+    """a rank that fails posts its error code through the dt allreduce-min; a healthy rank
+    then fails the same step with the same code and keeps the state of the last completed step.  The
+    peer is emulated by the CGKS_TEST_PEER_FAIL_STEP hook of the error-poison kernel (one GPU per call)."""
+    import torch  # noqa: F401
+    from paper_2508_19911_b200 import CgksError, Solver, nccl_unique_id
+    if not graph:
+        monkeypatch.setenv("CGKS_NO_GRAPH", "1")
+    case = random_smooth((16, 12, 10), seed=4)
+    kw = dict(mu=1e-3, Pr=0.72)
+    Q2, G2, t2, _ = _run(case, 1, 0, 2, False, **kw)
+    monkeypatch.setenv("CGKS_TEST_PEER_FAIL_STEP", "2")
+    S = Solver.from_case(case, scheme=1, nccl_id=nccl_unique_id(), **kw)
+    S.set_state(case.Q, case.G)
+    with pytest.raises(CgksError) as e:
+        S.step(5)
+    assert e.value.code == 3
+    assert "another rank" in S.last_error()
+    t, steps, _ = S.get_time()
+    assert steps == 2 and t == t2[0]
+    Q, G = S.get_state()
+    assert np.array_equal(Q, Q2) and np.array_equal(G, G2)
+    S.close()
