@@ -3,7 +3,15 @@
 cell-updates/s and the fraction of the FP64/HBM roofline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload tgv<N>|hit<N>|tgv_ss<N>|shock_vortex|vortex40] [--scheme cgks5|gks2]
+                  [--workload tgv<N>|hit<N>|tgv_ss<N>|tgv512slab|shock_vortex|vortex40] [--scheme cgks5|gks2]
+
+Multi-GPU (one process per GPU, NCCL): `python bench.py --gpus N` starts the N ranks itself
+(torch.distributed.run, 127.0.0.1) unless it already runs under a launcher (WORLD_SIZE set), and
+refuses a WORLD_SIZE that differs from --gpus.  Default workloads: N = 1 the 128^3 TGV (the
+north_star roofline case); N > 1 the north_star weak-scaling run, a 512 x 512 x 64 block of the
+512^3 TGV per GPU (BASELINE configs[4]: N = 8 is the 512^3 run); --strong --workload tgv<n> splits
+a global n^3 grid instead.  Every rank prints one line on stderr with its communicator's own rank
+and rank count (cgks_comm_info: ncclCommUserRank / ncclCommCount).
 
 A step is one full S2O4 time step of CGKS-5th (dt min-reduction + two stages of
 reconstruction, fluxes and update) over the whole grid.  Default workload: the
@@ -59,6 +67,19 @@ def make_case(name):
     if name == "vortex40":
         return vortex(40)
     raise ValueError(name)
+
+
+def workload_desc(name, ws):
+    """(config name, global cells, nonlinear) of a workload without building its initial state"""
+    import re
+    if name == "tgv512slab":
+        return f"tgv 512x512x{64 * ws}", 512 * 512 * 64 * ws, 0
+    m = re.fullmatch(r"(tgv_ss|tgv|hit)(\d+)", name)
+    if m:
+        n = int(m.group(2))
+        return f"{m.group(1)} {n}x{n}x{n}", n ** 3, 0 if m.group(1) == "tgv" else 1
+    c = make_case(name)
+    return f"{c.name} {c.n[0]}x{c.n[1]}x{c.n[2]}", c.ncell, c.nonlinear
 
 
 class ClockSampler:
@@ -176,7 +197,7 @@ def run_reference(args, rank, ws):
     import oracle
     from cgks_inputs import hit, tgv, tgv_supersonic
     oracle.build()
-    full = make_case(args.workload)
+    full_name, full_cells, full_nl = workload_desc(args.workload, ws)
     if args.workload.startswith("tgv_ss"):
         c = tgv_supersonic(24)
     elif args.workload.startswith("tgv"):
@@ -184,14 +205,16 @@ def run_reference(args, rank, ws):
     elif args.workload.startswith("hit"):
         c = hit(24)
     else:
-        c = full
+        c = make_case(args.workload)
     prob = oracle.Problem(**c.problem_kwargs(), scheme=1 if args.scheme == "cgks5" else 0,
                           time_scheme=2 if args.scheme == "cgks5" else 1)
     Q, G = c.Q, c.G
+    # all host cores (a launcher such as torch.distributed.run sets OMP_NUM_THREADS=1 per rank)
+    nth = os.cpu_count() or 1
     for _ in range(args.warmup):
-        Q, G, _, _, _ = oracle.run(prob, Q, G, 1)
+        Q, G, _, _, _ = oracle.run(prob, Q, G, 1, nthreads=nth)
     t0 = time.perf_counter()
-    Q, G, _, _, _ = oracle.run(prob, Q, G, args.steps)
+    Q, G, _, _, _ = oracle.run(prob, Q, G, args.steps, nthreads=nth)
     dt = time.perf_counter() - t0
     value = c.ncell * args.steps / dt
     cores = oracle.max_threads()
@@ -199,9 +222,9 @@ def run_reference(args, rank, ws):
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{full.name} {full.n[0]}x{full.n[1]}x{full.n[2]}",
-                       "scheme": args.scheme + ("-geno" if full.nonlinear else "-linear"),
-                       "time_scheme": "S2O4" if args.scheme == "cgks5" else "S1O2", "global_cells": full.ncell,
+            "config": {"workload": full_name,
+                       "scheme": args.scheme + ("-geno" if full_nl else "-linear"),
+                       "time_scheme": "S2O4" if args.scheme == "cgks5" else "S1O2", "global_cells": full_cells,
                        "parallelism": "host cores (CPU oracle)"},
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
                              "sample": f"{c.name} {c.n[0]}x{c.n[1]}x{c.n[2]} (bounded sample of the workload), "
@@ -244,6 +267,12 @@ def run_ours(args, rank, ws, lr):
         dist.broadcast_object_list(obj, src=0)
         S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, nproc=(1, 1, ws), rank=rank,
                              nccl_id=obj[0])
+        cr, cn, cb = S.comm_info()
+        print(json.dumps({"bench_rank": rank, "world_size": ws, "comm_rank": cr, "comm_nranks": cn,
+                          "backend": "nccl" if cb == 1 else cb, "device": torch.cuda.current_device()}),
+              file=sys.stderr, flush=True)
+        if (cr, cn) != (rank, ws):
+            raise SystemExit(f"communicator reports rank {cr} of {cn}, expected {rank} of {ws}")
     else:
         if args.workload == "tgv512slab":  # the block of one rank of the 512^3 run, with the periodic self halo
             case = slab512(1, 0)
@@ -402,13 +431,32 @@ def run_ours(args, rank, ws, lr):
     return 0
 
 
+def launch_plan(gpus, env):
+    """("run", None) under a launcher or for one GPU, ("exec", argv) to start the ranks with
+    torch.distributed.run, ("refuse", msg) if WORLD_SIZE contradicts --gpus."""
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            return "refuse", f"WORLD_SIZE={ws} but --gpus {gpus}: refusing to run a different rank count"
+        return "run", None
+    if gpus <= 1:
+        return "run", None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    return "exec", [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+                    "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="tgv128")
+    ap.add_argument("--workload", default=None,
+                    help="default: tgv128 on 1 GPU, tgv512slab (512 x 512 x 64 per GPU) on N > 1")
     ap.add_argument("--scheme", default="cgks5", choices=["cgks5", "gks2"])
     ap.add_argument("--nonlinear", type=int, default=None)
     ap.add_argument("--lines", type=int, default=0, help="CGKS-5th with line-averaged derivative DOFs (NEXT-1)")
@@ -420,7 +468,15 @@ def main():
     ap.add_argument("--nccl-self", action="store_true",
                     help="1 GPU through the z-slab path: ghost planes + NCCL halo exchange with itself")
     args = ap.parse_args()
+    what, info = launch_plan(args.gpus, os.environ)
+    if what == "refuse":
+        print(info, file=sys.stderr)
+        return 2
+    if what == "exec":
+        return subprocess.call(info + sys.argv[1:])
     rank, ws, lr = dist_init()
+    if args.workload is None:
+        args.workload = "tgv512slab" if ws > 1 and not args.strong else ("tgv512" if args.strong else "tgv128")
     if args.impl == "reference":
         return run_reference(args, rank, ws)
     return run_ours(args, rank, ws, lr)

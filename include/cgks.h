@@ -132,6 +132,12 @@ int cgks_nccl_unique_id(void* out128);
  * run bit for bit (same per-cell arithmetic, same global dt). */
 int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps);
 
+/* The context's decomposition as its communicator reports it: *rank and *nranks (for NCCL
+ * contexts from ncclCommUserRank / ncclCommCount of the live communicator, else the create-time
+ * values), *backend = 0 single context, 1 NCCL, 2 in-process group.  Host only; any pointer may be
+ * NULL.  CGKS_ERR_COMM if the NCCL queries fail. */
+int cgks_comm_info(const cgks_ctx* ctx, int* rank, int* nranks, int* backend);
+
 /* Set the state (user layout, rank-local block).  gradQ may be NULL (zero gradients;
  * not recommended for CGKS-5th, R26; ignored by GKS-2nd).  Resets t and the step count. */
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);

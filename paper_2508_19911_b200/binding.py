@@ -62,7 +62,7 @@ _lib = None
 
 EXPORTS = ["cgks_scheme_defaults", "cgks_create", "cgks_local_extent", "cgks_set_state", "cgks_step",
            "cgks_get_state", "cgks_get_time", "cgks_last_error", "cgks_launches_per_step", "cgks_profile",
-           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group",
+           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group", "cgks_comm_info",
            "cgks_set_state_async", "cgks_step_async", "cgks_get_state_async", "cgks_sync", "cgks_destroy"]
 
 
@@ -104,6 +104,8 @@ def load(path: str = LIB_PATH):
                                  ctypes.POINTER(ctypes.c_int)]
     L.cgks_nccl_unique_id.argtypes = [ctypes.c_void_p]
     L.cgks_step_group.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int]
+    ip = ctypes.POINTER(ctypes.c_int)
+    L.cgks_comm_info.argtypes = [vp, ip, ip, ip]
     L.cgks_destroy.argtypes = [vp]
     L.cgks_destroy.restype = None
     _lib = L
@@ -306,6 +308,13 @@ class Solver:
         out = np.zeros(self.n[::-1])
         self._check(self._L.cgks_qcriterion(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
+
+    def comm_info(self):
+        """cgks_comm_info: (rank, nranks, backend) as the live communicator reports them (backend 0 single,
+        1 NCCL, 2 in-process group)."""
+        r, n, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._check(self._L.cgks_comm_info(self.ctx, ctypes.byref(r), ctypes.byref(n), ctypes.byref(b)))
+        return r.value, n.value, b.value
 
     def last_error(self):
         return self._L.cgks_last_error(self.ctx).decode()

@@ -53,6 +53,8 @@ struct Api {
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
+  int (*CommCount)(Comm, int*) = nullptr;
+  int (*CommUserRank)(Comm, int*) = nullptr;
 };
 static Api g_api;
 static bool load() {
@@ -75,6 +77,8 @@ static bool load() {
   SYM(GroupStart);
   SYM(GroupEnd);
   SYM(GetErrorString);
+  SYM(CommCount);
+  SYM(CommUserRank);
 #undef SYM
   return g_api.GetUniqueId && g_api.CommInitRank && g_api.Send && g_api.Recv && g_api.AllReduce &&
          g_api.GroupStart && g_api.GroupEnd;
@@ -887,6 +891,20 @@ int cgks_nccl_unique_id(void* out128) {
   nccl::UniqueId id;
   if (nccl::g_api.GetUniqueId(&id)) return CGKS_ERR_COMM;
   std::memcpy(out128, id.internal, sizeof(id.internal));
+  return CGKS_OK;
+}
+
+int cgks_comm_info(const cgks_ctx* ctx, int* rank, int* nranks, int* backend) {
+  if (!ctx) return CGKS_ERR_CONFIG;
+  int r = ctx->rank, n = ctx->nranks;
+  if (ctx->comm_mode == 1) {
+    auto& A = nccl::g_api;
+    if (!A.CommCount || !A.CommUserRank || A.CommCount(ctx->comm, &n) || A.CommUserRank(ctx->comm, &r))
+      return CGKS_ERR_COMM;
+  }
+  if (rank) *rank = r;
+  if (nranks) *nranks = n;
+  if (backend) *backend = ctx->comm_mode;
   return CGKS_OK;
 }
 

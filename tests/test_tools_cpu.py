@@ -80,3 +80,36 @@ def test_bench_reference_arm_line():
     assert line["config"]["workload"] == "tgv 128x128x128" and line["config"]["global_cells"] == 128 ** 3
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_bench_launch_plan():
+    # --gpus N starts N ranks itself unless under a launcher; a mismatch is refused
+    import bench
+    what, argv = bench.launch_plan(4, {})
+    assert what == "exec"
+    assert "torch.distributed.run" in argv and "--nproc-per-node=4" in argv
+    assert argv[argv.index("--master-addr") + 1] == "127.0.0.1"
+    assert bench.launch_plan(1, {}) == ("run", None)
+    assert bench.launch_plan(2, {"WORLD_SIZE": "2"}) == ("run", None)
+    what, msg = bench.launch_plan(4, {"WORLD_SIZE": "2"})
+    assert what == "refuse" and "WORLD_SIZE=2" in msg
+
+
+def test_bench_gpus2_launches_two_ranks_cpu():
+    # the launcher end to end on CPU: the reference arm under 2 gloo ranks; rank 0 alone prints the line
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["config"]["workload"] == "tgv 512x512x128"  # north_star weak scaling: 512 x 512 x 64 per GPU
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4"], capture_output=True,
+                       text=True, timeout=60, env={**env, "WORLD_SIZE": "2"})
+    assert r.returncode == 2 and "refusing" in r.stderr
