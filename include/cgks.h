@@ -138,6 +138,12 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps);
  * NULL.  CGKS_ERR_COMM if the NCCL queries fail. */
 int cgks_comm_info(const cgks_ctx* ctx, int* rank, int* nranks, int* backend);
 
+/* Planes per z-chunk of the stage driver: 0 = each stage passes over the whole (slab) grid; C > 0 =
+ * the stages pass over z-chunks of C planes with chunk-sized reconstruction and face buffers (chosen
+ * at create when the whole-grid buffers do not fit in the free device memory, or forced by the
+ * environment variable CGKS_CHUNK=C; same results bit for bit).  -1 for a NULL context. */
+int cgks_z_chunk(const cgks_ctx* ctx);
+
 /* Set the state (user layout, rank-local block).  gradQ may be NULL (zero gradients;
  * not recommended for CGKS-5th, R26; ignored by GKS-2nd).  Resets t and the step count. */
 int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ);

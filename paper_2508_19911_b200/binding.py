@@ -63,6 +63,7 @@ _lib = None
 EXPORTS = ["cgks_scheme_defaults", "cgks_create", "cgks_local_extent", "cgks_set_state", "cgks_step",
            "cgks_get_state", "cgks_get_time", "cgks_last_error", "cgks_launches_per_step", "cgks_profile",
            "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group", "cgks_comm_info",
+           "cgks_z_chunk",
            "cgks_set_state_async", "cgks_step_async", "cgks_get_state_async", "cgks_sync", "cgks_destroy"]
 
 
@@ -106,6 +107,7 @@ def load(path: str = LIB_PATH):
     L.cgks_step_group.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int]
     ip = ctypes.POINTER(ctypes.c_int)
     L.cgks_comm_info.argtypes = [vp, ip, ip, ip]
+    L.cgks_z_chunk.argtypes = [vp]
     L.cgks_destroy.argtypes = [vp]
     L.cgks_destroy.restype = None
     _lib = L
@@ -315,6 +317,10 @@ class Solver:
         r, n, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         self._check(self._L.cgks_comm_info(self.ctx, ctypes.byref(r), ctypes.byref(n), ctypes.byref(b)))
         return r.value, n.value, b.value
+
+    def z_chunk(self):
+        """cgks_z_chunk: planes per z-chunk of the stages (0 = the whole grid per pass)."""
+        return int(self._L.cgks_z_chunk(self.ctx))
 
     def last_error(self):
         return self._L.cgks_last_error(self.ctx).decode()

@@ -124,6 +124,10 @@ struct cgks_ctx {
   bool async_latched = false;      // a batch's error record was latched into err_sticky
   cudaEvent_t ev_const = nullptr;  // end of this context's enqueued work when another takes the constants
   long long test_peer_fail = -1;   // CGKS_TEST_PEER_FAIL_STEP (NCCL ranks): emulated peer failure (tests only)
+  // z-chunked stages (grids whose whole-slab reconstruction and face buffers do not fit): chunk planes
+  // per pass (0 = the whole slab in one pass); the z axis then carries 2 stored ghost planes per side
+  // (periodic: filled by a local copy, decomposed: by the halo exchange)
+  int chunk = 0;
   int cur = 0;
   ClsTables cls;
   double Rp[ReconGen<3>::NNZ > ReconGenL<3>::NNZ ? ReconGen<3>::NNZ : ReconGenL<3>::NNZ];  // packed CLS matrix
@@ -249,6 +253,7 @@ static StageArgs stage_args(cgks_ctx* ctx, const double* Uin, double* Uout) {
   a.ts = ctx->ts;
   a.err = ctx->err;
   a.ncell = ctx->ncell;
+  a.nz = ctx->geo.n[2];
   a.necell = ctx->necell;
   a.scheme = ctx->scheme_id;
   a.nonlinear = ctx->nonlinear;
@@ -358,15 +363,62 @@ static int exchange_nccl(cgks_ctx* ctx, double* X, cudaStream_t st) {
   return nccl_check(ctx, e ? e : e2, "halo exchange");
 }
 
+// chunked periodic single context: the ghost planes are the periodic images (device copies)
+static int exchange_local(cgks_ctx* ctx, double* X, cudaStream_t st) {
+  double* Xl = lines_of(ctx, X);
+  for (int part = 0; part < (Xl ? 2 : 1); ++part) {
+    const bool l = part == 1;
+    double* B = l ? Xl : X;
+    const size_t bytes = sizeof(double) * (size_t)(2 * plane_block(ctx, l));
+    CK(cudaMemcpyAsync(low_ghost(ctx, B, l), high_send(ctx, B, l), bytes, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(high_ghost(ctx, B, l), low_send(ctx, B, l), bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return CGKS_OK;
+}
+
 static int exchange(cgks_ctx* ctx, double* X) {
   if (!ctx->geo.halo[2]) return CGKS_OK;
-  if (ctx->comm_mode == 1) return exchange_nccl(ctx, X, ctx->capturing ? ctx->cap_stream : ctx->stream);
+  cudaStream_t st = ctx->capturing ? ctx->cap_stream : ctx->stream;
+  if (ctx->comm_mode == 1) return exchange_nccl(ctx, X, st);
+  if (ctx->comm_mode == 0) return exchange_local(ctx, X, st);
   return CGKS_OK;  // group mode exchanges in cgks_step_group
+}
+
+// z-chunk c of a chunked stage: the reconstruction of its planes and their two neighbours, its fluxes,
+// the update of its cells (chunks write disjoint planes of Uout / carry and share the scratch buffers,
+// so they run in order on one stream)
+static int run_chunk(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, int stage, int c) {
+  StageArgs a = stage_args(ctx, Uin, Uout);
+  a.ck0 = c * ctx->chunk;
+  a.cn = std::min(ctx->chunk, ctx->geo.n[2] - a.ck0);
+  LaunchEnv env = env_of(ctx);
+  return ctx->ops->stage(env, a, mode, stage) ? CGKS_ERR_CUDA : CGKS_OK;
 }
 
 // one stage of a rank: halo exchange of Uin, then the stage; NCCL ranks overlap the exchange (on
 // halo_stream) with the interior reconstruction
 static int halo_stage(cgks_ctx* ctx, double* Uin, double* Uout, int mode, int stage) {
+  if (ctx->chunk) {
+    const int nch = (ctx->geo.n[2] + ctx->chunk - 1) / ctx->chunk;
+    int rc = CGKS_OK;
+    if (ctx->comm_mode == 1 && ctx->overlap && nch >= 3) {
+      // the exchange on the halo stream while the interior chunks (no ghost reads) run, then the two
+      // boundary chunks
+      cudaStream_t main = ctx->capturing ? ctx->cap_stream : ctx->stream;
+      CK(cudaEventRecord(ctx->ev_fork, main));
+      CK(cudaStreamWaitEvent(ctx->halo_stream, ctx->ev_fork, 0));
+      rc = exchange_nccl(ctx, Uin, ctx->halo_stream);
+      if (!rc) CK(cudaEventRecord(ctx->ev_join, ctx->halo_stream));
+      for (int c = 1; c < nch - 1 && !rc; ++c) rc = run_chunk(ctx, Uin, Uout, mode, stage, c);
+      if (!rc) CK(cudaStreamWaitEvent(main, ctx->ev_join, 0));
+      if (!rc) rc = run_chunk(ctx, Uin, Uout, mode, stage, 0);
+      if (!rc) rc = run_chunk(ctx, Uin, Uout, mode, stage, nch - 1);
+      return rc;
+    }
+    rc = exchange(ctx, Uin);
+    for (int c = 0; c < nch && !rc; ++c) rc = run_chunk(ctx, Uin, Uout, mode, stage, c);
+    return rc;
+  }
   if (!(ctx->geo.halo[2] && ctx->comm_mode == 1 && ctx->overlap)) {
     int rc = exchange(ctx, Uin);
     return rc ? rc : run_stage(ctx, Uin, Uout, mode, stage);
@@ -428,6 +480,7 @@ static int one_step(cgks_ctx* ctx) {
 
 static int count_launches(cgks_ctx* c) {
   int per_stage = (c->overlap ? 3 : 1) + c->dim + 1;  // overlapped halo: the reconstruction in 3 launches
+  if (c->chunk) per_stage = ((c->geo.n[2] + c->chunk - 1) / c->chunk) * (1 + c->dim + 1);
   int stages = (c->time_scheme == CGKS_TIME_S1O2) ? 1 : 2;
   return stages * per_stage + 1 + (c->comm_mode == 1 ? 1 : 0);  // + step end (+ error poison)
 }
@@ -512,6 +565,48 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   }
   ctx->nranks = P;
   ctx->rank = P > 1 ? grid->rank : 0;
+  // ---- z-chunking: stages pass over z-chunks of `chunk` planes when the whole-slab reconstruction
+  // coefficients and face records do not fit next to the state (or CGKS_CHUNK=C forces C planes)
+  {
+    const bool zper = grid->bc[2][0] == CGKS_BC_PERIODIC && grid->bc[2][1] == CGKS_BC_PERIODIC;
+    const long long nzl = grid->n[2] / P;
+    const bool can = grid->n[2] > 1 && zper && nzl >= 4 && (P == 1 || grid->nccl_id != nullptr);
+    if (can) {
+      const long long nx = grid->n[0], ny = grid->n[1];
+      const int NVc = scheme->id == CGKS_CGKS5 ? 20 : 5;
+      const int nrec = scheme->id == CGKS_CGKS5 ? 170 : 15;
+      const int ngl = 4;
+      const int nfr = scheme->id == CGKS_CGKS5 ? 30 + (scheme->lines ? 2 * ngl * 10 : 0) : 10;
+      const bool xb = !(grid->bc[0][0] == CGKS_BC_PERIODIC && grid->bc[0][1] == CGKS_BC_PERIODIC);
+      const bool yb = !(grid->bc[1][0] == CGKS_BC_PERIODIC && grid->bc[1][1] == CGKS_BC_PERIODIC);
+      const double ex = (double)(nx + (xb ? 2 : 0)) * (ny + (yb ? 2 : 0));  // extended plane
+      const double pl = (double)nx * ny;
+      const double nlin = scheme->lines ? 5.0 * 3 * ngl : 0.0;
+      const double state = 8.0 * pl * (nzl + 4) * (4.0 * (NVc + nlin));  // U[0], U[1], Us, carry (+ lines)
+      auto scratch = [&](double c) {  // reconstruction + face records of c planes
+        return 8.0 * (ex * (c + 2) * nrec + (pl + (xb ? ny : 0)) * c * nfr + (pl + (yb ? nx : 0)) * c * nfr +
+                      pl * (c + 1) * nfr);
+      };
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const double avail = 0.90 * (double)fr - 2e9;
+      const double staging_full = 8.0 * pl * nzl * (scheme->lines ? 60 : 15), staging_chunk = 8.0 * pl * nzl;
+      long long C = 0;
+      if (const char* ce = std::getenv("CGKS_CHUNK")) {
+        C = std::atoll(ce);
+      } else if (state + staging_full + scratch((double)nzl) > avail) {
+        // the largest chunk that fits (fewest passes; the reconstruction repeats 2 planes per chunk)
+        const double per_plane = scratch(2.0) - scratch(1.0);
+        C = (long long)((avail - state - staging_chunk - scratch(0.0)) / per_plane);
+        if (C < 1) C = 1;
+        if (C >= nzl) C = nzl - 1;
+        // equal chunks: C = ceil(nzl / number of passes)
+        const long long np = (nzl + C - 1) / C;
+        C = (nzl + np - 1) / np;
+      }
+      if (C > 0 && C < nzl) ctx->chunk = (int)C;
+    }
+  }
   int dim = grid->n[2] > 1 ? 3 : (grid->n[1] > 1 ? 2 : 1);
   if ((dim < 3 && grid->n[2] != 1) || (dim < 2 && grid->n[1] != 1)) {
     set_msg(ctx, "active axes must be the leading ones");
@@ -536,8 +631,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     g.n[a] = (int)grid->n[a];
     g.h[a] = (grid->hi[a] - grid->lo[a]) / grid->n[a];
     g.ih[a] = 1.0 / g.h[a];
-    if (a == 2 && slab) {  // this rank's slab; ghost planes filled by the halo exchange
-      g.n[2] = (int)(grid->n[2] / P);
+    if (a == 2 && (slab || ctx->chunk)) {  // this rank's slab; ghost planes filled by the halo exchange
+      g.n[2] = (int)(grid->n[2] / P);        // (or, chunked periodic z, by a local copy)
       g.halo[2] = 1;
       g.zoff = 2;
       ctx->zoff_global = (long long)ctx->rank * g.n[2];
@@ -656,16 +751,24 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   int nrec = ctx->scheme_id == CGKS_CGKS5 ? ctx->cls.nb * 5 : 15;
   int nff = g.nfr;
   const long long nstore = (long long)g.plane * (g.n[2] + 2 * g.zoff) * NV;  // incl. z ghost planes
+  if ((double)nstore >= 4294967296.0) {  // the reconstruction's staging map holds 32-bit element offsets
+    set_msg(ctx, "state of %lld doubles per buffer exceeds the 2^32-element limit: decompose the grid", nstore);
+    return fail(CGKS_ERR_CONFIG);
+  }
+  // chunked: the reconstruction of chunk planes k0 - 1 .. k0 + C, the face records of the chunk's planes
+  // (z: C + 1), host staging one field at a time
+  const long long rec_cells = ctx->chunk ? g.eplane * (ctx->chunk + 2) : ctx->necell;
   bool ok = alloc(&ctx->U[0], nstore) && alloc(&ctx->U[1], nstore) && alloc(&ctx->Us, nstore) &&
-            alloc(&ctx->carry, nstore) &&
-            alloc(&ctx->rec, ctx->necell * nrec) && alloc(&ctx->staging, ctx->ncell * (g.lines ? 60 : 15));
+            alloc(&ctx->carry, nstore) && alloc(&ctx->rec, rec_cells * nrec) &&
+            alloc(&ctx->staging, ctx->ncell * (ctx->chunk ? 1 : (g.lines ? 60 : 15)));
   if (ok && g.lines) {
     ctx->nl = dim * g.ngl;
     const long long nls = (long long)g.plane * (g.n[2] + 2 * g.zoff) * 5 * ctx->nl;
     ok = alloc(&ctx->Lb[0], nls) && alloc(&ctx->Lb[1], nls) && alloc(&ctx->Ls, nls) && alloc(&ctx->Lc, nls);
   }
   for (int a = 0; a < dim && ok; ++a)
-    ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] * g.fn[a][2] * nff);
+    ok = alloc(&ctx->face[a], (long long)g.fn[a][0] * g.fn[a][1] *
+                                  (ctx->chunk ? ctx->chunk + (a == 2 ? 1 : 0) : g.fn[a][2]) * nff);
   if (!ok || cudaMalloc((void**)&ctx->ts, sizeof(TimeState)) != cudaSuccess ||
       cudaMalloc((void**)&ctx->err, sizeof(ErrState)) != cudaSuccess ||
       cudaMalloc((void**)&ctx->err_sticky, sizeof(ErrState)) != cudaSuccess ||
@@ -691,7 +794,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
         const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
         {
           // [z][y][field][x]: dims (x, field, y, z)
-          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)nrec, (cuuint64_t)g.en[1], (cuuint64_t)g.en[2]};
+          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)nrec, (cuuint64_t)g.en[1],
+                                      (cuuint64_t)(ctx->chunk ? ctx->chunk + 2 : g.en[2])};
           const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.en[0] * nrec * 8,
                                      (cuuint64_t)g.eplane * nrec * 8};
           const cuuint32_t box[4] = {(cuuint32_t)tx, (cuuint32_t)nrec, by, bz};
@@ -908,6 +1012,8 @@ int cgks_comm_info(const cgks_ctx* ctx, int* rank, int* nranks, int* backend) {
   return CGKS_OK;
 }
 
+int cgks_z_chunk(const cgks_ctx* ctx) { return ctx ? ctx->chunk : -1; }
+
 static int finish_steps(cgks_ctx* ctx, int cur0, long long steps0);
 extern "C" int cgks_sync(cgks_ctx* ctx);
 // the synchronous calls first complete (and report) what the asynchronous ones enqueued
@@ -1055,6 +1161,13 @@ int cgks_set_state(cgks_ctx* ctx, const double* Q, const double* gradQ) {
     if (src) {
       if (is_device_ptr(src)) {
         dsrc = src;
+      } else if (ctx->chunk) {  // large grids: one field at a time through the staging buffer (stream order)
+        for (int f = 0; f < nf; ++f) {
+          CK(cudaMemcpyAsync(ctx->staging, src + nc * f, sizeof(double) * nc, cudaMemcpyHostToDevice, ctx->stream));
+          if (ctx->ops->pack(ctx->stream, ctx->staging, U, ctx->NV, f0 + f, 1, nc)) CK(cudaGetLastError());
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        return CGKS_OK;
       } else {
         CK(cudaMemcpyAsync(ctx->staging, src, sizeof(double) * nc * nf, cudaMemcpyHostToDevice, ctx->stream));
         dsrc = ctx->staging;
@@ -1097,6 +1210,14 @@ int cgks_set_lines(cgks_ctx* ctx, const double* L) {
   const long long nc = ctx->ncell;
   const int nf = 5 * ctx->nl;
   const double* dsrc = L;
+  if (!is_device_ptr(L) && ctx->chunk) {  // one field at a time (large grids)
+    for (int f = 0; f < nf; ++f) {
+      CK(cudaMemcpyAsync(ctx->staging, L + nc * f, sizeof(double) * nc, cudaMemcpyHostToDevice, ctx->stream));
+      if (ctx->ops->pack(ctx->stream, ctx->staging, ctx->Lb[ctx->cur], nf, f, 1, nc)) CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CGKS_OK;
+  }
   if (!is_device_ptr(L)) {
     CK(cudaMemcpyAsync(ctx->staging, L, sizeof(double) * nc * nf, cudaMemcpyHostToDevice, ctx->stream));
     dsrc = ctx->staging;
@@ -1117,6 +1238,14 @@ int cgks_get_lines(const cgks_ctx* cctx, double* L) {
   const long long nc = ctx->ncell;
   const int nf = 5 * ctx->nl;
   const bool dev = is_device_ptr(L);
+  if (!dev && ctx->chunk) {  // one field at a time (large grids)
+    for (int f = 0; f < nf; ++f) {
+      if (ctx->ops->unpack(ctx->stream, ctx->Lb[ctx->cur], ctx->staging, nf, f, 1, nc)) CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(L + nc * f, ctx->staging, sizeof(double) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CGKS_OK;
+  }
   double* ddst = dev ? L : ctx->staging;
   if (ctx->ops->unpack(ctx->stream, ctx->Lb[ctx->cur], ddst, nf, 0, nf, nc)) CK(cudaGetLastError());
   if (!dev) CK(cudaMemcpyAsync(L, ctx->staging, sizeof(double) * nc * nf, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1213,6 +1342,14 @@ int cgks_get_state(const cgks_ctx* cctx, double* Q, double* gradQ) {
   const double* U = ctx->U[ctx->cur];
   auto get = [&](double* dst, int f0, int nf) -> int {
     bool dev = is_device_ptr(dst);
+    if (!dev && ctx->chunk) {  // large grids: one field at a time through the staging buffer
+      for (int f = 0; f < nf; ++f) {
+        if (ctx->ops->unpack(ctx->stream, U, ctx->staging, ctx->NV, f0 + f, 1, nc)) CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(dst + nc * f, ctx->staging, sizeof(double) * nc, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+      CK(cudaStreamSynchronize(ctx->stream));
+      return CGKS_OK;
+    }
     double* ddst = dev ? dst : ctx->staging;
     long long n = nc * nf;
     if (ctx->ops->unpack(ctx->stream, U, ddst, ctx->NV, f0, nf, nc)) CK(cudaGetLastError());
@@ -1415,7 +1552,7 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
-    set_msg(ctx, "cgks_diagnostics: decomposed contexts are not supported (gather the state first)");
+    set_msg(ctx, "cgks_diagnostics: decomposed or z-chunked contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
   int rc = upload_constants(ctx);
@@ -1457,7 +1594,7 @@ int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
   if (ctx->geo.halo[2]) {
-    set_msg(ctx, "cgks_qcriterion: decomposed contexts are not supported (gather the state first)");
+    set_msg(ctx, "cgks_qcriterion: decomposed or z-chunked contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
   int rc = upload_constants(ctx);
@@ -1614,11 +1751,17 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
     rows.push_back({"update", (D * 30.0 + 30.0) * nc});
   }
   rows.push_back({"dt", 25.0 * D * nc});
+  if (ctx->chunk) {  // chunked stages: one launch per kernel and chunk; per launch = the chunk average
+    const double nch = (double)((ctx->geo.n[2] + ctx->chunk - 1) / ctx->chunk);
+    for (auto& r : rows)
+      if (r.first != "dt") r.second /= nch;
+  }
   int i = 0;
   double per_step = 0.0;
   const int stages = ctx->time_scheme == CGKS_TIME_S1O2 ? 1 : 2;
+  const double nch = ctx->chunk ? (double)((ctx->geo.n[2] + ctx->chunk - 1) / ctx->chunk) : 1.0;
   for (auto& r : rows) {
-    per_step += (r.first == "dt" ? 1 : stages) * r.second;
+    per_step += (r.first == "dt" ? 1 : stages * nch) * r.second;
     if (i < max) {
       std::snprintf(names + 64 * i, 64, "%s", r.first.c_str());
       flops_per_launch[i] = r.second;

@@ -52,6 +52,10 @@ struct StageArgs {
   // extended z planes [rz0, rz1) only (offsets from the first extended plane); 3 = fluxes + update only
   int part = 0;
   int rz0 = 0, rz1 = -1;
+  // z-chunked stage (large grids): cells of the planes [ck0, ck0 + cn) with the chunk's own
+  // reconstruction (planes ck0 - 1 .. ck0 + cn) and face buffers; cn < 0: the whole slab
+  int ck0 = 0, cn = -1;
+  int nz = 1;  // local cell planes
 };
 
 struct DimOps {

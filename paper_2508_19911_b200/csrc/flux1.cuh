@@ -70,7 +70,11 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
                                                 const double* __restrict__ gtab, double* __restrict__ face,
                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                 int stage, const __grid_constant__ CUtensorMap tm_rec,
-                                                const __grid_constant__ CUtensorMap tm_U, int use_tma) {
+                                                const __grid_constant__ CUtensorMap tm_U, int use_tma, int kb,
+                                                int ke, int kofs) {
+  // face planes [kb, ke) along z (a z-chunk of the stage, or all); face records of plane k at
+  // face + k * NFR * fpl (the caller shifts chunk buffers); reconstruction plane of cell k at extended
+  // plane k - elo[2] - kofs of rec (TMA coordinates; the pointer is shifted likewise)
   using FT = FluxTile1<DIM, AX, COMPACT>;
   constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT, NQ = FT::NQ;
   constexpr int NV = COMPACT ? 20 : 5;
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
   const int fn0 = c_geo.fn[AX][0];
   const int i0 = blockIdx.x * FX;
   const int j0 = AX == 1 ? blockIdx.y * FY : (AX == 2 ? blockIdx.z : blockIdx.y);
-  const int k0 = AX == 2 ? blockIdx.y * FY : blockIdx.z;
+  const int k0 = kb + (AX == 2 ? blockIdx.y * FY : blockIdx.z);
   // ---- stage the tile (as k_flux): TMA boxes when no periodic wrap, else cp.async per element
   const int x0 = AX == 0 ? i0 - 2 : i0, y0 = AX == 1 ? j0 - 1 : j0, z0 = AX == 2 ? k0 - 1 : k0;
   const bool wraps = (AX == 0 && x0 < 0 && !c_geo.bounded[0]) || (AX == 1 && y0 < 0 && !c_geo.bounded[1]) ||
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
       // tile boxes and the evaluation tables (one 1-D bulk copy) complete on one mbarrier
       mbar_init(bar, 1);
       mbar_expect_tx(bar, (unsigned)(sizeof(double) * ((FT::NREC + 5) * NT + FT::TAB)));
-      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2]);
+      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2] - kofs);
       tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
       if (COMPACT) bulk_load(tab, gtab, (unsigned)(sizeof(double) * FT::TAB), bar);
     }
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
         if (cj > jmax) cj = jmax;
       }
       if (AX == 2) {
-        const int kmax = c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0);
+        const int kmax = min(c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0), ke - 1);  // (chunk: its last cell)
         if (ck > kmax) ck = kmax;
       }
       const long long st = c_geo.en[0];  // field stride of the reconstruction array
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
   const int fl = lane / NG;  // face within the block
   const int fx = fl % FX, fy = fl / FX;
   const int i = i0 + fx, j = AX == 1 ? j0 + fy : j0, k = AX == 2 ? k0 + fy : k0;
-  const bool valid = i < fn0 && (AX != 1 || j < c_geo.fn[1][1]) && (AX != 2 || k < c_geo.fn[2][2]);
+  const bool valid = i < fn0 && (AX != 1 || j < c_geo.fn[1][1]) && k < ke;
   // tile columns of the two cells (left = side 0, right = side 1)
   const int cL = AX == 0 ? fl + 1 : fy * FX + fx;
   const int cR = AX == 0 ? fl + 2 : (fy + 1) * FX + fx;

@@ -103,13 +103,6 @@ HD void half_moments(T U, T lam, T r, double side, T* M) {  // r = 1/(2 lam)
   for (int k = 0; k < 5; ++k) M[k + 2] = U * M[k + 1] + (k + 1) * r * M[k];
 }
 
-// outputs of one Gauss point, normal frame
-template <typename T>
-struct GPOutT {
-  T Fn[5], Ft[5];
-  T QLn[5], QLt[5], QRn[5], QRt[5];
-};
-typedef GPOutT<double> GPOut;
 
 // ---------------------------------------------------------------------------
 // Half-range moment vectors and their directional derivatives.
@@ -312,303 +305,19 @@ HD void jvp_flux2(T rho, T ir, const T* U, T p, T uu, double K5, double K7, cons
   acc[4] += 0.5 * v4;
 }
 
-// per-lane parking slots (shared memory on the device) for values that live across phases
-struct ParkDev {
-  double* a;  // slots 0..19: a + slot * 128 (+ lane)
-  double* b;  // slots 20..39: b + (slot - 20) * 128 (+ lane)
-  __device__ __forceinline__ double* at(int s) const { return s < 20 ? a + s * 128 : b + (s - 20) * 128; }
-  __device__ __forceinline__ void put(int s, double v) const { *at(s) = v; }
-  __device__ __forceinline__ double get(int s) const { return *at(s); }
-  __device__ __forceinline__ void mark(int) const {}  // phase markers (used by the host flop count)
-};
-
 // ---------------------------------------------------------------------------
-// One side of the interface solver at one Gauss point (two cooperating lanes per Gauss
-// point: side 0 = left state restricted to u > 0, side 1 = right state restricted to u < 0).
-// Phases: (S) all half-range terms of this side (W0 and dW0 parts, MF3..MF5, MQ4, MQ5), as
-// values and directional derivatives of half-range moment vectors -> one exchange (lane xor 1)
-// sums the two sides -> (G) interface equilibrium g0, collision time and combined time
-// coefficients, equilibrium terms as Jacobian-vector products, everything folded into F^n,
-// F_t^n, Q^n, Q_t^n and the heat-flux scalars -> Prandtl fix and own side relaxation.
-// Both lanes run the same instruction stream.
-// Inputs in the normal frame: W (5) conservative state of this side, dW[dir][var] physical
-// derivatives (dir 0 = normal).  Outputs (normal frame): side 0 holds Fn, Ft, QLn, QLt;
-// side 1 holds Fn, Ft and its QRn, QRt in the QLn/QLt slots.  Returns false if a state
-// (own, other, or the equilibrium) is not positive.
-// ---------------------------------------------------------------------------
-template <bool COMPACT, typename T, typename X, typename P>
-HD bool gks_flux_side(int side, const T* W, const T (*dW)[5], T dt, T idt, const FluxConst& fc, const X& xchg,
-                      const P& park, GPOutT<T>& o) {
-  const T gm1 = fc.gamma - 1.0;
-  const double sgn = side == 0 ? 1.0 : -1.0;
-  // ---- (S) this side: primitives, half-range moments, and all half-range terms of Eq. (flux)
-  const T rho = W[0], ir = 1.0 / rho;
-  const T U = W[1] * ir, V = W[2] * ir, Ww = W[3] * ir;
-  const T uu2s = 0.5 * (U * U + V * V + Ww * Ww);
-  const T p = gm1 * (W[4] - rho * uu2s);
-  const bool ok = (rho > 0.0) && (p > 0.0);
-  const T ip = ok ? T(1.0) / p : T(1.0);
-  const T lam = ok ? T(0.5) * rho * ip : T(1.0);
-  const T sv = ok ? p * ir : T(0.5);  // variance 1/(2 lam)
-  const T Uv[3] = {U, V, Ww};
-  // Euler time derivative of this side (R23): dW/dt = rho <A psi> = -sum_al DF_al(W) dW_al (full
-  // moments, compatibility R16) as Jacobian-vector products
-  T dtw[5] = {0, 0, 0, 0, 0};
-  {
-    const Dprim<T> q0 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[0]);
-    jvp_flux<0>(rho, Uv, p, W[4], dW[0], q0, -1.0, dtw);
-    const Dprim<T> q1 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[1]);
-    jvp_flux<1>(rho, Uv, p, W[4], dW[1], q1, -1.0, dtw);
-    const Dprim<T> q2 = dprim(ir, Uv, uu2s, fc.gamma - 1.0, dW[2]);
-    jvp_flux<2>(rho, Uv, p, W[4], dW[2], q2, -1.0, dtw);
-  }
-  // x1: 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3 = rho <u psi>, 25-29 MF4 = rho <u (a.u) psi>,
-  // 30-34 MF5 = rho <u A psi>, 35-39 MQ4 = rho <(a.u) psi>, 40-44 MQ5 = rho <A psi>, 45 p (half ranges)
-  T x1[46];
-#pragma unroll
-  for (int i = 0; i < 45; ++i) x1[i] = 0.0;
-  x1[45] = p;
-  {
-    T M[7];
-    half_moments(U, lam, sv, sgn, M);  // H(u) or 1-H(u)
-    Tg<T> tg;
-    tg_value(V, Ww, sv, fc.N, tg);
-    const RW<T> G00 = rw_value<0, 0>(tg, rho), G10 = rw_value<1, 0>(tg, rho), G01 = rw_value<0, 1>(tg, rho);
-    col_value<0>(M, G00, x1 + 0);
-    col_value<1>(M, G00, x1 + 20);
-    // directional derivatives along dW_n, dW_t1, dW_t2 (micro-slopes a_al) and dW/dt (A)
-#pragma unroll
-    for (int dir = 0; dir < 4; ++dir) {
-      const T* d = dir < 3 ? dW[dir] : dtw;
-      const Dprim<T> q = dprim(ir, Uv, uu2s, fc.gamma - 1.0, d);
-      const T dlam = lam * (q.dr * ir - q.dp * ip);
-      const T ds = -2.0 * sv * sv * dlam;
-      T dM[5];
-      moments_deriv(M, U, lam, sv, q.du[0], dlam, dM);
-      Tg<T> dt;
-      tg_deriv(V, Ww, sv, fc.N, q.du[1], q.du[2], ds, dt);
-      const RW<T> H00 = rw_deriv<0, 0>(tg, dt, rho, q.dr);
-      if (dir == 0) {
-        col_deriv<0>(M, dM, G00, H00, x1 + 5);
-        col_deriv<1>(M, dM, G00, H00, x1 + 35);
-        col_deriv<2>(M, dM, G00, H00, x1 + 25);
-      } else if (dir == 1) {
-        const RW<T> H10 = rw_deriv<1, 0>(tg, dt, rho, q.dr);
-        col_deriv<0>(M, dM, G00, H00, x1 + 10);
-        col_deriv<0>(M, dM, G10, H10, x1 + 35);
-        col_deriv<1>(M, dM, G10, H10, x1 + 25);
-      } else if (dir == 2) {
-        const RW<T> H01 = rw_deriv<0, 1>(tg, dt, rho, q.dr);
-        col_deriv<0>(M, dM, G00, H00, x1 + 15);
-        col_deriv<0>(M, dM, G01, H01, x1 + 35);
-        col_deriv<1>(M, dM, G01, H01, x1 + 25);
-      } else {
-        col_deriv<0>(M, dM, G00, H00, x1 + 40);
-        col_deriv<1>(M, dM, G00, H00, x1 + 30);
-      }
-    }
-  }
-  // ---- exchange 1: W0, dW0 = sum of the two half-range contributions
-  park.mark(1);  // from here to mark 5 both lanes compute the same values (counted once)
-  const bool ok_other = xchg.flag(ok);
-  T other_p;
-  {
-#pragma unroll
-    for (int i = 0; i < 46; ++i) {
-      const T y = xchg(x1[i]);
-      if (i < 45)
-        x1[i] += y;
-      else
-        other_p = y;
-    }
-  }
-  // park the summed half-range terms and this side's W, dW/dt until the final phase
-#pragma unroll
-  for (int i = 0; i < 25; ++i) park.put(i, x1[20 + i]);
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    park.put(25 + i, dtw[i]);
-    park.put(30 + i, W[i]);
-  }
-  bool good = ok && ok_other;
-  const T pL = side == 0 ? p : other_p, pR = side == 0 ? other_p : p;
-  // ---- (G) interface equilibrium g0 (R13, R14)
-  const T r0 = x1[0], i0 = 1.0 / r0;
-  const T U0 = x1[1] * i0, V0 = x1[2] * i0, Ww0 = x1[3] * i0;
-  const T uu2 = 0.5 * (U0 * U0 + V0 * V0 + Ww0 * Ww0);
-  const T p0 = gm1 * (x1[4] - r0 * uu2);
-  good = good && (r0 > 0.0) && (p0 > 0.0);
-  const T l0 = good ? T(0.5) * r0 / p0 : T(1.0);
-  // collision time (R17) and combined time coefficients:
-  // F^n = sum alpha_k MF_k, F_t^n = sum beta_k MF_k (E2 = e^{-dt/(2tau)}, tau = 0 -> Euler limit)
-  // one reciprocal serves 1/p0 and 1/(pL + pR)
-  const T rpp = 1.0 / (p0 * (pL + pR));
-  const T jump = fabs(pL - pR) * (p0 * rpp);
-  // mu / p0 with mu = mu(T0), T0 = p0 / rho0 (Sutherland): mu(T0) / p0 = mu (1+S) sqrt(T0) / (rho0 (T0+S))
-  T mu_p0 = fc.mu * ((pL + pR) * rpp);
-  if (fc.suth > 0.0) {
-    const T T0 = p0 * i0;
-    mu_p0 = fc.mu * (1.0 + fc.suth) * sqrt(T0) * i0 / (T0 + fc.suth);
-  }
-  const T tau = (fc.mu > 0.0) ? (mu_p0 + fc.tau_C * jump * dt) : (fc.tau_eps + fc.tau_C * jump) * dt;
-  // accumulators: Fn, Ft, Qn, Qt, and the heat-flux scalars qn, qt of the Prandtl fix (R20):
-  // q = sum_k alpha'_k s_k with s_k = qF(MF_k) - U0n qF(MQ_k), alpha'_0 = alpha_0 - 1,
-  // beta'_2 = beta_2 - 1 (non-equilibrium part f - (T g0 + T^2/2 Abar g0))
-  // (the time coefficients and the accumulators are formed after the equilibrium Jacobian-vector
-  // products, so that 24 values are not live across them -- tau and W0 stay live instead: the phase
-  // then fits 168 registers without stack spills; flux 2.21 -> 2.17 ms)
-  T al[6], be[6];  // combined time coefficients (computed after the Jacobian-vector products)
-  T acc[22];
-  {
-    // equilibrium terms (full Maxwellian g0): MF0 = F_n(W0), MQa = rho0 <(abar.u) psi> =
-    // sum_al DF_al(W0) dW0_al, MF1 = rho0 <u (abar.u) psi> = sum_al DH_al(W0) dW0_al,
-    // MF2 = rho0 <u Abar psi> = DF_n(W0) (rho0 <Abar psi>) = -DF_n(W0) MQa (compatibility R16)
-    const T U0v[3] = {U0, V0, Ww0};
-    const T uu0 = 2.0 * uu2;
-    const double K5 = fc.N + 5.0, K7 = fc.N + 7.0;
-    T MQa[1][5], MF1[1][5], MF2[1][5], MF0[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) MQa[0][i] = MF1[0][i] = MF2[0][i] = 0.0;
-    {
-      const T* d0 = x1 + 5;
-      const Dprim<T> q0 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d0);
-      jvp_flux<0>(r0, U0v, p0, x1[4], d0, q0, 1.0, MQa[0]);
-      jvp_flux2<0>(r0, i0, U0v, p0, uu0, K5, K7, q0, MF1[0]);
-      const T* d1 = x1 + 10;
-      const Dprim<T> q1 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d1);
-      jvp_flux<1>(r0, U0v, p0, x1[4], d1, q1, 1.0, MQa[0]);
-      jvp_flux2<1>(r0, i0, U0v, p0, uu0, K5, K7, q1, MF1[0]);
-      const T* d2 = x1 + 15;
-      const Dprim<T> q2 = dprim(i0, U0v, uu2, fc.gamma - 1.0, d2);
-      jvp_flux<2>(r0, U0v, p0, x1[4], d2, q2, 1.0, MQa[0]);
-      jvp_flux2<2>(r0, i0, U0v, p0, uu0, K5, K7, q2, MF1[0]);
-      const Dprim<T> qa = dprim(i0, U0v, uu2, fc.gamma - 1.0, MQa[0]);
-      jvp_flux<0>(r0, U0v, p0, x1[4], MQa[0], qa, -1.0, MF2[0]);
-    }
-    {
-      const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation
-      const T E2 = 1.0 - m2;
-      const T c3 = tau * m2 * (3.0 - E2) * idt;
-      const T qq = 4.0 * tau * m2 * m2 * idt * idt;
-      al[0] = 1.0 - c3;
-      be[0] = qq;
-      al[1] = 2.0 * tau * c3 - tau * (1.0 + 2.0 * E2 - E2 * E2);
-      be[1] = 4.0 * tau * m2 * (dt * E2 - 2.0 * tau * m2) * idt * idt;
-      al[2] = -tau + tau * c3;
-      be[2] = 1.0 - tau * qq;
-      al[3] = c3;
-      be[3] = -qq;
-      al[4] = -2.0 * tau * c3 + tau * E2 * (2.0 - E2);
-      be[4] = -be[1];
-      al[5] = -tau * c3;
-      be[5] = tau * qq;
-    }
-    MF0[0] = r0 * U0;
-    MF0[1] = r0 * U0 * U0 + p0;
-    MF0[2] = r0 * U0 * V0;
-    MF0[3] = r0 * U0 * Ww0;
-    MF0[4] = U0 * (x1[4] + p0);
-    const T sMF0 = qF(MF0, U0, V0, Ww0, uu2), sMF1 = qF(MF1[0], U0, V0, Ww0, uu2),
-            sMF2 = qF(MF2[0], U0, V0, Ww0, uu2), sMQa = qF(MQa[0], U0, V0, Ww0, uu2);
-    {
-      const T sW = qF(x1, U0, V0, Ww0, uu2);  // qF(W0); MQ0 = MQ3 = W0
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        acc[i] = 0.0;
-        acc[5 + i] = 0.0;
-        acc[10 + i] = (al[0] + al[3]) * x1[i];
-        acc[15 + i] = (be[0] + be[3]) * x1[i];
-      }
-      acc[20] = -U0 * sW * (al[0] - 1.0 + al[3]);
-      acc[21] = -U0 * sW * (be[0] + be[3]);
-    }
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const T mf0 = MF0[i], mf1 = MF1[0][i], mf2 = MF2[0][i], mqa = MQa[0][i];
-      acc[i] += al[0] * mf0 + al[1] * mf1 + al[2] * mf2;
-      acc[5 + i] += be[0] * mf0 + be[1] * mf1 + be[2] * mf2;
-      acc[10 + i] += (al[1] - al[2]) * mqa;  // MQ1 = MQa, MQ2 = -MQa (compatibility)
-      acc[15 + i] += (be[1] - be[2]) * mqa;
-    }
-    // s0 = qF(MF0) - U0n qF(W0) (W0 part added above), s1 = qF(MF1) - U0n qF(MQa), s2 = qF(MF2) + U0n qF(MQa)
-    acc[20] += (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) + al[2] * (sMF2 + U0 * sMQa);
-    acc[21] += be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
-  }
-  // ---- half-range terms of both sides (summed by the exchange): k = 3, 4, 5 of Eq. (flux)
-  T dtW[5], Wown[5];
-  {
-    T v3[5], v4[5], v5[5], q4[5], q5[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      v3[i] = park.get(i);
-      v4[i] = park.get(5 + i);
-      v5[i] = park.get(10 + i);
-      q4[i] = park.get(15 + i);
-      q5[i] = park.get(20 + i);
-      dtW[i] = park.get(25 + i);
-      Wown[i] = park.get(30 + i);
-    }
-    const T s3 = qF(v3, U0, V0, Ww0, uu2);
-    const T s4 = qF(v4, U0, V0, Ww0, uu2) - U0 * qF(q4, U0, V0, Ww0, uu2);
-    const T s5 = qF(v5, U0, V0, Ww0, uu2) - U0 * qF(q5, U0, V0, Ww0, uu2);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
-      acc[5 + i] += be[3] * v3[i] + be[4] * v4[i] + be[5] * v5[i];
-      acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
-      acc[15 + i] += be[4] * q4[i] + be[5] * q5[i];
-    }
-    acc[20] += al[3] * s3 + al[4] * s4 + al[5] * s5;
-    acc[21] += be[3] * s3 + be[4] * s4 + be[5] * s5;
-  }
-  // ---- Prandtl fix (R20) and outputs
-  if (fc.Pr != 1.0) {
-    const double pf = fc.pfix;
-    acc[4] += pf * acc[20];
-    acc[9] += pf * acc[21];
-  }
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    o.Fn[i] = acc[i];
-    o.Ft[i] = acc[5 + i];
-  }
-  park.mark(5);  // end of the part both lanes compute identically
-  if (COMPACT) {
-    // side-state relaxation of this side (R23)
-    // ee = exp(-dt / tau0) with tau0 = C |pL - pR| / (pL + pR) dt = rC dt: exp(-1 / rC), which
-    // is below 1e-304 for rC < 1/700 (smooth regions) and is then taken as 0 -- the reciprocal is
-    // only formed in its safe range (no division slow path for tau0 -> 0)
-    const T rC = fc.relax_C * jump;
-    const T ee = (rC > 1.0 / 700.0) ? exp(-1.0 / fmax(rC, T(1.0 / 700.0))) : T(0.0);
-    const T w = 1.0 - ee;
-#ifdef __CUDA_ARCH__
-    if constexpr (std::is_same<T, double>::value) {
-      if (__all_sync(0xffffffffu, ee == 0.0)) {  // smooth flow in the whole warp: the interface values
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-          o.QLn[i] = acc[10 + i];
-          o.QLt[i] = acc[15 + i];
-        }
-        return good;
-      }
-    }
-#endif
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      o.QLn[i] = w * acc[10 + i] + ee * Wown[i];
-      o.QLt[i] = w * acc[15 + i] + ee * dtW[i];
-    }
-  }
-  return good;
-}
-
-
-// ---------------------------------------------------------------------------
-// One lane per Gauss point (k_flux1): the same interface solver as gks_flux_side, with both sides'
-// half-range terms computed by one lane (no lane exchange, the interface phase executed once).
-// side_terms adds one side's half-range contributions into x1[0..44] (layout of gks_flux_side:
-// 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3, 25-29 MF4, 30-34 MF5, 35-39 MQ4, 40-44 MQ5) and
-// returns the side's pressure, positivity and Euler time derivative dW/dt (R23).
+// The interface solver at one Gauss point, run by one lane (k_flux1):
+//   (S) side_terms, once per side: all half-range terms of Eq. (flux) of that side (W0 and dW0 parts,
+//       MF3..MF5, MQ4, MQ5) as values and directional derivatives of half-range moment vectors,
+//       accumulated into x1[0..44]: 0-4 W0 part (R13), 5-19 dW0 parts (R14), 20-24 MF3 =
+//       rho <u psi>, 25-29 MF4 = rho <u (a.u) psi>, 30-34 MF5 = rho <u A psi>, 35-39 MQ4 =
+//       rho <(a.u) psi>, 40-44 MQ5 = rho <A psi> (half ranges); also the side's pressure, positivity
+//       and Euler time derivative dW/dt (R23, for the side relaxation);
+//   (G) interface_terms, once: interface equilibrium g0, collision time and combined time
+//       coefficients, equilibrium terms as Jacobian-vector products, everything folded into F^n,
+//       F_t^n, Q^n, Q_t^n and the heat-flux scalars of the Prandtl fix;
+//   then the side relaxation (relax_ee) of both sides.
+// All in the normal frame (normal = first axis; dW[dir][var], dir 0 = normal).
 // ---------------------------------------------------------------------------
 template <typename T>
 HD bool side_terms(double sgn, const T* W, const T (*dW)[5], const FluxConst& fc, T* x1, T& p_out, T* dtw) {
@@ -673,7 +382,7 @@ HD bool side_terms(double sgn, const T* W, const T (*dW)[5], const FluxConst& fc
   return ok;
 }
 
-// Interface phase (G) of gks_flux_side from the summed half-range terms: x1[0..19] in registers, the
+// Interface phase (G) from the summed half-range terms: x1[0..19] in registers, the
 // half-range vectors x1[20..44] in parking slots 0..24 (get(i)).  Writes acc[0..9] = F^n, F_t^n
 // (Prandtl fix applied) and acc[10..19] = Q^n, Q_t^n of the interface, and the relative pressure jump
 // |pL - pR| / (pL + pR) for the side relaxation.  Returns the positivity of the equilibrium state.
@@ -788,7 +497,8 @@ HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& f
 }
 
 // side-state relaxation weight (R23): ee = exp(-dt / tau0), tau0 = C |pL - pR| / (pL + pR) dt,
-// taken as 0 below 1e-304 (smooth flow; see gks_flux_side)
+// which is below 1e-304 for C jump < 1/700 (smooth regions) and is then taken as 0: the reciprocal is only
+// formed in its safe range (no division slow path for tau0 -> 0)
 template <typename T>
 HD T relax_ee(T jump, const FluxConst& fc) {
   const T rC = fc.relax_C * jump;

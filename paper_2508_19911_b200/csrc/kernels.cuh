@@ -2,9 +2,9 @@
 //
 //   k_recon5   compact CLS quartic coefficients per cell, GENO folded in
 //   k_recon2   GKS-2nd least-squares slopes with Venkatakrishnan limiting
-//   k_flux     one thread per (face, Gauss point): evaluate both sides, gas-kinetic
+//   k_flux1    one thread per (face, Gauss point): evaluate both sides, gas-kinetic
 //              flux + interface values, 2x2 Gauss face average by warp
-//              shuffles, one face record per face
+//              shuffles, one face record per face (flux1.cuh)
 //   k_update   residual L, dL/dt, Gauss-theorem gradients and the
 //              S2O4 / S1O2 stage combinations
 //   k_dt       CFL candidate per cell, warp-shuffle + block min, atomicMin
@@ -488,374 +488,13 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 }
 
 // ---------------------------------------------------------------------------
-// K2: interface flux.  Two lanes per (face, Gauss point): lane side 0 evaluates the left
-// cell at its +1/2 face, lane side 1 the right cell at its -1/2 face; they cooperate on
-// the gas-kinetic solver through shuffles (gks_flux_side).  2*NG consecutive lanes per face.
+// K2: interface flux, one lane per (face, Gauss point): flux1.cuh (k_flux1).
 // Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
 // The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
 // ---------------------------------------------------------------------------
-struct XchgDev {
-  __device__ __forceinline__ double operator()(double x) const { return __shfl_xor_sync(0xffffffffu, x, 1); }
-  __device__ __forceinline__ bool flag(bool b) const { return __shfl_xor_sync(0xffffffffu, (int)b, 1) != 0; }
-};
-
-#ifndef CGKS_FYZ
-#define CGKS_FYZ 4
-#endif
 #ifndef CGKS_FLUX_MINB
 #define CGKS_FLUX_MINB 3
 #endif
-
-// flux kernel geometry: 128 threads = FPB faces, 2*NG lanes per face.  x-faces: a run of FPB
-// faces along x (tile: FPB + 1 cells of one row).  y-/z-faces: a patch of FX faces along x by
-// FY faces along the normal axis (tile: FX x (FY + 1) cells, 32-byte x-runs), so each staged
-// cell serves FY / (FY + 1) faces instead of 1/2.
-template <int DIM, int AX, bool COMPACT>
-struct FluxTile {
-  static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
-  static constexpr int LPF = 2 * NG;                         // lanes per face
-  static constexpr int FPB = 128 / LPF;                      // faces per block
-  static constexpr int FY = AX == 0 ? 1 : (AX == 2 ? CGKS_FYZ : 4);  // faces along the normal axis
-  static constexpr int FX = FPB / FY;                        // faces along x
-  // tile cells (x-faces: cells i0 - 2 .. i0 + FPB - 1, of which the first feeds no face: TMA rows
-  // start at an even cell and span a multiple of 16 bytes)
-  static constexpr int NT = AX == 0 ? FPB + 2 : FX * (FY + 1);
-  static constexpr int TX = AX == 0 ? NT : FX;               // cells of the tile along x
-  static constexpr int TN = AX == 0 ? 1 : FY + 1;            // cells of the tile along the normal axis
-  static constexpr int NB = Sten<DIM>::NB;
-  static constexpr int NREC = COMPACT ? NB * 5 : 15;         // per-cell reconstruction fields
-  static constexpr int NFLD = NREC + 5;                      // + the cell averages Q
-  static constexpr int NQ = DIM + 1;                         // value + DIM derivatives
-  // per-(side, quantity) table row: even with TS / 2 odd, so 128-bit loads of entry pairs are aligned
-  // and conflict-free across the 8 rows a warp reads
-  static constexpr int TS = ((NB / 2) % 2 == 1) ? NB : NB + 2;
-  static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;      // face evaluation tables
-  // Tile layout = the TMA box layouts: reconstruction fields, then the cell averages; cell c =
-  // (normal index) * TX + x index.
-  // reconstruction fields ([z][y][field][x] arrays): x-faces [field][cell], y- and z-faces
-  // [normal index][field][x index] (field stride FX); cell averages ([z][field][y][x] arrays): x- and
-  // y-faces [field][cell] (field stride NT), z-faces [cz][field][cx]
-  static constexpr int FS = AX == 0 ? NT : FX;
-  __host__ __device__ static constexpr int cbase(int c, int nfield) {
-    return AX == 0 ? c : (c / FX) * nfield * FX + c % FX;
-  }
-  static constexpr int FSU = AX == 2 ? FX : NT;
-  __host__ __device__ static constexpr int cbaseU(int c) { return AX == 2 ? (c / FX) * 5 * FX + c % FX : c; }
-  static constexpr int STILE = (NREC * NT + 15) / 16 * 16;   // start of the cell-average tile (128-byte aligned)
-  // the tile region is reused for parking slots 20..39 after the evaluation
-  static constexpr int TILE = STILE + 5 * NT > 20 * 128 ? STILE + 5 * NT : 20 * 128;
-  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB + 20 * 128) + 16; }
-};
-
-template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR = false>
-__global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux(const double* __restrict__ U, const double* __restrict__ rec,
-                                               const double* __restrict__ gtab, double* __restrict__ face,
-                                               const TimeState* __restrict__ ts, ErrState* __restrict__ err,
-                                               int stage, const __grid_constant__ CUtensorMap tm_rec,
-                                               const __grid_constant__ CUtensorMap tm_U, int use_tma) {
-  using FT = FluxTile<DIM, AX, COMPACT>;
-  constexpr int NG = FT::NG, NB = FT::NB, NT = FT::NT;
-  constexpr int NV = COMPACT ? 20 : 5;
-  constexpr int NF = COMPACT ? 30 : 10;
-  constexpr int NR = COMPACT ? 20 : 10;  // values each lane reduces over the Gauss points
-  extern __shared__ __align__(128) double smem[];
-  double* tile = smem;                            // reconstruction fields, then Q (TMA box layout)
-  double* tab = smem + FT::TILE;                  // [side][quantity][NB] face evaluation tables
-  double* scratch = tab + FT::TAB;                // [20][128] evaluation results, then parking slots
-  uint64_t* bar = reinterpret_cast<uint64_t*>(scratch + 20 * 128);  // TMA completion barrier
-  constexpr int FX = FT::FX, FY = FT::FY;
-  const int fn0 = c_geo.fn[AX][0];
-  // block origin: face (i0, j0, k0); y-/z-faces cover FY faces along their normal axis
-  const int i0 = blockIdx.x * FX;
-  // (z-faces: grid (x, z, y), so the blocks sharing a tile plane run close together and the
-  // shared plane is still in L2)
-  const int j0 = AX == 1 ? blockIdx.y * FY : (AX == 2 ? blockIdx.z : blockIdx.y);
-  const int k0 = AX == 2 ? blockIdx.y * FY : blockIdx.z;
-  // ---- stage the tile: the cells on both sides of the block's faces (x-contiguous runs).
-  // TMA: one 4-D box per array (reconstruction fields, cell averages) issued by one thread, landing
-  // on an mbarrier -- used when the tile needs no periodic wrap (all blocks but the first along a
-  // periodic normal axis); otherwise cp.async per element into the same layout.
-  // (the innermost TMA coordinate must be 16-byte aligned: x-tiles start at the even cell i0 - 2)
-  const int x0 = AX == 0 ? i0 - 2 : i0, y0 = AX == 1 ? j0 - 1 : j0, z0 = AX == 2 ? k0 - 1 : k0;
-  const bool wraps = (AX == 0 && x0 < 0 && !c_geo.bounded[0]) || (AX == 1 && y0 < 0 && !c_geo.bounded[1]) ||
-                     (AX == 2 && z0 < 0 && !c_geo.bounded[2]);
-  const bool tma = !BOX && use_tma && !wraps;
-  if (tma) {
-    if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
-      mbar_expect_tx(bar, (unsigned)(sizeof(double) * (FT::NREC + 5) * NT));
-      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2]);  // (x, field, y, z)
-      tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
-    }
-  } else {
-    // Each thread serves one tile cell (index math once) and a strided subset of its fields.
-    constexpr int TPC = 128 / NT;  // threads per cell
-    const int c = threadIdx.x % NT, fsub = threadIdx.x / NT;
-    if (fsub < TPC) {
-      int ci, cj = j0, ck = k0;
-      if (AX == 0) {
-        ci = i0 - 2 + c;
-        if (c_geo.bounded[0] && ci < -1) ci = -1;  // column 0 feeds no face
-      } else {
-        ci = i0 + c % FX;
-        if (AX == 1) cj += c / FX - 1;
-        if (AX == 2) ck += c / FX - 1;
-      }
-      // clamp the ragged tails (those cells only feed faces that are not stored)
-      const int imax = c_geo.n[0] - 1 + (c_geo.bounded[0] ? 1 : 0);
-      if (ci > imax) ci = imax;
-      if (AX == 1) {
-        const int jmax = c_geo.n[1] - 1 + (c_geo.bounded[1] ? 1 : 0);
-        if (cj > jmax) cj = jmax;
-      }
-      if (AX == 2) {
-        const int kmax = c_geo.n[2] - 1 + (c_geo.bounded[2] ? 1 : 0);
-        if (ck > kmax) ck = kmax;
-      }
-      const long long st = c_geo.en[0];  // field stride of the reconstruction array
-      // asynchronous global -> shared copies (LDGSTS): all in flight at once; running addresses
-      const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
-      unsigned dst = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NREC) + fsub * FT::FS);
-#pragma unroll 4
-      for (int fld = fsub; fld < FT::NREC; fld += TPC) {
-        cp_async8s(dst, src);
-        src += TPC * st;
-        dst += TPC * FT::FS * (unsigned)sizeof(double);
-      }
-      double* sdst = tile + FT::STILE + FT::cbaseU(c);
-      if (BOX) {
-        for (int v = fsub; v < 5; v += TPC) sdst[v * FT::FSU] = ld_state<BOX>(U, NV, v, ci, cj, ck);
-      } else {
-        const double* ub = U + sidx(NV, 0, wrap_ax(0, ci), wrap_ax(1, cj), wrap_ax(2, ck));
-        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FSU, ub + v * c_geo.plane);
-      }
-    }
-  }
-  if (COMPACT)
-    for (int q = threadIdx.x; q < 2 * FT::NQ * FT::TS; q += blockDim.x) cp_async8(tab + q, gtab + q);  // padded rows
-  // block-uniform early exit (the flag can be raised by another block while this one starts); the
-  // copies are issued first so that they overlap this barrier, and are drained before an exit
-  const bool stop = __syncthreads_or(err->code != 0);  // also orders the barrier init before the waits
-  cp_async_wait_all();
-  if (tma) mbar_wait(bar, 0);
-  if (stop) return;
-  __syncthreads();
-
-  const double dt = ts->dt;
-  const int lane = threadIdx.x;
-  const int side = lane & 1;
-  const int gp = (lane >> 1) % NG;
-  const int fl = lane / FT::LPF;  // face within the block
-  const int fx = fl % FX, fy = fl / FX;
-  const int i = i0 + fx, j = AX == 1 ? j0 + fy : j0, k = AX == 2 ? k0 + fy : k0;
-  const bool valid = i < fn0 && (AX != 1 || j < c_geo.fn[1][1]) && (AX != 2 || k < c_geo.fn[2][2]);
-  // tile column of this lane's cell
-  const int c = AX == 0 ? fl + side + 1 : (fy + side) * FX + fx;
-  const double* tc = tile + FT::cbase(c, FT::NREC);           // field f at tc[f * FS]
-  const double* sc = tile + FT::STILE + FT::cbaseU(c);        // cell average v at sc[v * FSU]
-
-  // normal frame: normal first, then the cyclic transverse axes t1 = AX+1, t2 = AX+2 (bit-exact permutation)
-  constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
-  // inverse widths of this lane's cell (the left cell of the face for side 0): uniform or per cell (R37)
-  double ihc[3] = {0.0, 0.0, 0.0};
-  if (STR) {
-    const int cc[3] = {AX == 0 ? i - 1 + side : i, AX == 1 ? j - 1 + side : j, AX == 2 ? k - 1 + side : k};
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) ihc[a] = icw(a, min(cc[a], c_geo.n[a] + 1));
-  }
-  double wn[5], dn[3][5];
-  if (COMPACT) {
-    // Evaluation of the side's quartic at the face Gauss points in the face-plane
-    // parity form: with the normal coordinate fixed, p_d at (+-s, +-s) is a sign character of
-    // the transverse exponents times a constant, so one pass over the coefficients gives the
-    // value or one derivative at all NG Gauss points.  Lane gp computes quantity q = gp
-    // (0 value, 1 d/dn, 2 d/dtA, 3 d/dtB) and scatters the NG results through shared memory.
-    constexpr int NQ = FT::NQ;
-    constexpr int TA = DIM == 3 ? P1 : (DIM == 2 ? 1 - AX : 0);  // active transverse axes
-    constexpr int TB = DIM == 3 ? P2 : 0;
-    const double* Tb = tab + side * NQ * FT::TS;
-    double* xs = scratch;  // exchange slots [q*5 + v][128]
-    for (int q = gp; q < NQ; q += NG) {
-      const double* T = Tb + q * FT::TS;
-      double S[5][NG];
-#pragma unroll
-      for (int v = 0; v < 5; ++v)
-#pragma unroll
-        for (int cc = 0; cc < NG; ++cc) S[v][cc] = 0.0;
-#pragma unroll
-      for (int k2 = 0; k2 < NB; k2 += 2) {
-        const double2 tt = *reinterpret_cast<const double2*>(T + k2);  // table entries k2, k2 + 1
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kk = k2 + h;
-          const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
-                                   : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
-          const double t = h ? tt.y : tt.x;
-#pragma unroll
-          for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * FT::FS], t, S[v][cls]);
-        }
-      }
-      const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);  // derivative along tA / tB flips that parity
-      // point g2 = (sA, sB) = (bit 0, bit 1) takes S0 + sA S1 + sB S2 + sA sB S3 = a_sA + sB b_sA with
-      // a+- = S0 +- S1, b+- = S2 +- S3 (8 additions for the 4 points), times chi = sA and / or sB for
-      // the transverse derivatives, applied as a sign-bit flip (integer pipe, no multiplication)
-      unsigned neg[NG];
-#pragma unroll
-      for (int g2 = 0; g2 < NG; ++g2)
-        neg[g2] = (((flip & 1) && !(g2 & 1)) ? 1u : 0u) ^ (((flip & 2) && !(g2 & 2)) ? 1u : 0u);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        double r[NG];
-        if constexpr (NG == 1) {
-          r[0] = S[v][0];
-        } else {
-          const double ap = S[v][0] + S[v][1], am = S[v][0] - S[v][1];
-          if constexpr (NG == 2) {
-            r[0] = am;
-            r[1] = ap;
-          } else {
-            const double bp = S[v][2] + S[v][3], bm = S[v][2] - S[v][3];
-            r[0] = am - bm;
-            r[1] = ap - bp;
-            r[2] = am + bm;
-            r[3] = ap + bp;
-          }
-        }
-#pragma unroll
-        for (int g2 = 0; g2 < NG; ++g2) {
-          const long long bits = __double_as_longlong(r[g2]) ^ ((long long)neg[g2] << 63);
-          xs[(lane - 2 * gp + 2 * g2) + (q * 5 + v) * 128] = __longlong_as_double(bits);
-        }
-      }
-    }
-    __syncwarp();
-    double W[5], dW[NQ][5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      W[v] = sc[v * FT::FSU] + xs[v * 128 + lane];
-#pragma unroll
-      for (int q = 1; q < NQ; ++q) dW[q][v] = xs[(q * 5 + v) * 128 + lane];
-    }
-    __syncwarp();  // the exchange slots are reused as parking slots by gks_flux_side
-    // physical derivatives along AX, TA, TB, placed in the normal-frame slots
-    double g[3][5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      g[0][v] = g[1][v] = g[2][v] = 0.0;
-      g[AX][v] = dW[1][v] * (STR ? ihc[AX] : c_geo.ih[AX]);
-      if (DIM > 1) g[TA][v] = dW[2 % NQ][v] * (STR ? ihc[TA] : c_geo.ih[TA]);
-      if (DIM > 2) g[TB][v] = dW[3 % NQ][v] * (STR ? ihc[TB] : c_geo.ih[TB]);
-    }
-    wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
-    const int pp[3] = {P0, P1, P2};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      dn[d][0] = g[pp[d]][0];
-      dn[d][1] = g[pp[d]][1 + P0];
-      dn[d][2] = g[pp[d]][1 + P1];
-      dn[d][3] = g[pp[d]][1 + P2];
-      dn[d][4] = g[pp[d]][4];
-    }
-  } else {
-    double W[5], dW[3][5];
-    const double hs = side ? -0.5 : 0.5;
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      const double q = sc[v * FT::FSU];
-      W[v] = q + hs * tc[(AX * 5 + v) * FT::FS];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) dW[a][v] = tc[(a * 5 + v) * FT::FS] * (STR ? ihc[a] : c_geo.ih[a]);
-    }
-    wn[0] = W[0]; wn[1] = W[1 + P0]; wn[2] = W[1 + P1]; wn[3] = W[1 + P2]; wn[4] = W[4];
-    const int pp[3] = {P0, P1, P2};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      dn[d][0] = dW[pp[d]][0];
-      dn[d][1] = dW[pp[d]][1 + P0];
-      dn[d][2] = dW[pp[d]][1 + P1];
-      dn[d][3] = dW[pp[d]][1 + P2];
-      dn[d][4] = dW[pp[d]][4];
-    }
-  }
-  // the tile is dead from here on: its space (with the scratch) holds the per-lane parking slots
-  __syncthreads();
-  GPOut o;
-  const bool ok =
-      gks_flux_side<COMPACT>(side, wn, dn, dt, ts->idt, c_fc, XchgDev(), ParkDev{scratch + lane, smem + lane}, o);
-  if (valid && !ok && side == 0) flag_error(err, 3, 1, stage, ts->steps, i, j, k);
-  const int fn1 = c_geo.fn[AX][1];
-  const long long fpl = (long long)fn0 * fn1;
-  constexpr int NGL_ = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
-  constexpr int NFR = COMPACT ? (LINES ? 30 + 2 * NGL_ * 10 : 30) : NF;  // face record fields
-  const long long base = (long long)k * NFR * fpl + (long long)j * fn0 + i;
-  const double wgt = 1.0 / NG;
-  // back to the global frame with weight 1/NG: y[0..9] = Fn, Ft (equal in both lanes), y[10..19] =
-  // this side's Qn, Qt (QL on side 0, QR on side 1)
-  double y[NR];
-#pragma unroll
-  for (int s = 0; s < NR / 5; ++s) {
-#pragma unroll
-    for (int cc = 0; cc < 5; ++cc) {
-      const double a = s == 0 ? o.Fn[cc] : (s == 1 ? o.Ft[cc] : (s == 2 ? o.QLn[cc] : o.QLt[cc]));
-      const int g = cc == 0 ? 0 : (cc == 4 ? 4 : 1 + (cc == 1 ? P0 : (cc == 2 ? P1 : P2)));
-      y[s * 5 + g] = a;  // the 1/NG weight is applied after the Gauss-point sum (exact: a power of 2)
-    }
-  }
-  if (COMPACT && LINES && valid) {
-    // line DOFs: this lane's own-side relaxed values at its Gauss point, in the line order g = p * n2 + q
-    // (p along TA, q along TB): Gauss point gp has signs (sA, sB) = (bit 0, bit 1)
-    const int gcan = NG == 4 ? 2 * (gp & 1) + ((gp >> 1) & 1) : gp;
-    double* dst = face + base + (long long)(30 + (side * NG + gcan) * 10) * fpl;
-#pragma unroll
-    for (int q = 0; q < 10; ++q) dst[q * fpl] = y[10 + q];
-  }
-  if constexpr (NG == 1) {
-    if (valid && side == 0) {
-#pragma unroll
-      for (int q = 0; q < NR; ++q) face[base + q * fpl] = y[q];
-    } else if (valid && COMPACT) {
-#pragma unroll
-      for (int q = 10; q < NR; ++q) face[base + (q + 10) * fpl] = y[q];
-    }
-  } else {
-    // Gauss-point sum by a reduce-scatter over the face's lanes (lane = 2 gp + side): round 1 with
-    // partner gp^1 halves the 20 values (even gp keeps y[0..9] = Fn Ft, odd gp keeps y[10..19] = this
-    // side's Qn Qt), round 2 with partner gp^2 halves again (NG = 4); each lane then holds NR / NG
-    // fully summed outputs ((g0 + g1) + (g2 + g3) in every lane: deterministic) and stores them; the
-    // side-1 lanes skip the duplicate Fn Ft.
-    constexpr int H = NR / 2;
-    constexpr int NOUT = NR / NG;
-    const bool up = gp & 1;
-    double z[H];
-#pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const double send = up ? y[q] : y[H + q];
-      const double keep = up ? y[H + q] : y[q];
-      z[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    int o0 = up ? H : 0;  // first of this lane's outputs among the side's NR values
-    double zz[NOUT];
-    if constexpr (NG > 2) {
-      const bool up2 = gp & 2;
-#pragma unroll
-      for (int q = 0; q < H / 2; ++q) {
-        const double send = up2 ? z[q] : z[H / 2 + q];
-        const double keep = up2 ? z[H / 2 + q] : z[q];
-        zz[q] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      o0 += up2 ? H / 2 : 0;
-    } else {
-#pragma unroll
-      for (int q = 0; q < NOUT; ++q) zz[q] = z[q];
-    }
-    // face slots: 0..9 Fn Ft, 10..19 QLn QLt (side 0), 20..29 QRn QRt (side 1)
-    if (valid && (o0 >= 10 || side == 0)) {
-      double* dst = face + base + (long long)(o0 + (o0 >= 10 && side ? 10 : 0)) * fpl;
-#pragma unroll
-      for (int q = 0; q < NOUT; ++q) dst[q * fpl] = wgt * zz[q];
-    }
-  }
-}
 
 }  // namespace cgks
 #include "flux1.cuh"
@@ -916,16 +555,18 @@ __global__ void __launch_bounds__(256) k_update(const double* __restrict__ Uin, 
                                                  const double* __restrict__ fy, const double* __restrict__ fz,
                                                  double* __restrict__ Uout, double* __restrict__ carry,
                                                  TimeState* __restrict__ ts, ErrState* __restrict__ err,
-                                                 double* __restrict__ Lout = nullptr,
-                                                 double* __restrict__ Lcarry = nullptr) {
+                                                 double* __restrict__ Lout, double* __restrict__ Lcarry,
+                                                 int kc0, int kc1) {
   constexpr int NV = COMPACT ? 20 : 5;
   constexpr int NF = COMPACT ? (LINES ? 30 + 2 * (DIM == 3 ? 4 : (DIM == 2 ? 2 : 1)) * 10 : 30) : 10;
   // the final update of a step (MODE 1, 2) also forms the next step's CFL candidates (fused):
   // block min, atomicMin into ts->dtmin_bits; k_step_end turns the (global) min into dt
   constexpr bool DT = MODE != 0;
   if (__syncthreads_or(err->code != 0)) return;  // block-uniform (block reduction below)
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nc = (long long)c_geo.n[0] * c_geo.n[1] * c_geo.n[2];
+  // cells of the planes [kc0, kc1) (a z-chunk, or all); face records of plane k at F[a] + k * NF * fpl
+  // (the caller shifts chunk buffers)
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x + (long long)kc0 * c_geo.plane;
+  const long long nc = (long long)kc1 * c_geo.plane;
   double cand = 1e300;
   if (t < nc) {
   const int i = (int)(t % c_geo.n[0]);

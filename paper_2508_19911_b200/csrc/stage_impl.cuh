@@ -54,7 +54,15 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
     attr = true;
   }
-  const int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+  // extended z planes [z0, z1): all, a part (halo overlap), or a z-chunk's cells and their two
+  // neighbour planes (chunked stage: rec holds extended planes ck0 .. ck0 + cn + 1 from its start)
+  int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+  double* rec = a.rec;
+  if (a.cn >= 0) {
+    z0 = a.ck0;
+    z1 = a.ck0 + a.cn + 2;
+    rec = a.rec - (long long)a.ck0 * a.en[0] * a.en[1] * (5 * Sten<D>::NB);
+  }
   if (z1 <= z0) return 0;
   const dim3 grid((unsigned)((a.en[0] + RT::TX - 1) / RT::TX), (unsigned)((a.en[1] + RT::TY - 1) / RT::TY),
                   (unsigned)((z1 - z0 + RT::TZ - 1) / RT::TZ));
@@ -64,7 +72,7 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0, env.stream);
   }
-  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, a.rec, a.err, a.Lin, z0, z1);
+  kern<<<grid, RT::NTH, smem, env.stream>>>(a.Uin, rec, a.err, a.Lin, z0, z1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of recon5 failed: %s", cudaGetErrorString(e));
@@ -78,33 +86,30 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 }
 
 // flux kernel: one block per FPB faces of an x-row, dynamic shared memory tile
-#ifndef CGKS_FLUX1
-#define CGKS_FLUX1 1  // 1: k_flux1 (one lane per Gauss point), 0: k_flux (two lanes per Gauss point)
-#endif
-#if CGKS_FLUX1
 template <int AX, bool COMPACT>
 using FluxTileSel = FluxTile1<D, AX, COMPACT>;
-#else
-template <int AX, bool COMPACT>
-using FluxTileSel = FluxTile<D, AX, COMPACT>;
-#endif
 
 template <bool COMPACT, bool BOX, int AX, bool LINES = false, bool STR = false>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
   using FT = FluxTileSel<AX, COMPACT>;
-#if CGKS_FLUX1
   auto kern = k_flux1<D, AX, COMPACT, BOX, LINES, STR>;
-#else
-  auto kern = k_flux<D, AX, COMPACT, BOX, LINES, STR>;
-#endif
   static bool attr = false;
   const size_t smem = FT::smem_bytes();
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
     attr = true;
   }
+  // face planes [kb, ke) along z: all of them, or those of the z-chunk a.ck0 .. a.ck0 + a.cn (chunked
+  // stage; z-faces: cn + 1 planes); the chunk's face records and reconstruction planes start at kb
+  const int kb = a.cn < 0 ? 0 : a.ck0;
+  const int ke = a.cn < 0 ? a.fn[AX][2] : a.ck0 + a.cn + (AX == 2 ? 1 : 0);
+  if (ke <= kb) return 0;
+  constexpr int NGL_ = D == 3 ? 4 : (D == 2 ? 2 : 1);
+  constexpr int NFR = COMPACT ? (LINES ? 30 + 2 * NGL_ * 10 : 30) : 10;
+  double* face = a.face[AX] - (long long)kb * NFR * a.fn[AX][0] * a.fn[AX][1];
+  const double* rec = a.rec - (long long)kb * a.en[0] * a.en[1] * (COMPACT ? 5 * Sten<D>::NB : 15);
   const unsigned gy = (unsigned)(AX == 1 ? (a.fn[AX][1] + FT::FY - 1) / FT::FY : a.fn[AX][1]);
-  const unsigned gz = (unsigned)(AX == 2 ? (a.fn[AX][2] + FT::FY - 1) / FT::FY : a.fn[AX][2]);
+  const unsigned gz = (unsigned)(AX == 2 ? (ke - kb + FT::FY - 1) / FT::FY : ke - kb);
   const unsigned gx = (unsigned)((a.fn[AX][0] + FT::FX - 1) / FT::FX);
   const dim3 grid = AX == 2 ? dim3(gx, gz, gy) : dim3(gx, gy, gz);  // z-faces: (x, z, y) order
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -114,9 +119,9 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
     cudaEventRecord(e0, env.stream);
   }
   static const CUtensorMap none{};
-  kern<<<grid, 128, smem, env.stream>>>(a.Uin, a.rec, a.gtab[AX], a.face[AX], a.ts, a.err, stage,
+  kern<<<grid, 128, smem, env.stream>>>(a.Uin, rec, a.gtab[AX], face, a.ts, a.err, stage,
                                         a.use_tma ? a.tm_rec[AX] : none, a.use_tma ? a.tm_U[AX] : none,
-                                        a.use_tma && !BOX ? 1 : 0);
+                                        a.use_tma && !BOX ? 1 : 0, kb, ke, a.cn < 0 ? 0 : kb);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (env.msg) std::snprintf(env.msg, env.msglen, "launch of %s failed: %s", name, cudaGetErrorString(e));
@@ -136,9 +141,15 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
       int rc = recon5_launch<NONLIN, BOX, LINES, STR>(env, a);
       if (rc) return rc;
     } else {
-      const int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+      int z0 = a.rz1 < 0 ? 0 : a.rz0, z1 = a.rz1 < 0 ? a.en[2] : a.rz1;
+      double* rec = a.rec;
+      if (a.cn >= 0) {  // z-chunk (see recon5_launch)
+        z0 = a.ck0;
+        z1 = a.ck0 + a.cn + 2;
+        rec = a.rec - (long long)a.ck0 * a.en[0] * a.en[1] * 15;
+      }
       if (z1 > z0)
-        LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), (long long)a.en[0] * a.en[1] * (z1 - z0), 256, a.Uin, a.rec,
+        LAUNCH("recon2", (k_recon2<D, NONLIN, BOX>), (long long)a.en[0] * a.en[1] * (z1 - z0), 256, a.Uin, rec,
                a.err, z0, z1);
     }
     if (a.part == 1) return 0;
@@ -149,15 +160,25 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
     if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES, STR>(env, "flux_z", a, stage);
     if (rc) return rc;
   }
-  if (mode == 0)
-    LAUNCH("update", (k_update<D, COMPACT, 0, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
-  else if (mode == 1)
-    LAUNCH("update", (k_update<D, COMPACT, 1, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
-  else
-    LAUNCH("update", (k_update<D, COMPACT, 2, LINES>), a.ncell, 256, a.Uin, a.face[0], a.face[1], a.face[2], a.Uout,
-           a.carry, a.ts, a.err, a.Lout, a.Lcarry);
+  {
+    // cells of the planes [kc0, kc1): all, or the z-chunk; chunk face records start at plane kc0
+    const int kc0 = a.cn < 0 ? 0 : a.ck0, kc1 = a.cn < 0 ? a.nz : a.ck0 + a.cn;
+    constexpr int NGL_ = D == 3 ? 4 : (D == 2 ? 2 : 1);
+    constexpr int NFR = COMPACT ? (LINES ? 30 + 2 * NGL_ * 10 : 30) : 10;
+    double* fc[3];
+    for (int d = 0; d < 3; ++d)
+      fc[d] = a.face[d] ? a.face[d] - (long long)kc0 * NFR * a.fn[d][0] * a.fn[d][1] : nullptr;
+    const long long ncl = (long long)(kc1 - kc0) * (a.ncell / a.nz);
+    if (mode == 0)
+      LAUNCH("update", (k_update<D, COMPACT, 0, LINES>), ncl, 256, a.Uin, fc[0], fc[1], fc[2], a.Uout, a.carry,
+             a.ts, a.err, a.Lout, a.Lcarry, kc0, kc1);
+    else if (mode == 1)
+      LAUNCH("update", (k_update<D, COMPACT, 1, LINES>), ncl, 256, a.Uin, fc[0], fc[1], fc[2], a.Uout, a.carry,
+             a.ts, a.err, a.Lout, a.Lcarry, kc0, kc1);
+    else
+      LAUNCH("update", (k_update<D, COMPACT, 2, LINES>), ncl, 256, a.Uin, fc[0], fc[1], fc[2], a.Uout, a.carry,
+             a.ts, a.err, a.Lout, a.Lcarry, kc0, kc1);
+  }
   return 0;
 }
 
