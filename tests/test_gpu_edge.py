@@ -69,7 +69,7 @@ def test_impossible_allocation_fails_cleanly():
     Solver, CgksError = _S()
     with pytest.raises(CgksError) as e:
         Solver(n=(4096, 4096, 4096), lo=(0, 0, 0), hi=(1, 1, 1), scheme=1)
-    assert e.value.code == 5
+    assert e.value.code in (2, 5)  # 2: beyond the 2^32-element buffer limit (checked first), 5: allocation
     c = uniform((6, 6, 6))
     S = Solver.from_case(c, scheme=1)  # the device is still usable
     S.set_state(c.Q, c.G)
