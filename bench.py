@@ -183,9 +183,19 @@ def cpu_baseline(case_name, scheme, budget_s=20.0):
         if rc or t_used > budget_s:
             break
     cores = oracle.max_threads()
+    # one thread: the same flow at 16^3, one step (~5 s)
+    from cgks_inputs import hit, tgv_supersonic
+    c1 = tgv_supersonic(16) if case_name.startswith("tgv_ss") else (hit(16) if case_name.startswith("hit") else tgv(16))
+    p1 = oracle.Problem(**c1.problem_kwargs(), scheme=1 if scheme == "cgks5" else 0,
+                        time_scheme=2 if scheme == "cgks5" else 1)
+    t0 = time.perf_counter()
+    oracle.run(p1, c1.Q, c1.G, 1, nthreads=1)
+    t1 = time.perf_counter() - t0
     return {"value": c.ncell * steps / t_used, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
             "sample": f"{c.name} {c.n[0]}x{c.n[1]}x{c.n[2]}, {steps} step(s), {t_used:.1f} s, "
-                      f"OpenMP threads={cores}"}
+                      f"OpenMP threads={cores}",
+            "value_1thread": c1.ncell / t1,
+            "sample_1thread": f"{c1.name} {c1.n[0]}x{c1.n[1]}x{c1.n[2]}, 1 step, {t1:.1f} s, 1 thread"}
 
 
 def run_reference(args, rank, ws):
