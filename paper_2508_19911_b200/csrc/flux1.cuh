@@ -20,7 +20,8 @@ namespace cgks {
 template <int DIM, int AX, bool COMPACT>
 struct FluxTile1 {
   static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
-  static constexpr int FPB = 128 / NG;                       // faces per block
+  static constexpr int NTHR = AX == 0 ? CGKS_FLUX_NTHR_X : CGKS_FLUX_NTHR_YZ;  // threads per block (one per Gauss point)
+  static constexpr int FPB = NTHR / NG;                      // faces per block
   static constexpr int FY = AX == 0 ? 1 : CGKS_FY1;          // faces along the normal axis
   static constexpr int FX = FPB / FY;                        // faces along x
   static constexpr int NT = AX == 0 ? FPB + 2 : FX * (FY + 1);
@@ -40,14 +41,14 @@ struct FluxTile1 {
   static constexpr int FSU = AX == 2 ? FX : NT;
   __host__ __device__ static constexpr int cbaseU(int c) { return AX == 2 ? (c / FX) * 5 * FX + c % FX : c; }
   static constexpr int STILE = (NREC * NT + 15) / 16 * 16;
-  // Per-lane rows (row r of lane l at r * 128 + l): CGKS-5th uses the dead tile -- the evaluation
+  // Per-lane rows (row r of lane l at r * NTHR + l): CGKS-5th uses the dead tile -- the evaluation
   // results [side][q][v] (XR rows), each side's dW/dt parked over its consumed d/dn rows, and 25 slots
   // for the half-range vectors x1[20..44]; GKS-2nd parks those 25 behind its (small) tile.
   static constexpr int FREE0 = COMPACT ? NQ * 5 - 10 : 0;  // rows 10 .. NQ*5-1: free once side 0 is read
   static constexpr int PROWS = COMPACT ? XR + 25 - FREE0 : 25;
-  static constexpr int PARK0 = COMPACT ? 0 : (STILE + 5 * NT + 127) / 128 * 128;
-  static constexpr int TILE = COMPACT ? (STILE + 5 * NT > PROWS * 128 ? STILE + 5 * NT : PROWS * 128)
-                                      : PARK0 + PROWS * 128;
+  static constexpr int PARK0 = COMPACT ? 0 : (STILE + 5 * NT + NTHR - 1) / NTHR * NTHR;
+  static constexpr int TILE = COMPACT ? (STILE + 5 * NT > PROWS * NTHR ? STILE + 5 * NT : PROWS * NTHR)
+                                      : PARK0 + PROWS * NTHR;
   static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB) + 16; }
   // parking slot j (0..24, the half-range vectors x1[20..44]) -> row: free of both sides' W and dW/dt
   // rows and of side 1's unread rows
@@ -60,13 +61,15 @@ template <int DIM, int AX, bool COMPACT>
 struct ParkDev1 {
   double* col;
   __device__ __forceinline__ void put(int s, double v) const {
-    col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * 128] = v;
+    col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::NTHR] = v;
   }
-  __device__ __forceinline__ double get(int s) const { return col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * 128]; }
+  __device__ __forceinline__ double get(int s) const {
+    return col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::NTHR];
+  }
 };
 
 template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR = false>
-__global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
+__global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, 384 / FluxTile1<DIM, AX, COMPACT>::NTHR) k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
                                                 const double* __restrict__ gtab, double* __restrict__ face,
                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                 int stage, const __grid_constant__ CUtensorMap tm_rec,
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
     }
   } else {
     // cp.async: TPC threads per tile cell (index math once per cell), a strided subset of its fields each
-    constexpr int TPC = 128 / NT > 0 ? 128 / NT : 1;
+    constexpr int TPC = FT::NTHR / NT > 0 ? FT::NTHR / NT : 1;
     for (int w = threadIdx.x; w < NT * TPC; w += blockDim.x) {
       const int c = w % NT, fsub = w / NT;
       int ci, cj = j0, ck = k0;
@@ -178,7 +181,8 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
       }
     }
   }
-  double* col = tile + lane;                // this lane's rows in the dead tile: row r at col[r * 128]
+  constexpr int RS = FT::NTHR;              // row stride of the lanes' rows
+  double* col = tile + lane;                // this lane's rows in the dead tile: row r at col[r * RS]
   const ParkDev1<DIM, AX, COMPACT> park{tile + FT::PARK0 + lane};
   // global-frame W (5) and physical derivatives (3 x 5) of side s -> normal frame
   auto to_normal = [&](const double* W, const double (*g)[5], double* wn, double (*dn)[5]) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
 #pragma unroll
         for (int v = 0; v < 5; ++v)
 #pragma unroll
-          for (int g2 = 0; g2 < NG; ++g2) tile[((s * NQ + q) * 5 + v) * 128 + (lane - gp + g2)] = R[s][qi][v][g2];
+          for (int g2 = 0; g2 < NG; ++g2) tile[((s * NQ + q) * 5 + v) * RS + (lane - gp + g2)] = R[s][qi][v][g2];
       }
     __syncwarp();
   }
@@ -297,14 +301,14 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
     double W[5], g[3][5];
     const double* ih = s ? ihR : ihL;
     if (COMPACT) {
-      const double* rb = col + s * NQ * 5 * 128;
+      const double* rb = col + s * NQ * 5 * RS;
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
-        W[v] = rb[v * 128];
+        W[v] = rb[v * RS];
         g[0][v] = g[1][v] = g[2][v] = 0.0;
-        g[AX][v] = rb[(5 + v) * 128] * ih[AX];
-        if (DIM > 1) g[TA][v] = rb[((2 % NQ) * 5 + v) * 128] * ih[TA];
-        if (DIM > 2) g[TB][v] = rb[((3 % NQ) * 5 + v) * 128] * ih[TB];
+        g[AX][v] = rb[(5 + v) * RS] * ih[AX];
+        if (DIM > 1) g[TA][v] = rb[((2 % NQ) * 5 + v) * RS] * ih[TA];
+        if (DIM > 2) g[TB][v] = rb[((3 % NQ) * 5 + v) * RS] * ih[TB];
       }
     } else {
       const int cs = s ? cR : cL;
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
     okLR &= oks ? 1 : 0;
     if (COMPACT)
 #pragma unroll
-      for (int v = 0; v < 5; ++v) col[(s * NQ * 5 + 5 + v) * 128] = dtw[v];  // over the side's consumed d/dn rows
+      for (int v = 0; v < 5; ++v) col[(s * NQ * 5 + 5 + v) * RS] = dtw[v];  // over the side's consumed d/dn rows
     asm volatile("" ::: "memory");  // the parked side-0 vectors stay out of registers during side 1
 #pragma unroll
     for (int q = 0; q < 25; ++q) {
@@ -373,15 +377,15 @@ __global__ void __launch_bounds__(128, CGKS_FLUX_MINB) k_flux1(const double* __r
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         // W_s (global frame, rows s*NQ*5 + 0..4) and dW_s/dt (normal frame, rows s*NQ*5 + 5..9)
-        const double* rb = col + s * NQ * 5 * 128;
+        const double* rb = col + s * NQ * 5 * RS;
         double Wg[5];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) Wg[v] = rb[v * 128];
+        for (int v = 0; v < 5; ++v) Wg[v] = rb[v * RS];
         const double Wn[5] = {Wg[0], Wg[1 + P0], Wg[1 + P1], Wg[1 + P2], Wg[4]};
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
           y[10 + 10 * s + gidx(cc)] = w * acc[10 + cc] + ee * Wn[cc];
-          y[15 + 10 * s + gidx(cc)] = w * acc[15 + cc] + ee * rb[(5 + cc) * 128];
+          y[15 + 10 * s + gidx(cc)] = w * acc[15 + cc] + ee * rb[(5 + cc) * RS];
         }
       }
     }

@@ -492,8 +492,14 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 // Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
 // The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
 // ---------------------------------------------------------------------------
-#ifndef CGKS_FLUX_MINB
-#define CGKS_FLUX_MINB 3
+// threads per flux block (= Gauss points per block) per normal axis: x-faces 64 (16 faces), y-/z-faces 128
+// (32 faces) -- measured per axis (x: 1.79 vs 1.83 ms; y / z: 1.75 / 1.74 vs 1.77 / 1.77 ms); 12 warps
+// per SM either way (168 registers)
+#ifndef CGKS_FLUX_NTHR_X
+#define CGKS_FLUX_NTHR_X 64
+#endif
+#ifndef CGKS_FLUX_NTHR_YZ
+#define CGKS_FLUX_NTHR_YZ 128
 #endif
 
 }  // namespace cgks

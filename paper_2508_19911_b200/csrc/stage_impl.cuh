@@ -119,7 +119,7 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
     cudaEventRecord(e0, env.stream);
   }
   static const CUtensorMap none{};
-  kern<<<grid, 128, smem, env.stream>>>(a.Uin, rec, a.gtab[AX], face, a.ts, a.err, stage,
+  kern<<<grid, FT::NTHR, smem, env.stream>>>(a.Uin, rec, a.gtab[AX], face, a.ts, a.err, stage,
                                         a.use_tma ? a.tm_rec[AX] : none, a.use_tma ? a.tm_U[AX] : none,
                                         a.use_tma && !BOX ? 1 : 0, kb, ke, a.cn < 0 ? 0 : kb);
   cudaError_t e = cudaGetLastError();
