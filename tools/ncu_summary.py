@@ -94,7 +94,7 @@ BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def bench_name(kernel):
-    m = re.search(r"k_flux<(\d+), (\d+),", kernel)
+    m = re.search(r"k_flux1?<(\d+), (\d+),", kernel)
     if m:
         return "flux_" + "xyz"[int(m.group(2))]
     for k in ("recon5", "recon2", "update", "dt_finalize", "dt", "step_end", "pack", "unpack"):
