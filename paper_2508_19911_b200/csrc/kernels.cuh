@@ -205,8 +205,8 @@ struct ReconTile {
   static constexpr int HX = TX + 2, HY = DIM >= 2 ? TY + 2 : 1, HZ = DIM == 3 ? TZ + 2 : 1;
   static constexpr int HALO = HX * HY * HZ;
   static constexpr int NFS = 1 + DIM;  // staged fields per component: Q_v, dQ_v/dx_a
-  // two component buffers + the staging offset table (ReconStageMap)
-  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO + sizeof(unsigned) * NFS * HALO; }
+  // two component buffers + the per-position staging offsets (ReconStageMap)
+  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * NFS * HALO + sizeof(unsigned) * HALO; }
 };
 
 template <int DIM, bool STR = false>
@@ -237,27 +237,24 @@ struct Recon5TileLoader {
   }
 };
 
-// Halo-tile staging of the reconstruction.  Each tile element's global offset for component
-// v = 0 (index arithmetic, periodic wrap) is computed once per block into a shared table, so
-// staging component v is one shared load, one add and one cp.async per element: field f of
-// component v sits at offset(f, v = 0) + v * plane in the [z][field][y][x] layout.
+// Halo-tile staging of the reconstruction.  The global offset of each tile position (index arithmetic,
+// periodic wrap) is computed once per block into a shared table; field f of component v of that position
+// sits at offset + (fld(f) + v) * plane in the [z][field][y][x] layout, so staging a component is one
+// table load per position and one address add + cp.async per element.
 template <int DIM>
 struct ReconStageMap {
   using RT = ReconTile<DIM>;
-  static constexpr int NEL = RT::NFS * RT::HALO;
-  unsigned* off;  // [NEL] in shared memory
+  unsigned* off;  // [HALO] in shared memory
   __device__ __forceinline__ void init(int x0, int y0, int z0) const {
-    for (int idx = threadIdx.x; idx < NEL; idx += RT::NTH) {
-      const int f = idx / RT::HALO, h = idx % RT::HALO;
+    for (int h = threadIdx.x; h < RT::HALO; h += RT::NTH) {
       const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
       const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
-      const int fld = f == 0 ? 0 : 5 + (f - 1) * 5;
-      off[idx] = (unsigned)sidx(20, fld, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk));
+      off[h] = (unsigned)sidx(20, 0, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk));
     }
   }
 };
 
-// stage fields (Q_v, G_{a,v}) of the block's halo tile into buf
+// stage fields (Q_v, G_{a,v}) of the block's halo tile into buf ([field][position])
 template <int DIM, bool BOX>
 __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double* buf, int v, int x0, int y0,
                                             int z0, const ReconStageMap<DIM>& map) {
@@ -273,7 +270,14 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
   } else {
     const double* Uv = U + (long long)v * c_geo.plane;
 #pragma unroll 1
-    for (int idx = threadIdx.x; idx < ReconStageMap<DIM>::NEL; idx += RT::NTH) cp_async8(buf + idx, Uv + map.off[idx]);
+    for (int h = threadIdx.x; h < RT::HALO; h += RT::NTH) {
+      {
+        const double* src = Uv + map.off[h];
+#pragma unroll
+        for (int f = 0; f < RT::NFS; ++f)
+          cp_async8(buf + f * RT::HALO + h, src + (f == 0 ? 0 : 5 + (f - 1) * 5) * c_geo.plane);
+      }
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
