@@ -13,6 +13,9 @@
 
 namespace cgks {
 
+#ifndef CGKS_RPAD
+#define CGKS_RPAD 2
+#endif
 #ifndef CGKS_FY1
 #define CGKS_FY1 4  // faces of a y- / z-face patch along the normal axis (x extent = faces per block / FY1)
 #endif
@@ -21,6 +24,7 @@ template <int DIM, int AX, bool COMPACT>
 struct FluxTile1 {
   static constexpr int NG = COMPACT ? Sten<DIM>::NG : 1;
   static constexpr int NTHR = AX == 0 ? CGKS_FLUX_NTHR_X : CGKS_FLUX_NTHR_YZ;  // threads per block (one per Gauss point)
+  static constexpr int MINB = (AX == 0 ? CGKS_FLUX_WARPS_X : CGKS_FLUX_WARPS_YZ) * 32 / NTHR;  // resident blocks per SM
   static constexpr int FPB = NTHR / NG;                      // faces per block
   static constexpr int FY = AX == 0 ? 1 : CGKS_FY1;          // faces along the normal axis
   static constexpr int FX = FPB / FY;                        // faces along x
@@ -46,9 +50,16 @@ struct FluxTile1 {
   // for the half-range vectors x1[20..44]; GKS-2nd parks those 25 behind its (small) tile.
   static constexpr int FREE0 = COMPACT ? NQ * 5 - 10 : 0;  // rows 10 .. NQ*5-1: free once side 0 is read
   static constexpr int PROWS = COMPACT ? XR + 25 - FREE0 : 25;
+  // row stride of the lanes' rows: NTHR + CGKS_RPAD (even) moves the rows of the 4 quantities (5 rows apart)
+  // onto different banks, so the scatter of the evaluation results (a face's 4 lanes write 4 rows, STS.128)
+  // is no longer 4-way conflicted; lanes read their own column (conflict-free at any stride).  Measured
+  // per launch (x / y / z, ms): pad 0: 1.78 / 1.75 / 1.74; 2: 1.62 / 1.62 / 1.62; 4: 1.63 / 1.62 / 1.62;
+  // 6, 10: 1.65 / 1.62 / 1.62; 18, 26: x 1.95 (shared memory then caps x-face blocks at 5 per SM)
+  static constexpr int RS = COMPACT ? NTHR + CGKS_RPAD : NTHR;
   static constexpr int PARK0 = COMPACT ? 0 : (STILE + 5 * NT + NTHR - 1) / NTHR * NTHR;
-  static constexpr int TILE = COMPACT ? (STILE + 5 * NT > PROWS * NTHR ? STILE + 5 * NT : PROWS * NTHR)
+  static constexpr int TILE = COMPACT ? (STILE + 5 * NT > PROWS * RS ? STILE + 5 * NT : PROWS * RS)
                                       : PARK0 + PROWS * NTHR;
+  static_assert(CGKS_RPAD % 2 == 0, "the evaluation tables behind the rows are read as double2");
   static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB) + 16; }
   // parking slot j (0..24, the half-range vectors x1[20..44]) -> row: free of both sides' W and dW/dt
   // rows and of side 1's unread rows
@@ -61,15 +72,15 @@ template <int DIM, int AX, bool COMPACT>
 struct ParkDev1 {
   double* col;
   __device__ __forceinline__ void put(int s, double v) const {
-    col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::NTHR] = v;
+    col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::RS] = v;
   }
   __device__ __forceinline__ double get(int s) const {
-    return col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::NTHR];
+    return col[FluxTile1<DIM, AX, COMPACT>::park_row(s) * FluxTile1<DIM, AX, COMPACT>::RS];
   }
 };
 
 template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR = false>
-__global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, 384 / FluxTile1<DIM, AX, COMPACT>::NTHR) k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
+__global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<DIM, AX, COMPACT>::MINB) k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
                                                 const double* __restrict__ gtab, double* __restrict__ face,
                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                 int stage, const __grid_constant__ CUtensorMap tm_rec,
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, 384 / FluxT
       }
     }
   }
-  constexpr int RS = FT::NTHR;              // row stride of the lanes' rows
+  constexpr int RS = FT::RS;                // row stride of the lanes' rows
   double* col = tile + lane;                // this lane's rows in the dead tile: row r at col[r * RS]
   const ParkDev1<DIM, AX, COMPACT> park{tile + FT::PARK0 + lane};
   // global-frame W (5) and physical derivatives (3 x 5) of side s -> normal frame

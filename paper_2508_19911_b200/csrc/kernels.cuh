@@ -505,6 +505,13 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 #ifndef CGKS_FLUX_NTHR_YZ
 #define CGKS_FLUX_NTHR_YZ 128
 #endif
+// resident warps per SM the flux kernels are compiled for (register cap = 65536 / (32 x warps))
+#ifndef CGKS_FLUX_WARPS_X
+#define CGKS_FLUX_WARPS_X 12
+#endif
+#ifndef CGKS_FLUX_WARPS_YZ
+#define CGKS_FLUX_WARPS_YZ 12
+#endif
 
 }  // namespace cgks
 #include "flux1.cuh"
