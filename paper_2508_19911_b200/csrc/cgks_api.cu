@@ -789,8 +789,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       const cuuint32_t es[4] = {1, 1, 1, 1};
       bool good = true;
       for (int a = 0; a < 3 && good; ++a) {
-        int tx = 0, tn = 0;
-        ctx->ops->flux_tile(a, ctx->scheme_id == CGKS_CGKS5 ? 1 : 0, &tx, &tn);
+        int tx = 0, tn = 0, nfbox = 0;
+        ctx->ops->flux_tile(a, ctx->scheme_id == CGKS_CGKS5 ? 1 : 0, &tx, &tn, &nfbox);
         const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
         {
           // [z][y][field][x]: dims (x, field, y, z)
@@ -798,7 +798,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
                                       (cuuint64_t)(ctx->chunk ? ctx->chunk + 2 : g.en[2])};
           const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.en[0] * nrec * 8,
                                      (cuuint64_t)g.eplane * nrec * 8};
-          const cuuint32_t box[4] = {(cuuint32_t)tx, (cuuint32_t)nrec, by, bz};
+          const cuuint32_t box[4] = {(cuuint32_t)tx, (cuuint32_t)nfbox, by, bz};  // one part of the fields
           good = good && encode(&ctx->tm_rec[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->rec, dims, str, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

@@ -74,7 +74,7 @@ struct DimOps {
   // flow diagnostics of a.Uin (reconstruction + quadrature); *nblk = number of 4-double block partials
   int (*diag)(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part, long long* nblk);
   // flux tile extent (cells along x, cells along the normal axis) for the TMA boxes, CGKS-5th
-  void (*flux_tile)(int ax, int compact, int* tx, int* tn);
+  void (*flux_tile)(int ax, int compact, int* tx, int* tn, int* nfbox);  // flux tile extents, fields per TMA box
   // Q-criterion of a.Uin at the cell centroids (reconstruction + k_qcrit) into out[ncell]
   int (*qcrit)(LaunchEnv& env, const StageArgs& a, const double* wc, double* out);
   // line DOFs initialised from the gradients of U

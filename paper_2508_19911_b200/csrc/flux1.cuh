@@ -16,8 +16,15 @@ namespace cgks {
 #ifndef CGKS_RPAD
 #define CGKS_RPAD 2
 #endif
+#ifndef CGKS_TMA_SPLIT
+#define CGKS_TMA_SPLIT 1
+#endif
+#ifndef CGKS_EVAL_SQ
+#define CGKS_EVAL_SQ 1
+#endif
 #ifndef CGKS_FY1
-#define CGKS_FY1 4  // faces of a y- / z-face patch along the normal axis (x extent = faces per block / FY1)
+#define CGKS_FY1 2  // faces of a y- / z-face patch along the normal axis (x extent = faces per block / FY1):
+                        // 16 x 2 patches (128-byte TMA rows), measured 1.611 / 1.609 ms vs 8 x 4: 1.622 / 1.617, 4 x 8: 1.66
 #endif
 
 template <int DIM, int AX, bool COMPACT>
@@ -39,12 +46,21 @@ struct FluxTile1 {
   static constexpr int TS = ((NB / 2) % 2 == 1) ? NB : NB + 2;
   static constexpr int TAB = COMPACT ? 2 * NQ * TS : 0;
   static constexpr int FS = AX == 0 ? NT : FX;
+  // the reconstruction fields arrive in NSPL parts of NRH fields (TMA boxes on their own mbarriers, so the
+  // evaluation of the first basis functions overlaps the load of the rest): tile layout [part][plane][field
+  // of the part][x]; field f of tile cell c at cbase(c, NRH) + faddr(f)
+  static constexpr int NSPL = COMPACT ? CGKS_TMA_SPLIT : 1;
+  static constexpr int NRH = NREC / NSPL;
+  static_assert(NREC % NSPL == 0 && NRH % 5 == 0, "parts of whole basis functions");
+  static constexpr int KH = NRH / 5;  // basis functions per part
+  static constexpr int PSTR = (NRH * NT + 15) / 16 * 16;  // 128-byte aligned parts (bulk-tensor destinations)
+  __host__ __device__ static constexpr int faddr(int f) { return (f / NRH) * PSTR + (f % NRH) * FS; }
   __host__ __device__ static constexpr int cbase(int c, int nfield) {
     return AX == 0 ? c : (c / FX) * nfield * FX + c % FX;
   }
   static constexpr int FSU = AX == 2 ? FX : NT;
   __host__ __device__ static constexpr int cbaseU(int c) { return AX == 2 ? (c / FX) * 5 * FX + c % FX : c; }
-  static constexpr int STILE = (NREC * NT + 15) / 16 * 16;
+  static constexpr int STILE = NSPL * PSTR;
   // Per-lane rows (row r of lane l at r * NTHR + l): CGKS-5th uses the dead tile -- the evaluation
   // results [side][q][v] (XR rows), each side's dW/dt parked over its consumed d/dn rows, and 25 slots
   // for the half-range vectors x1[20..44]; GKS-2nd parks those 25 behind its (small) tile.
@@ -60,7 +76,7 @@ struct FluxTile1 {
   static constexpr int TILE = COMPACT ? (STILE + 5 * NT > PROWS * RS ? STILE + 5 * NT : PROWS * RS)
                                       : PARK0 + PROWS * NTHR;
   static_assert(CGKS_RPAD % 2 == 0, "the evaluation tables behind the rows are read as double2");
-  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB) + 16; }
+  static constexpr size_t smem_bytes() { return sizeof(double) * ((size_t)TILE + TAB) + 8 * NSPL; }
   // parking slot j (0..24, the half-range vectors x1[20..44]) -> row: free of both sides' W and dW/dt
   // rows and of side 1's unread rows
   __host__ __device__ static constexpr int park_row(int j) {
@@ -108,10 +124,17 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   const bool tma = !BOX && use_tma && !wraps;
   if (tma) {
     if (threadIdx.x == 0) {
-      // tile boxes and the evaluation tables (one 1-D bulk copy) complete on one mbarrier
-      mbar_init(bar, 1);
-      mbar_expect_tx(bar, (unsigned)(sizeof(double) * ((FT::NREC + 5) * NT + FT::TAB)));
-      tma_load_4d(tile, &tm_rec, bar, x0 - c_geo.elo[0], 0, y0 - c_geo.elo[1], z0 - c_geo.elo[2] - kofs);
+      // the first part of the reconstruction fields, Q and the evaluation tables (one 1-D bulk copy) complete
+      // on mbarrier 0, part p > 0 on mbarrier p
+#pragma unroll
+      for (int p = 0; p < FT::NSPL; ++p) mbar_init(bar + p, 1);
+      mbar_expect_tx(bar, (unsigned)(sizeof(double) * ((FT::NRH + 5) * NT + FT::TAB)));
+#pragma unroll
+      for (int p = 1; p < FT::NSPL; ++p) mbar_expect_tx(bar + p, (unsigned)(sizeof(double) * FT::NRH * NT));
+#pragma unroll
+      for (int p = 0; p < FT::NSPL; ++p)
+        tma_load_4d(tile + p * FT::PSTR, &tm_rec, bar + p, x0 - c_geo.elo[0], p * FT::NRH, y0 - c_geo.elo[1],
+                    z0 - c_geo.elo[2] - kofs);
       tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
       if (COMPACT) bulk_load(tab, gtab, (unsigned)(sizeof(double) * FT::TAB), bar);
     }
@@ -142,12 +165,11 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       }
       const long long st = c_geo.en[0];  // field stride of the reconstruction array
       const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
-      unsigned dst = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NREC) + fsub * FT::FS);
+      const unsigned dst0 = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NRH));
 #pragma unroll 4
       for (int fld = fsub; fld < FT::NREC; fld += TPC) {
-        cp_async8s(dst, src);
+        cp_async8s(dst0 + FT::faddr(fld) * (unsigned)sizeof(double), src);
         src += TPC * st;
-        dst += TPC * FT::FS * (unsigned)sizeof(double);
       }
       double* sdst = tile + FT::STILE + FT::cbaseU(c);
       if (BOX) {
@@ -163,7 +185,12 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   const bool stop = __syncthreads_or(err->code != 0);
   cp_async_wait_all();
   if (tma) mbar_wait(bar, 0);
-  if (stop) return;
+  if (stop) {
+    if (tma)
+#pragma unroll
+      for (int p = 1; p < FT::NSPL; ++p) mbar_wait(bar + p, 0);  // no bulk copy may land after the exit
+    return;
+  }
   __syncthreads();
 
   const double dt = ts->dt;
@@ -214,7 +241,75 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   };
   constexpr int TA = DIM == 3 ? P1 : (DIM == 2 ? 1 - AX : 0);  // active transverse axes
   constexpr int TB = DIM == 3 ? P2 : 0;
-  if (COMPACT) {
+#if CGKS_EVAL_SQ
+  constexpr bool SQ = COMPACT && DIM == 3 && NG == 4;
+#else
+  constexpr bool SQ = false;
+#endif
+  if constexpr (SQ) {
+    // Face-plane parity evaluation, one side per lane: lane gp of a face evaluates side s = gp & 1 for the
+    // quantities qa = gp >> 1 (value or d/dn) and qa + 2 (d/dtA or d/dtB) at all 4 Gauss points, so every
+    // coefficient it loads feeds two FMAs (170 shared-memory loads per lane instead of 340 for both sides);
+    // the results wait in registers for the block barrier (tile dead), then go to their lanes' columns.
+    const int sd = gp & 1, qa = gp >> 1;
+    const int cs = sd ? cR : cL;
+    const double* tc = tile + FT::cbase(cs, FT::NRH);
+    const double* sc = tile + FT::STILE + FT::cbaseU(cs);
+    const double* Ta = tab + (sd * NQ + qa) * FT::TS;
+    const double* Tb = Ta + 2 * FT::TS;
+    double Sa[5][4], Sb[5][4];
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        Sa[v][cc] = (cc == 0 && qa == 0) ? sc[v * FT::FSU] : 0.0;  // the value's sums start from the average
+        Sb[v][cc] = 0.0;
+      }
+#pragma unroll
+    for (int k2 = 0; k2 < NB; k2 += 2) {
+      const double2 ta = *reinterpret_cast<const double2*>(Ta + k2);
+      const double2 tb = *reinterpret_cast<const double2*>(Tb + k2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kk = k2 + h;
+        if (kk >= NB) break;
+        const int cls = (ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const double c = tc[FT::faddr(kk * 5 + v)];
+          Sa[v][cls] = fma(c, h ? ta.y : ta.x, Sa[v][cls]);
+          Sb[v][cls] = fma(c, h ? tb.y : tb.x, Sb[v][cls]);
+        }
+      }
+    }
+    // Gauss point g (bit 0: + along tA, bit 1: + along tB) = sum over the parity classes with signs; a
+    // tangential derivative (quantity qa + 2: flip 1 for d/dtA, 2 for d/dtB) lowers one parity (sign of
+    // the points on the - side of that axis)
+    const int flipb = qa == 0 ? 1 : 2;
+    double R[2][5][4];
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const double* S = w ? Sb[v] : Sa[v];
+        const double ap = S[0] + S[1], am = S[0] - S[1];
+        const double bp = S[2] + S[3], bm = S[2] - S[3];
+        const double r[4] = {am - bm, ap - bp, am + bm, ap + bp};
+#pragma unroll
+        for (int g2 = 0; g2 < 4; ++g2) {
+          const unsigned neg = w ? ((((flipb & 1) && !(g2 & 1)) ? 1u : 0u) ^ (((flipb & 2) && !(g2 & 2)) ? 1u : 0u)) : 0u;
+          R[w][v][g2] = __longlong_as_double(__double_as_longlong(r[g2]) ^ ((long long)neg << 63));
+        }
+      }
+    __syncthreads();  // the tile is dead: its space holds the lanes' rows from here on
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+#pragma unroll
+        for (int g2 = 0; g2 < 4; ++g2) tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2)] = R[w][v][g2];
+    __syncwarp();
+  } else if (COMPACT) {
     // Face-plane parity evaluation (as k_flux): lane gp computes quantity q = gp (+ NG ...) of both
     // sides at all NG Gauss points; the results wait in registers for the block barrier (tile dead),
     // then go to their destination lanes' columns.
@@ -225,7 +320,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
     constexpr bool ROLLED = AX == 0;
     auto eval_side = [&](const int s) {
       const int cs = s ? cR : cL;
-      const double* tc = tile + FT::cbase(cs, FT::NREC);
+      const double* tc = tile + FT::cbase(cs, FT::NRH);
       const double* sc = tile + FT::STILE + FT::cbaseU(cs);
       const double* Tb = tab + s * NQ * FT::TS;
 #pragma unroll
@@ -247,11 +342,12 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
           for (int h = 0; h < 2; ++h) {
             const int kk = k2 + h;
             if (kk >= NB) break;
+            if (FT::NSPL > 1 && kk % FT::KH == 0 && kk > 0 && tma) mbar_wait(bar + kk / FT::KH, 0);  // next part
             const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
                                      : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
             const double t = h ? tt.y : tt.x;
 #pragma unroll
-            for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[(kk * 5 + v) * FT::FS], t, S[v][cls]);
+            for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[FT::faddr(kk * 5 + v)], t, S[v][cls]);
           }
         }
         const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);
@@ -323,7 +419,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       }
     } else {
       const int cs = s ? cR : cL;
-      const double* tc = tile + FT::cbase(cs, FT::NREC);
+      const double* tc = tile + FT::cbase(cs, FT::NRH);
       const double* sc = tile + FT::STILE + FT::cbaseU(cs);
       const double hs = s ? -0.5 : 0.5;
 #pragma unroll

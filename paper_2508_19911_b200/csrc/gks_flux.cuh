@@ -207,14 +207,6 @@ HD RW<T> rw_deriv(const Tg<T>& t, const Tg<T>& dt, T rho, T drho) {
 // c += rho c_X (value), X = u^p v^q w^r with G = rw_value<q, r>
 template <int p, typename T>
 HD void col_value(const T* M, const RW<T>& G, T* c) {
-#ifdef CGKS_FMA_NEST
-  c[0] = fma(M[p], G.x0, c[0]);
-  c[1] = fma(M[p + 1], G.x0, c[1]);
-  c[2] = fma(M[p], G.x1, c[2]);
-  c[3] = fma(M[p], G.x2, c[3]);
-  c[4] = fma(M[p + 2], G.x0h, fma(M[p], G.x3h, c[4]));
-  return;
-#endif
   c[0] += M[p] * G.x0;
   c[1] += M[p + 1] * G.x0;
   c[2] += M[p] * G.x1;
@@ -226,14 +218,6 @@ HD void col_value(const T* M, const RW<T>& G, T* c) {
 // dM and the pick's rho-weighted value G and derivative H
 template <int p, typename T>
 HD void col_deriv(const T* M, const T* dM, const RW<T>& G, const RW<T>& H, T* c) {
-#ifdef CGKS_FMA_NEST
-  c[0] = fma(dM[p], G.x0, fma(M[p], H.x0, c[0]));
-  c[1] = fma(dM[p + 1], G.x0, fma(M[p + 1], H.x0, c[1]));
-  c[2] = fma(dM[p], G.x1, fma(M[p], H.x1, c[2]));
-  c[3] = fma(dM[p], G.x2, fma(M[p], H.x2, c[3]));
-  c[4] = fma(dM[p + 2], G.x0h, fma(M[p + 2], H.x0h, fma(dM[p], G.x3h, fma(M[p], H.x3h, c[4]))));
-  return;
-#endif
   c[0] += dM[p] * G.x0 + M[p] * H.x0;
   c[1] += dM[p + 1] * G.x0 + M[p + 1] * H.x0;
   c[2] += dM[p] * G.x1 + M[p] * H.x1;

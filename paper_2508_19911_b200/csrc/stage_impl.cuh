@@ -279,24 +279,27 @@ int diag_fn(LaunchEnv& env, const StageArgs& a, const double* wtab, double* part
 }
 
 template <bool C>
-void flux_tile_t(int ax, int* tx, int* tn) {
+void flux_tile_t(int ax, int* tx, int* tn, int* nfbox) {
   if (ax == 0) {
     *tx = FluxTileSel<0, C>::TX;
     *tn = FluxTileSel<0, C>::TN;
+    *nfbox = FluxTileSel<0, C>::NRH;
   } else if (ax == 1) {
     *tx = FluxTileSel<(D > 1 ? 1 : 0), C>::TX;
     *tn = FluxTileSel<(D > 1 ? 1 : 0), C>::TN;
+    *nfbox = FluxTileSel<(D > 1 ? 1 : 0), C>::NRH;
   } else {
     *tx = FluxTileSel<(D > 2 ? 2 : 0), C>::TX;
     *tn = FluxTileSel<(D > 2 ? 2 : 0), C>::TN;
+    *nfbox = FluxTileSel<(D > 2 ? 2 : 0), C>::NRH;
   }
 }
 
-void flux_tile_fn(int ax, int compact, int* tx, int* tn) {
+void flux_tile_fn(int ax, int compact, int* tx, int* tn, int* nfbox) {
   if (compact)
-    flux_tile_t<true>(ax, tx, tn);
+    flux_tile_t<true>(ax, tx, tn, nfbox);
   else
-    flux_tile_t<false>(ax, tx, tn);
+    flux_tile_t<false>(ax, tx, tn, nfbox);
 }
 
 int lines_init_fn(cudaStream_t s, const double* U, double* Lb, long long ncell) {
