@@ -196,6 +196,9 @@ __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, 
 // Block tile of the reconstruction: TX x TY x TZ cells, stencil data of one component
 // (Q_v and the three gradient components) staged with a one-cell halo in shared memory by
 // cp.async, double-buffered over the five components.
+#ifndef CGKS_RECON_MINB
+#define CGKS_RECON_MINB 2  // resident reconstruction blocks per SM (register cap 128)
+#endif
 template <int DIM>
 struct ReconTile {
   static constexpr int TX = 32;
@@ -283,7 +286,7 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
 }
 
 template <int DIM, bool NONLIN, bool BOX, bool LINES = false, bool STR = false>
-__global__ void __launch_bounds__(ReconTile<DIM>::NTH, 2) k_recon5(const double* __restrict__ U,
+__global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5(const double* __restrict__ U,
                                                                     double* __restrict__ coef,
                                                                     const ErrState* __restrict__ err,
                                                                     const double* __restrict__ Lin = nullptr,
@@ -496,14 +499,16 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 // Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
 // The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
 // ---------------------------------------------------------------------------
-// threads per flux block (= Gauss points per block) per normal axis: x-faces 64 (16 faces), y-/z-faces 128
-// (32 faces) -- measured per axis (x: 1.79 vs 1.83 ms; y / z: 1.75 / 1.74 vs 1.77 / 1.77 ms); 12 warps
-// per SM either way (168 registers)
+// threads per flux block (= Gauss points per block) per normal axis: 64 (16 faces: an x-run of 16, or an
+// 8 x 2 y-/z-face patch), 6 blocks = 12 warps per SM (168 registers).  Measured per launch (ms, x / y / z):
+// x-faces 64 threads 1.535 vs 128: 1.71, 32: 1.92; y/z-faces 64 threads (8 x 2) 1.539 / 1.530 vs 128 (16 x 2)
+// 1.542 / 1.545, 128 (8 x 4) 1.62 / 1.62 (round-2 kernel); 16 warps per SM (128 registers) spill and lose
+// ~35 %
 #ifndef CGKS_FLUX_NTHR_X
 #define CGKS_FLUX_NTHR_X 64
 #endif
 #ifndef CGKS_FLUX_NTHR_YZ
-#define CGKS_FLUX_NTHR_YZ 128
+#define CGKS_FLUX_NTHR_YZ 64
 #endif
 // resident warps per SM the flux kernels are compiled for (register cap = 65536 / (32 x warps))
 #ifndef CGKS_FLUX_WARPS_X
