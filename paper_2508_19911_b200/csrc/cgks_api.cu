@@ -1732,8 +1732,10 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
     rows.push_back({"recon5", 5.0 * per_comp * nec});
     const int NG = D == 3 ? 4 : (D == 2 ? 2 : 1);
     // face-plane parity evaluation: per face side and quantity one pass over the coefficients
-    // (2 flops per coefficient and component) plus the sign combinations at the NG points
-    const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * (2.0 * (NG - 1) + 1.0)) + 2.0 * 5.0 * D * NG;
+    // (2 flops per coefficient and component) plus the butterfly of the NG parity-class sums into the NG
+    // points (NG log2 NG additions), and the scaling of the D derivatives by 1/h at each point
+    const double lg = NG > 1 ? std::log2((double)NG) : 0.0;
+    const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * lg) + 2.0 * 5.0 * D * NG;
     const double per_face = eval_face + NG * (fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
     const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
     for (int a = 0; a < D; ++a) {
