@@ -821,6 +821,8 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   // entry = (+-1/2)^{d_n} s^{d_tA + d_tB} / d! with one exponent lowered for derivatives, minus the
   // own-cell average of delta^d/d! for the value; the Gauss-point signs are applied in the kernel.
   if (ctx->scheme_id == CGKS_CGKS5) {
+    bool stretched_mesh = false;
+    for (int a = 0; a < dim; ++a) stretched_mesh = stretched_mesh || grid->nodes[a] != nullptr;
     const int nb = ctx->cls.nb, nq = dim + 1;
     const double sg = 0.5 / std::sqrt(3.0);  // 2-point Gauss-Legendre on [-1/2, 1/2] (R27)
     auto f = [](double x, int n) {
@@ -845,6 +847,9 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
               val = f(dn, e[a]) * (tA >= 0 ? f(sg, e[tA]) : 1.0) * (tB >= 0 ? f(sg, e[tB]) : 1.0);
               if (q == 0) val -= ctx->cls.avg0[kk];
             }
+            // uniform mesh: the physical derivative's 1/h_axis folded into the table (a stretched mesh
+            // scales per cell in the kernel instead)
+            if (low >= 0 && !stretched_mesh) val *= g.ih[low];
             tab[((size_t)side * nq + q) * ts + kk] = val;
           }
       }
@@ -1733,9 +1738,10 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
     const int NG = D == 3 ? 4 : (D == 2 ? 2 : 1);
     // face-plane parity evaluation: per face side and quantity one pass over the coefficients
     // (2 flops per coefficient and component) plus the butterfly of the NG parity-class sums into the NG
-    // points (NG log2 NG additions), and the scaling of the D derivatives by 1/h at each point
+    // points (NG log2 NG additions), and on a stretched mesh the scaling of the D derivatives by 1/h at each
+    // point (a uniform mesh has 1/h folded into the tables)
     const double lg = NG > 1 ? std::log2((double)NG) : 0.0;
-    const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * lg) + 2.0 * 5.0 * D * NG;
+    const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * lg) + (ctx->geo.stretched ? 2.0 * 5.0 * D * NG : 0.0);
     const double per_face = eval_face + NG * (fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
     const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
     for (int a = 0; a < D; ++a) {

@@ -413,9 +413,10 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       for (int v = 0; v < 5; ++v) {
         W[v] = rb[v * RS];
         g[0][v] = g[1][v] = g[2][v] = 0.0;
-        g[AX][v] = rb[(5 + v) * RS] * ih[AX];
-        if (DIM > 1) g[TA][v] = rb[((2 % NQ) * 5 + v) * RS] * ih[TA];
-        if (DIM > 2) g[TB][v] = rb[((3 % NQ) * 5 + v) * RS] * ih[TB];
+        // physical derivatives: 1/h is in the evaluation table on a uniform mesh, per cell on a stretched one
+        g[AX][v] = STR ? rb[(5 + v) * RS] * ih[AX] : rb[(5 + v) * RS];
+        if (DIM > 1) g[TA][v] = STR ? rb[((2 % NQ) * 5 + v) * RS] * ih[TA] : rb[((2 % NQ) * 5 + v) * RS];
+        if (DIM > 2) g[TB][v] = STR ? rb[((3 % NQ) * 5 + v) * RS] * ih[TB] : rb[((3 % NQ) * 5 + v) * RS];
       }
     } else {
       const int cs = s ? cR : cL;
