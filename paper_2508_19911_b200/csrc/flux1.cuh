@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   // tile columns of the two cells (left = side 0, right = side 1)
   const int cL = AX == 0 ? fl + 1 : fy * FX + fx;
   const int cR = AX == 0 ? fl + 2 : (fy + 1) * FX + fx;
+  CGKS_BOUND(cR, NT, "flux tile cell");
+  static_assert(!COMPACT || FT::PROWS * FT::RS <= FT::TILE, "lane rows inside the tile region");
+  static_assert(FT::STILE + 5 * NT <= FT::TILE, "tile inside its region");
   constexpr int P0 = AX, P1 = (AX + 1) % 3, P2 = (AX + 2) % 3;
   double ihL[3], ihR[3];
 #pragma unroll
@@ -307,7 +310,10 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
 #pragma unroll
       for (int v = 0; v < 5; ++v)
 #pragma unroll
-        for (int g2 = 0; g2 < 4; ++g2) tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2)] = R[w][v][g2];
+        for (int g2 = 0; g2 < 4; ++g2) {
+          CGKS_BOUND(((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2), FT::TILE, "flux eval scatter");
+          tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2)] = R[w][v][g2];
+        }
     __syncwarp();
   } else if (COMPACT) {
     // Face-plane parity evaluation (as k_flux): lane gp computes quantity q = gp (+ NG ...) of both
@@ -399,7 +405,10 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
 #pragma unroll
         for (int v = 0; v < 5; ++v)
 #pragma unroll
-          for (int g2 = 0; g2 < NG; ++g2) tile[((s * NQ + q) * 5 + v) * RS + (lane - gp + g2)] = R[s][qi][v][g2];
+          for (int g2 = 0; g2 < NG; ++g2) {
+            CGKS_BOUND(((s * NQ + q) * 5 + v) * RS + (lane - gp + g2), FT::TILE, "flux eval scatter");
+            tile[((s * NQ + q) * 5 + v) * RS + (lane - gp + g2)] = R[s][qi][v][g2];
+          }
       }
     __syncwarp();
   }
@@ -503,6 +512,11 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   constexpr int NGL_ = DIM == 3 ? 4 : (DIM == 2 ? 2 : 1);
   constexpr int NFR = COMPACT ? (LINES ? 30 + 2 * NGL_ * 10 : 30) : 10;
   const long long base = (long long)k * NFR * fpl + (long long)j * fn0 + i;
+  if (valid) {  // face records of planes [kb, ke) (the caller shifts a chunk's buffer)
+    CGKS_BOUND(i, fn0, "flux face i");
+    CGKS_BOUND(j, fn1, "flux face j");
+    CGKS_BOUND(k - kb, ke - kb, "flux face k");
+  }
   if (COMPACT && LINES && valid) {
     // line DOFs: both sides' relaxed values at this Gauss point, line order g = p * n2 + q
     const int gcan = NG == 4 ? 2 * (gp & 1) + ((gp >> 1) & 1) : gp;

@@ -178,6 +178,23 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                : "memory");
 }
 
+// Debug bounds checks (build with CGKS_NVCC_DEFS=-DCGKS_CHECK; the pool has no compute-sanitizer): an index
+// outside its buffer prints the site and traps (the context then reports CGKS_ERR_CUDA)
+#ifdef CGKS_CHECK
+#define CGKS_BOUND(i, n, what)                                                                              \
+  do {                                                                                                      \
+    if ((long long)(i) < 0 || (long long)(i) >= (long long)(n)) {                                           \
+      printf("CGKS_CHECK %s: index %lld outside [0, %lld) at %s:%d block (%d,%d,%d) thread %d\n", what,     \
+             (long long)(i), (long long)(n), __FILE__, __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x); \
+      __trap();                                                                                             \
+    }                                                                                                       \
+  } while (0)
+#else
+#define CGKS_BOUND(i, n, what) \
+  do {                         \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
                                            int j, int k) {
   if (atomicCAS(&err->code, 0, code) == 0) {
@@ -314,6 +331,9 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
   const bool valid = (i < c_geo.elo[0] + c_geo.en[0]) && (j < c_geo.elo[1] + c_geo.en[1]) &&
                      (k < c_geo.elo[2] + min(c_geo.en[2], ze));
   const int own = (DIM == 3 ? (tz + 1) * RT::HX * RT::HY : 0) + (DIM >= 2 ? (ty + 1) * RT::HX : 0) + tx + 1;
+  // the stencil reads own +- one cell per axis of the halo tile
+  CGKS_BOUND(own - 1 - (DIM >= 2 ? RT::HX : 0) - (DIM == 3 ? RT::HX * RT::HY : 0), RT::HALO, "recon halo low");
+  CGKS_BOUND(own + 1 + (DIM >= 2 ? RT::HX : 0) + (DIM == 3 ? RT::HX * RT::HY : 0), RT::HALO, "recon halo high");
   const ReconStageMap<DIM> map{reinterpret_cast<unsigned*>(rsm + 2 * RT::NFS * RT::HALO)};
   if (!BOX) {
     map.init(x0, y0, z0);
@@ -321,6 +341,10 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
   }
   // coefficient q of component v at cb[(q * 5 + v) * eplane]
   double* cb = coef + (valid ? eidx(NCO, 0, i, j, k) : 0);
+  if (valid) {  // the extended range of this launch (zb .. ze planes of the buffer)
+    CGKS_BOUND(i - c_geo.elo[0], c_geo.en[0], "recon i");
+    CGKS_BOUND(j - c_geo.elo[1], c_geo.en[1], "recon j");
+  }
   const long long ep = c_geo.en[0];  // field stride
   recon_stage<DIM, BOX>(U, rsm, 0, x0, y0, z0, map);
 #pragma unroll 1
