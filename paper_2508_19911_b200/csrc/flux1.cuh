@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
   if (COMPACT && !tma)
     for (int q = threadIdx.x; q < FT::TAB; q += blockDim.x) cp_async8(tab + q, gtab + q);
   const bool stop = __syncthreads_or(err->code != 0);
+  CGKS_JIT(5);
   cp_async_wait_all();
   if (tma) mbar_wait(bar, 0);
   if (stop) {
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
           R[w][v][g2] = __longlong_as_double(__double_as_longlong(r[g2]) ^ ((long long)neg << 63));
         }
       }
+    CGKS_JIT(3);
     __syncthreads();  // the tile is dead: its space holds the lanes' rows from here on
 #pragma unroll
     for (int w = 0; w < 2; ++w)
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
           CGKS_BOUND(((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2), FT::TILE, "flux eval scatter");
           tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2)] = R[w][v][g2];
         }
+    CGKS_JIT(4);
     __syncwarp();
   } else if (COMPACT) {
     // Face-plane parity evaluation (as k_flux): lane gp computes quantity q = gp (+ NG ...) of both
@@ -395,6 +398,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       eval_side(0);
       eval_side(1);
     }
+    CGKS_JIT(3);
     __syncthreads();  // the tile is dead: its space holds the lanes' rows from here on
 #pragma unroll
     for (int s = 0; s < 2; ++s)
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
             tile[((s * NQ + q) * 5 + v) * RS + (lane - gp + g2)] = R[s][qi][v][g2];
           }
       }
+    CGKS_JIT(4);
     __syncwarp();
   }
   // side s of this lane's Gauss point in the normal frame

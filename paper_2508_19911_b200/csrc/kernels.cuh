@@ -195,6 +195,35 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
   } while (0)
 #endif
 
+// Schedule perturbation (build with -DCGKS_JITTER): each warp sleeps a pseudo-random 0-4 us before the
+// synchronisation points of the flux and reconstruction kernels, so that a missing barrier shows up as a
+// run-to-run difference against the unperturbed build (results must stay bitwise equal)
+#ifdef CGKS_JITTER
+__device__ __forceinline__ void cgks_jitter(unsigned salt) {
+  unsigned h = (blockIdx.x * 2654435761u) ^ (blockIdx.y * 40503u) ^ (blockIdx.z * 69069u) ^ ((threadIdx.x >> 5) * 97u) ^
+               (salt * 2246822519u);
+  h ^= h >> 13;
+  h *= 3266489917u;
+  h ^= h >> 16;
+#ifdef CGKS_JITTER_ZERO
+  __nanosleep(h & 1u);
+#else
+  __nanosleep(h & 4095u);
+#endif
+}
+#ifndef CGKS_JIT_MASK
+#define CGKS_JIT_MASK 0xff
+#endif
+#define CGKS_JIT(salt)                                    \
+  do {                                                    \
+    if ((CGKS_JIT_MASK >> (salt)) & 1) cgks_jitter(salt); \
+  } while (0)
+#else
+#define CGKS_JIT(salt) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void flag_error(ErrState* err, int code, int kernel, int stage, long long step, int i,
                                            int j, int k) {
   if (atomicCAS(&err->code, 0, code) == 0) {
@@ -356,6 +385,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
+    CGKS_JIT(1);
     __syncthreads();
     Recon5TileLoader<DIM, STR> L{cur + own, 0.0, c_geo.h[0], c_geo.h[1], c_geo.h[2]};
     L.q0 = L.at(0, 0, 0, 0);
@@ -467,6 +497,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
         cv += 5 * ep;
       }
     }
+    CGKS_JIT(2);
     __syncthreads();  // this buffer is refilled by the prefetch two components ahead
   }
 }
