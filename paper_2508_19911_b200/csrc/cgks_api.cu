@@ -1682,7 +1682,7 @@ struct ParkCount {
   void put(int s, const fc::CD& v) const { slots[s] = v; }
   fc::CD get(int s) const { return slots[s]; }
 };
-static double flux_point_flops(const FluxConst& f, bool compact) {
+static double flux_point_flops(const FluxConst& f, bool compact, bool tonly = false) {
   using fc::CD;
   CD W[2][5], dW[2][3][5];
   const double w0[5] = {1.0, 0.3, -0.2, 0.1, 2.7}, w1[5] = {1.01, 0.29, -0.21, 0.12, 2.71};
@@ -1704,13 +1704,16 @@ static double flux_point_flops(const FluxConst& f, bool compact) {
       x1[20 + q] = CD::run(0.0);
     }
   }
-  interface_terms<CD>(x1, p[0], p[1], CD::run(1e-3), CD::run(1e3), f, ParkCount{slots}, acc, jump);
+  if (tonly)
+    interface_terms<CD, ParkCount, true>(x1, p[0], p[1], CD::run(1e-3), CD::run(1e3), f, ParkCount{slots}, acc, jump);
+  else
+    interface_terms<CD>(x1, p[0], p[1], CD::run(1e-3), CD::run(1e3), f, ParkCount{slots}, acc, jump);
   if (compact) {
     CD ee = relax_ee<CD>(jump, f);
     CD w = CD::run(1.0) - ee;
     for (int s = 0; s < 2; ++s)
       for (int i = 0; i < 5; ++i) {
-        acc[10 + i] = w * acc[10 + i] + ee * W[s][i];
+        if (!tonly) acc[10 + i] = w * acc[10 + i] + ee * W[s][i];
         acc[15 + i] = w * acc[15 + i] + ee * dtw[s][i];
       }
   }
@@ -1742,11 +1745,23 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
     // point (a uniform mesh has 1/h folded into the tables)
     const double lg = NG > 1 ? std::log2((double)NG) : 0.0;
     const double eval_face = 2.0 * (D + 1) * 5.0 * (2.0 * NB + NG * lg) + (ctx->geo.stretched ? 2.0 * 5.0 * D * NG : 0.0);
-    const double per_face = eval_face + NG * (fp + 30.0) + 30.0 * (NG > 1 ? std::log2((double)NG) : 0.0);
+    // per Gauss point the solver with the side relaxation (fp); per face the Gauss-point sums of the 30
+    // record values (NG - 1 additions each) and their weights 1/NG
+    const double per_face = eval_face + NG * fp + 30.0 * NG;
     const char* fnm[3] = {"flux_x", "flux_y", "flux_z"};
     for (int a = 0; a < D; ++a) {
       double nf = (double)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
       rows.push_back({fnm[a], per_face * nf});
+    }
+    if (ctx->time_scheme != CGKS_TIME_S1O2) {
+      // second S2O4 stage: only the time derivatives (F_t, Q_t; 15 record values)
+      const double fpt = flux_point_flops(ctx->fc, c5, true);
+      const double per_face_t = eval_face + NG * fpt + 15.0 * NG;
+      const char* fnt[3] = {"flux_x_t", "flux_y_t", "flux_z_t"};
+      for (int a = 0; a < D; ++a) {
+        double nf = (double)ctx->geo.fn[a][0] * ctx->geo.fn[a][1] * ctx->geo.fn[a][2];
+        rows.push_back({fnt[a], per_face_t * nf});
+      }
     }
     rows.push_back({"update", (D * (30.0 + 20.0) + 60.0) * nc});
   } else {
@@ -1768,8 +1783,10 @@ extern "C" int cgks_algorithmic_flops(const cgks_ctx* ctx, int max, char* names,
   double per_step = 0.0;
   const int stages = ctx->time_scheme == CGKS_TIME_S1O2 ? 1 : 2;
   const double nch = ctx->chunk ? (double)((ctx->geo.n[2] + ctx->chunk - 1) / ctx->chunk) : 1.0;
+  const bool split_flux = c5 && stages == 2;  // stage 1: flux_*, stage 2: flux_*_t
   for (auto& r : rows) {
-    per_step += (r.first == "dt" ? 1 : stages * nch) * r.second;
+    const bool fl = r.first.rfind("flux_", 0) == 0;
+    per_step += (r.first == "dt" ? 1 : ((fl && split_flux) ? 1 : stages) * nch) * r.second;
     if (i < max) {
       std::snprintf(names + 64 * i, 64, "%s", r.first.c_str());
       flops_per_launch[i] = r.second;

@@ -396,7 +396,9 @@ HD bool side_terms(double sgn, const T* W, const T (*dW)[5], const FluxConst& fc
 // half-range vectors x1[20..44] in parking slots 0..24 (get(i)).  Writes acc[0..9] = F^n, F_t^n
 // (Prandtl fix applied) and acc[10..19] = Q^n, Q_t^n of the interface, and the relative pressure jump
 // |pL - pR| / (pL + pR) for the side relaxation.  Returns the positivity of the equilibrium state.
-template <typename T, typename P>
+// TONLY (the second stage of S2O4, which needs only the time derivatives): only F_t^n and Q_t^n
+// (acc[5..9], acc[15..19]) are formed; acc[0..4] and acc[10..14] are left unset.
+template <typename T, typename P, bool TONLY = false>
 HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& fc, const P& park, T* acc, T& jump_out) {
   const T gm1 = fc.gamma - 1.0;
   const T r0 = x1[0], i0 = 1.0 / r0;
@@ -441,20 +443,22 @@ HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& f
     {
       const T m2 = -expm1(-0.5 * dt / tau);  // 1 - E2 without cancellation
       const T E2 = 1.0 - m2;
-      const T c3 = tau * m2 * (3.0 - E2) * idt;
       const T qq = 4.0 * tau * m2 * m2 * idt * idt;
-      al[0] = 1.0 - c3;
       be[0] = qq;
-      al[1] = 2.0 * tau * c3 - tau * (1.0 + 2.0 * E2 - E2 * E2);
       be[1] = 4.0 * tau * m2 * (dt * E2 - 2.0 * tau * m2) * idt * idt;
-      al[2] = -tau + tau * c3;
       be[2] = 1.0 - tau * qq;
-      al[3] = c3;
       be[3] = -qq;
-      al[4] = -2.0 * tau * c3 + tau * E2 * (2.0 - E2);
       be[4] = -be[1];
-      al[5] = -tau * c3;
       be[5] = tau * qq;
+      if (!TONLY) {
+        const T c3 = tau * m2 * (3.0 - E2) * idt;
+        al[0] = 1.0 - c3;
+        al[1] = 2.0 * tau * c3 - tau * (1.0 + 2.0 * E2 - E2 * E2);
+        al[2] = -tau + tau * c3;
+        al[3] = c3;
+        al[4] = -2.0 * tau * c3 + tau * E2 * (2.0 - E2);
+        al[5] = -tau * c3;
+      }
     }
     MF0[0] = r0 * U0;
     MF0[1] = r0 * U0 * U0 + p0;
@@ -467,13 +471,16 @@ HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& f
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       const T mf0 = MF0[i], mf1 = MF1[i], mf2 = MF2[i], mqa = MQa[i];
-      acc[i] = al[0] * mf0 + al[1] * mf1 + al[2] * mf2;
+      if (!TONLY) {
+        acc[i] = al[0] * mf0 + al[1] * mf1 + al[2] * mf2;
+        acc[10 + i] = (al[0] + al[3]) * x1[i] + (al[1] - al[2]) * mqa;  // MQ1 = MQa, MQ2 = -MQa (compatibility)
+      }
       acc[5 + i] = be[0] * mf0 + be[1] * mf1 + be[2] * mf2;
-      acc[10 + i] = (al[0] + al[3]) * x1[i] + (al[1] - al[2]) * mqa;  // MQ1 = MQa, MQ2 = -MQa (compatibility)
       acc[15 + i] = (be[0] + be[3]) * x1[i] + (be[1] - be[2]) * mqa;
     }
-    a20 = -U0 * sW * (al[0] - 1.0 + al[3]) + (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) +
-          al[2] * (sMF2 + U0 * sMQa);
+    if (!TONLY)
+      a20 = -U0 * sW * (al[0] - 1.0 + al[3]) + (al[0] - 1.0) * sMF0 + al[1] * (sMF1 - U0 * sMQa) +
+            al[2] * (sMF2 + U0 * sMQa);
     a21 = -U0 * sW * (be[0] + be[3]) + be[0] * sMF0 + be[1] * (sMF1 - U0 * sMQa) + (be[2] - 1.0) * (sMF2 + U0 * sMQa);
   }
   {
@@ -491,16 +498,18 @@ HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& f
     const T s5 = qF(v5, U0, V0, Ww0, uu2) - U0 * qF(q5, U0, V0, Ww0, uu2);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
+      if (!TONLY) {
+        acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
+        acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
+      }
       acc[5 + i] += be[3] * v3[i] + be[4] * v4[i] + be[5] * v5[i];
-      acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
       acc[15 + i] += be[4] * q4[i] + be[5] * q5[i];
     }
-    a20 += al[3] * s3 + al[4] * s4 + al[5] * s5;
+    if (!TONLY) a20 += al[3] * s3 + al[4] * s4 + al[5] * s5;
     a21 += be[3] * s3 + be[4] * s4 + be[5] * s5;
   }
   if (fc.Pr != 1.0) {  // Prandtl fix (R20)
-    acc[4] += fc.pfix * a20;
+    if (!TONLY) acc[4] += fc.pfix * a20;
     acc[9] += fc.pfix * a21;
   }
   return good;

@@ -89,10 +89,10 @@ int recon5_launch(LaunchEnv& env, const StageArgs& a) {
 template <int AX, bool COMPACT>
 using FluxTileSel = FluxTile1<D, AX, COMPACT>;
 
-template <bool COMPACT, bool BOX, int AX, bool LINES = false, bool STR = false>
+template <bool COMPACT, bool BOX, int AX, bool LINES = false, bool STR = false, bool TONLY = false>
 int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage) {
   using FT = FluxTileSel<AX, COMPACT>;
-  auto kern = k_flux1<D, AX, COMPACT, BOX, LINES, STR>;
+  auto kern = k_flux1<D, AX, COMPACT, BOX, LINES, STR, TONLY>;
   static bool attr = false;
   const size_t smem = FT::smem_bytes();
   if (!attr) {
@@ -154,7 +154,13 @@ int stage_t(LaunchEnv& env, const StageArgs& a, int mode, int stage) {
     }
     if (a.part == 1) return 0;
   }
-  {
+  if (COMPACT && mode == 1) {
+    // second stage of S2O4: the update uses only the time derivatives (flux kernels "flux_*_t")
+    int rc = flux_launch<COMPACT, BOX, 0, LINES, STR, true>(env, "flux_x_t", a, stage);
+    if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0), LINES, STR, true>(env, "flux_y_t", a, stage);
+    if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES, STR, true>(env, "flux_z_t", a, stage);
+    if (rc) return rc;
+  } else {
     int rc = flux_launch<COMPACT, BOX, 0, LINES, STR>(env, "flux_x", a, stage);
     if (!rc && D > 1) rc = flux_launch<COMPACT, BOX, (D > 1 ? 1 : 0), LINES, STR>(env, "flux_y", a, stage);
     if (!rc && D > 2) rc = flux_launch<COMPACT, BOX, (D > 2 ? 2 : 0), LINES, STR>(env, "flux_z", a, stage);

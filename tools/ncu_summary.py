@@ -94,9 +94,9 @@ BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def bench_name(kernel):
-    m = re.search(r"k_flux1?<(\d+), (\d+),", kernel)
-    if m:
-        return "flux_" + "xyz"[int(m.group(2))]
+    m = re.search(r"k_flux1?<(\d+), (\d+), \d+, \d+, \d+, \d+(?:, (\d+))?>", kernel)
+    if m:  # the 7th template argument (TONLY) marks the second-stage sweeps
+        return "flux_" + "xyz"[int(m.group(2))] + ("_t" if m.group(3) == "1" else "")
     for k in ("recon5", "recon2", "update", "dt_finalize", "dt", "step_end", "pack", "unpack"):
         if "k_" + k + "<" in kernel or kernel.startswith("k_" + k) or "::k_" + k in kernel:
             return k
