@@ -536,56 +536,104 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       for (int q = TONLY ? 5 : 0; q < 10; ++q) dst[q * fpl] = y[10 + 10 * s + q];
     }
   }
-  // the record fields this launch writes: all NR, or (TONLY) F_t, Q^L_t, Q^R_t (CGKS-5th) / F_t (GKS-2nd)
-  constexpr int NO = TONLY ? (COMPACT ? 15 : 5) : NR;
-  auto fld = [](int o) { return !TONLY ? o : (o < 5 ? 5 + o : (o < 10 ? 15 + (o - 5) : 25 + (o - 10))); };
-  double yo[NO];
+  if constexpr (!TONLY) {
+    if constexpr (NG == 1) {
+      if (valid)
 #pragma unroll
-  for (int o = 0; o < NO; ++o) yo[o] = y[fld(o)];
-  if constexpr (NG == 1) {
-    if (valid)
-#pragma unroll
-      for (int o = 0; o < NO; ++o) face[base + fld(o) * fpl] = yo[o];
-  } else {
-    // Gauss-point sum by a reduce-scatter over the face's NG lanes: round 1 (partner gp ^ 1) splits the NO
-    // outputs into H1 + (NO - H1), round 2 (gp ^ 2, NG = 4) each half into H2 + rest; every sum is
-    // (g0 + g1) + (g2 + g3) whichever lane forms it (deterministic); weight 1/NG after the sum
-    // (a sum through the lanes' shared-memory rows instead: slower, measured twice)
-    constexpr int H1 = (NO + 1) / 2, H2 = (H1 + 1) / 2;
-    const bool up = gp & 1;
-    double z[H1];
-#pragma unroll
-    for (int q = 0; q < H1; ++q) {
-      const double hi = H1 + q < NO ? yo[H1 + q < NO ? H1 + q : 0] : 0.0;
-      const double send = up ? yo[q] : hi;
-      const double keep = up ? hi : yo[q];
-      z[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-    }
-    const double wgt = 1.0 / NG;
-    const int lim = up ? NO : H1;  // end of this lane's half
-    if constexpr (NG == 2) {
-      if (valid) {
-        const int o0 = up ? H1 : 0;
-#pragma unroll
-        for (int q = 0; q < H1; ++q)
-          if (o0 + q < lim) face[base + fld(o0 + q) * fpl] = wgt * z[q];
-      }
+        for (int q = 0; q < NR; ++q) face[base + q * fpl] = y[q];
     } else {
-      const bool up2 = gp & 2;
-      double zz[H2];
+      // Gauss-point sum by a reduce-scatter over the face's NG lanes: round 1 (partner gp ^ 1) halves
+      // the 30 values, round 2 (gp ^ 2, NG = 4) splits the 15 into 8 + 7; every sum is
+      // (g0 + g1) + (g2 + g3) whichever lane forms it (deterministic); weight 1/NG after the sum
+      // (a sum through the lanes' shared-memory rows instead: 3 % slower per step, measured)
+      constexpr int H = NR / 2;  // 15
+      const bool up = gp & 1;
+      double z[16];
 #pragma unroll
-      for (int q = 0; q < H2; ++q) {
-        const double hi = H2 + q < H1 ? z[H2 + q < H1 ? H2 + q : 0] : 0.0;
-        const double send = up2 ? z[q] : hi;
-        const double keep = up2 ? hi : z[q];
-        zz[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      for (int q = 0; q < H; ++q) {
+        const double send = up ? y[q] : y[H + q];
+        const double keep = up ? y[H + q] : y[q];
+        z[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
       }
-      if (valid) {
-        const int o0 = (up ? H1 : 0) + (up2 ? H2 : 0);
-        const int lim2 = up2 ? lim : (up ? H1 : 0) + H2;
+      z[15] = 0.0;
+      const double wgt = 1.0 / NG;
+      if constexpr (NG == 2) {
+        if (valid) {
+          double* dst = face + base + (long long)(up ? H : 0) * fpl;
 #pragma unroll
-        for (int q = 0; q < H2; ++q)
-          if (o0 + q < lim2) face[base + fld(o0 + q) * fpl] = wgt * zz[q];
+          for (int q = 0; q < H; ++q) dst[q * fpl] = wgt * z[q];
+        }
+      } else {
+        const bool up2 = gp & 2;
+        double zz[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double send = up2 ? z[q] : z[8 + q];
+          const double keep = up2 ? z[8 + q] : z[q];
+          zz[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        if (valid) {
+          const int o0 = (up ? H : 0) + (up2 ? 8 : 0);
+          const int cnt = up2 ? H - 8 : 8;
+          double* dst = face + base + (long long)o0 * fpl;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < cnt) dst[q * fpl] = wgt * zz[q];
+        }
+      }
+    }
+  } else {
+  // the record fields this launch writes: all NR, or (TONLY) F_t, Q^L_t, Q^R_t (CGKS-5th) / F_t (GKS-2nd)
+    constexpr int NO = TONLY ? (COMPACT ? 15 : 5) : NR;
+    auto fld = [](int o) { return !TONLY ? o : (o < 5 ? 5 + o : (o < 10 ? 15 + (o - 5) : 25 + (o - 10))); };
+    double yo[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) yo[o] = y[fld(o)];
+    if constexpr (NG == 1) {
+      if (valid)
+#pragma unroll
+        for (int o = 0; o < NO; ++o) face[base + fld(o) * fpl] = yo[o];
+    } else {
+      // Gauss-point sum by a reduce-scatter over the face's NG lanes: round 1 (partner gp ^ 1) splits the NO
+      // outputs into H1 + (NO - H1), round 2 (gp ^ 2, NG = 4) each half into H2 + rest; every sum is
+      // (g0 + g1) + (g2 + g3) whichever lane forms it (deterministic); weight 1/NG after the sum
+      // (a sum through the lanes' shared-memory rows instead: slower, measured twice)
+      constexpr int H1 = (NO + 1) / 2, H2 = (H1 + 1) / 2;
+      const bool up = gp & 1;
+      double z[H1];
+#pragma unroll
+      for (int q = 0; q < H1; ++q) {
+        const double hi = H1 + q < NO ? yo[H1 + q < NO ? H1 + q : 0] : 0.0;
+        const double send = up ? yo[q] : hi;
+        const double keep = up ? hi : yo[q];
+        z[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+      const double wgt = 1.0 / NG;
+      const int lim = up ? NO : H1;  // end of this lane's half
+      if constexpr (NG == 2) {
+        if (valid) {
+          const int o0 = up ? H1 : 0;
+#pragma unroll
+          for (int q = 0; q < H1; ++q)
+            if (o0 + q < lim) face[base + fld(o0 + q) * fpl] = wgt * z[q];
+        }
+      } else {
+        const bool up2 = gp & 2;
+        double zz[H2];
+#pragma unroll
+        for (int q = 0; q < H2; ++q) {
+          const double hi = H2 + q < H1 ? z[H2 + q < H1 ? H2 + q : 0] : 0.0;
+          const double send = up2 ? z[q] : hi;
+          const double keep = up2 ? hi : z[q];
+          zz[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        if (valid) {
+          const int o0 = (up ? H1 : 0) + (up2 ? H2 : 0);
+          const int lim2 = up2 ? lim : (up ? H1 : 0) + H2;
+#pragma unroll
+          for (int q = 0; q < H2; ++q)
+            if (o0 + q < lim2) face[base + fld(o0 + q) * fpl] = wgt * zz[q];
+        }
       }
     }
   }
