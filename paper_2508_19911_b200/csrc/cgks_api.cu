@@ -793,12 +793,14 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
         ctx->ops->flux_tile(a, ctx->scheme_id == CGKS_CGKS5 ? 1 : 0, &tx, &tn, &nfbox);
         const cuuint32_t by = a == 1 ? tn : 1, bz = a == 2 ? tn : 1;
         {
-          // [z][y][field][x]: dims (x, field, y, z)
-          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0], (cuuint64_t)nrec, (cuuint64_t)g.en[1],
+          // GKS-2nd [z][y][field][x]: dims (x, field, y, z); CGKS-5th [z][y][pair][x][2] (cidx): dims (2 x, pair,
+          // y, z), rows of 2 x the tile width
+          const int pw = ctx->scheme_id == CGKS_CGKS5 ? 2 : 1;
+          const cuuint64_t dims[4] = {(cuuint64_t)g.en[0] * pw, (cuuint64_t)nrec / pw, (cuuint64_t)g.en[1],
                                       (cuuint64_t)(ctx->chunk ? ctx->chunk + 2 : g.en[2])};
-          const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * 8, (cuuint64_t)g.en[0] * nrec * 8,
+          const cuuint64_t str[3] = {(cuuint64_t)g.en[0] * pw * 8, (cuuint64_t)g.en[0] * nrec * 8,
                                      (cuuint64_t)g.eplane * nrec * 8};
-          const cuuint32_t box[4] = {(cuuint32_t)tx, (cuuint32_t)nfbox, by, bz};  // one part of the fields
+          const cuuint32_t box[4] = {(cuuint32_t)(tx * pw), (cuuint32_t)(nfbox / pw), by, bz};
           good = good && encode(&ctx->tm_rec[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->rec, dims, str, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

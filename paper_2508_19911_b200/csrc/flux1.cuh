@@ -58,6 +58,12 @@ struct FluxTile1 {
   __host__ __device__ static constexpr int cbase(int c, int nfield) {
     return AX == 0 ? c : (c / FX) * nfield * FX + c % FX;
   }
+  // CGKS-5th: the coefficient pairs of the global layout (cidx) arrive as they are: tile row r (one x-row of
+  // FS cells) holds [pair p][cell x][2], so coefficient kk of component v of tile cell c is at
+  // pbase(c) + coef(kk, v); GKS-2nd keeps one field per TMA row (faddr / cbase)
+  static_assert(!COMPACT || NSPL == 1, "coefficient pairs: one TMA part");
+  __host__ __device__ static constexpr int pbase(int c) { return AX == 0 ? 2 * c : (c / FX) * NREC * FX + 2 * (c % FX); }
+  __host__ __device__ static constexpr int coef(int kk, int v) { return ((kk >> 1) * 5 + v) * 2 * FS + (kk & 1); }
   static constexpr int FSU = AX == 2 ? FX : NT;
   __host__ __device__ static constexpr int cbaseU(int c) { return AX == 2 ? (c / FX) * 5 * FX + c % FX : c; }
   static constexpr int STILE = NSPL * PSTR;
@@ -99,7 +105,13 @@ struct ParkDev1 {
 // state; the kernel then forms and stores only those (half of the face record; k_update<MODE 1> reads
 // nothing else)
 template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR = false, bool TONLY = false>
-__global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<DIM, AX, COMPACT>::MINB) k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
+__global__ void
+#ifdef CGKS_FLUX_MAXNREG
+__maxnreg__(CGKS_FLUX_MAXNREG)
+#else
+__launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<DIM, AX, COMPACT>::MINB)
+#endif
+k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
                                                 const double* __restrict__ gtab, double* __restrict__ face,
                                                 const TimeState* __restrict__ ts, ErrState* __restrict__ err,
                                                 int stage, const __grid_constant__ CUtensorMap tm_rec,
@@ -136,8 +148,8 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
       for (int p = 1; p < FT::NSPL; ++p) mbar_expect_tx(bar + p, (unsigned)(sizeof(double) * FT::NRH * NT));
 #pragma unroll
       for (int p = 0; p < FT::NSPL; ++p)
-        tma_load_4d(tile + p * FT::PSTR, &tm_rec, bar + p, x0 - c_geo.elo[0], p * FT::NRH, y0 - c_geo.elo[1],
-                    z0 - c_geo.elo[2] - kofs);
+        tma_load_4d(tile + p * FT::PSTR, &tm_rec, bar + p, COMPACT ? 2 * (x0 - c_geo.elo[0]) : x0 - c_geo.elo[0],
+                    COMPACT ? 0 : p * FT::NRH, y0 - c_geo.elo[1], z0 - c_geo.elo[2] - kofs);
       tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
       if (COMPACT) bulk_load(tab, gtab, (unsigned)(sizeof(double) * FT::TAB), bar);
     }
@@ -167,12 +179,22 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
         if (ck > kmax) ck = kmax;
       }
       const long long st = c_geo.en[0];  // field stride of the reconstruction array
-      const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
-      const unsigned dst0 = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NRH));
+      if (COMPACT) {  // 16-byte coefficient pairs (cidx layout)
+        const double* src = rec + cidx(FT::NREC, 0, 0, ci, cj, ck) + fsub * 2 * st;
+        const unsigned dst0 = (unsigned)__cvta_generic_to_shared(tile + FT::pbase(c));
 #pragma unroll 4
-      for (int fld = fsub; fld < FT::NREC; fld += TPC) {
-        cp_async8s(dst0 + FT::faddr(fld) * (unsigned)sizeof(double), src);
-        src += TPC * st;
+        for (int pr = fsub; pr < FT::NREC / 2; pr += TPC) {
+          cp_async16s(dst0 + pr * 2 * FT::FS * (unsigned)sizeof(double), src);
+          src += TPC * 2 * st;
+        }
+      } else {
+        const double* src = rec + eidx(FT::NREC, 0, ci, cj, ck) + fsub * st;
+        const unsigned dst0 = (unsigned)__cvta_generic_to_shared(tile + FT::cbase(c, FT::NRH));
+#pragma unroll 4
+        for (int fld = fsub; fld < FT::NREC; fld += TPC) {
+          cp_async8s(dst0 + FT::faddr(fld) * (unsigned)sizeof(double), src);
+          src += TPC * st;
+        }
       }
       double* sdst = tile + FT::STILE + FT::cbaseU(c);
       if (BOX) {
@@ -260,7 +282,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
     // the results wait in registers for the block barrier (tile dead), then go to their lanes' columns.
     const int sd = gp & 1, qa = gp >> 1;
     const int cs = sd ? cR : cL;
-    const double* tc = tile + FT::cbase(cs, FT::NRH);
+    const double* tc = tile + FT::pbase(cs);
     const double* sc = tile + FT::STILE + FT::cbaseU(cs);
     const double* Ta = tab + (sd * NQ + qa) * FT::TS;
     const double* Tb = Ta + 2 * FT::TS;
@@ -276,17 +298,15 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
     for (int k2 = 0; k2 < NB; k2 += 2) {
       const double2 ta = *reinterpret_cast<const double2*>(Ta + k2);
       const double2 tb = *reinterpret_cast<const double2*>(Tb + k2);
+      const int cls0 = (ReconGen<DIM>::expo(k2, TA) & 1) | ((ReconGen<DIM>::expo(k2, TB) & 1) << 1);
+      const int cls1 = (ReconGen<DIM>::expo(k2 + 1, TA) & 1) | ((ReconGen<DIM>::expo(k2 + 1, TB) & 1) << 1);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kk = k2 + h;
-        if (kk >= NB) break;
-        const int cls = (ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          const double c = tc[FT::faddr(kk * 5 + v)];
-          Sa[v][cls] = fma(c, h ? ta.y : ta.x, Sa[v][cls]);
-          Sb[v][cls] = fma(c, h ? tb.y : tb.x, Sb[v][cls]);
-        }
+      for (int v = 0; v < 5; ++v) {
+        const double2 c = *reinterpret_cast<const double2*>(tc + FT::coef(k2, v));  // coefficients k2, k2 + 1
+        Sa[v][cls0] = fma(c.x, ta.x, Sa[v][cls0]);
+        Sb[v][cls0] = fma(c.x, tb.x, Sb[v][cls0]);
+        Sa[v][cls1] = fma(c.y, ta.y, Sa[v][cls1]);
+        Sb[v][cls1] = fma(c.y, tb.y, Sb[v][cls1]);
       }
     }
     // Gauss point g (bit 0: + along tA, bit 1: + along tB) = sum over the parity classes with signs; a
@@ -332,7 +352,7 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
     constexpr bool ROLLED = AX == 0;
     auto eval_side = [&](const int s) {
       const int cs = s ? cR : cL;
-      const double* tc = tile + FT::cbase(cs, FT::NRH);
+      const double* tc = tile + FT::pbase(cs);
       const double* sc = tile + FT::STILE + FT::cbaseU(cs);
       const double* Tb = tab + s * NQ * FT::TS;
 #pragma unroll
@@ -354,12 +374,11 @@ __global__ void __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<D
           for (int h = 0; h < 2; ++h) {
             const int kk = k2 + h;
             if (kk >= NB) break;
-            if (FT::NSPL > 1 && kk % FT::KH == 0 && kk > 0 && tma) mbar_wait(bar + kk / FT::KH, 0);  // next part
             const int cls = DIM == 3 ? ((ReconGen<DIM>::expo(kk, TA) & 1) | ((ReconGen<DIM>::expo(kk, TB) & 1) << 1))
                                      : (DIM == 2 ? (ReconGen<DIM>::expo(kk, TA) & 1) : 0);
             const double t = h ? tt.y : tt.x;
 #pragma unroll
-            for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[FT::faddr(kk * 5 + v)], t, S[v][cls]);
+            for (int v = 0; v < 5; ++v) S[v][cls] = fma(tc[FT::coef(kk, v)], t, S[v][cls]);
           }
         }
         const int flip = q == 2 ? 1 : (q == 3 ? 2 : 0);

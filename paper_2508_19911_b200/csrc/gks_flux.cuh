@@ -208,22 +208,22 @@ HD RW<T> rw_deriv(const Tg<T>& t, const Tg<T>& dt, T rho, T drho) {
 // c += rho c_X (value), X = u^p v^q w^r with G = rw_value<q, r>
 template <int p, typename T>
 HD void col_value(const T* M, const RW<T>& G, T* c) {
-  c[0] += M[p] * G.x0;
-  c[1] += M[p + 1] * G.x0;
-  c[2] += M[p] * G.x1;
-  c[3] += M[p] * G.x2;
-  c[4] += M[p + 2] * G.x0h + M[p] * G.x3h;
+  c[0] = fma(M[p], G.x0, c[0]);
+  c[1] = fma(M[p + 1], G.x0, c[1]);
+  c[2] = fma(M[p], G.x1, c[2]);
+  c[3] = fma(M[p], G.x2, c[3]);
+  c[4] = fma(M[p + 2], G.x0h, fma(M[p], G.x3h, c[4]));
 }
 
 // c += D[rho c_X] = rho dc_X + drho c_X: directional derivative, with the normal moments' derivative
 // dM and the pick's rho-weighted value G and derivative H
 template <int p, typename T>
 HD void col_deriv(const T* M, const T* dM, const RW<T>& G, const RW<T>& H, T* c) {
-  c[0] += dM[p] * G.x0 + M[p] * H.x0;
-  c[1] += dM[p + 1] * G.x0 + M[p + 1] * H.x0;
-  c[2] += dM[p] * G.x1 + M[p] * H.x1;
-  c[3] += dM[p] * G.x2 + M[p] * H.x2;
-  c[4] += dM[p + 2] * G.x0h + M[p + 2] * H.x0h + dM[p] * G.x3h + M[p] * H.x3h;
+  c[0] = fma(dM[p], G.x0, fma(M[p], H.x0, c[0]));
+  c[1] = fma(dM[p + 1], G.x0, fma(M[p + 1], H.x0, c[1]));
+  c[2] = fma(dM[p], G.x1, fma(M[p], H.x1, c[2]));
+  c[3] = fma(dM[p], G.x2, fma(M[p], H.x2, c[3]));
+  c[4] = fma(dM[p + 2], G.x0h, fma(M[p + 2], H.x0h, fma(dM[p], G.x3h, fma(M[p], H.x3h, c[4]))));
 }
 
 // derivative of the normal moments M_0..M_4 along (dU, dlam):
@@ -250,7 +250,7 @@ HD void moments_deriv(const T* A, const T* B, T lam, T dU, T dlam, T* dM) {
 // qF(v) = v_E - U0 . v_mom + |U0|^2/2 v_rho; a state vector Q contributes -U0n qF(Q)
 template <typename T>
 HD T qF(const T* v, T U0, T V0, T W0, T uu2) {
-  return v[4] - (U0 * v[1] + V0 * v[2] + W0 * v[3]) + uu2 * v[0];
+  return fma(uu2, v[0], fma(-U0, v[1], fma(-V0, v[2], fma(-W0, v[3], v[4]))));
 }
 
 // ---------------------------------------------------------------------------
@@ -272,7 +272,7 @@ HD Dprim<T> dprim(T ir, const T* U, T uu2, double gm1, const T* d) {
   q.dr = d[0];
 #pragma unroll
   for (int i = 0; i < 3; ++i) q.du[i] = (d[1 + i] - U[i] * d[0]) * ir;
-  q.dp = gm1 * (d[4] - (U[0] * d[1] + U[1] * d[2] + U[2] * d[3]) + uu2 * d[0]);
+  q.dp = gm1 * fma(uu2, d[0], fma(-U[0], d[1], fma(-U[1], d[2], fma(-U[2], d[3], d[4]))));
   q.udu = U[0] * q.du[0] + U[1] * q.du[1] + U[2] * q.du[2];
   return q;
 }
@@ -280,15 +280,15 @@ HD Dprim<T> dprim(T ir, const T* U, T uu2, double gm1, const T* d) {
 // acc += s DF_al(W) d, F_al = (m_al, m_al U + p e_al, U_al (E + p)) the Euler flux along al
 template <int AL, typename T, typename S>
 HD void jvp_flux(T rho, const T* U, T p, T E, const T* d, const Dprim<T>& q, S s, T* acc) {
-  const T mA = rho * U[AL];
-  acc[0] += s * d[1 + AL];
+  // s = +-1 (a sign, folded into the FMAs): acc += s * DF d as FMA chains into the accumulators
+  const T smA = s * (rho * U[AL]), sd = s * d[1 + AL];
+  acc[0] += sd;
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
-    T v = d[1 + AL] * U[b] + mA * q.du[b];
-    if (b == AL) v += q.dp;
-    acc[1 + b] += s * v;
+    const T a = b == AL ? acc[1 + b] + s * q.dp : acc[1 + b];
+    acc[1 + b] = fma(sd, U[b], fma(smA, q.du[b], a));
   }
-  acc[4] += s * (q.du[AL] * (E + p) + U[AL] * (d[4] + q.dp));
+  acc[4] = fma(s * q.du[AL], E + p, fma(s * U[AL], d[4] + q.dp, acc[4]));
 }
 
 // acc += DH_al(W) d, H_al = rho <u_n u_al psi> (n = 0, the face normal):
@@ -299,21 +299,22 @@ template <int AL, typename T>
 HD void jvp_flux2(T rho, T ir, const T* U, T p, T uu, double K5, double K7, const Dprim<T>& q, T* acc) {
   const T UnUa = U[0] * U[AL];
   const T dUnUa = q.du[0] * U[AL] + U[0] * q.du[AL];
-  acc[0] += q.dr * UnUa + rho * dUnUa;
-  if (AL == 0) acc[0] += q.dp;
+  const T cU = q.dr * UnUa + rho * dUnUa;  // D(rho U_n U_al)
+  const T rU = rho * UnUa;
+  acc[0] += AL == 0 ? cU + q.dp : cU;
 #pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    T v = q.dr * UnUa * U[b] + rho * (dUnUa * U[b] + UnUa * q.du[b]);
-    if (AL == 0) v += q.dp * U[b] + p * q.du[b];
-    if (b == 0) v += q.dp * U[AL] + p * q.du[AL];
-    if (AL == b) v += q.dp * U[0] + p * q.du[0];
-    acc[1 + b] += v;
+  for (int b = 0; b < 3; ++b) {  // FMA chains into the accumulators
+    T a = acc[1 + b];
+    if (AL == 0) a = fma(q.dp, U[b], fma(p, q.du[b], a));
+    if (b == 0) a = fma(q.dp, U[AL], fma(p, q.du[AL], a));
+    if (AL == b) a = fma(q.dp, U[0], fma(p, q.du[0], a));
+    acc[1 + b] = fma(cU, U[b], fma(rU, q.du[b], a));
   }
   const T c1 = rho * uu + K7 * p;
   const T dc1 = q.dr * uu + 2.0 * rho * q.udu + K7 * q.dp;
   T v4 = dc1 * UnUa + c1 * dUnUa;
   if (AL == 0) v4 += q.dp * uu + 2.0 * p * q.udu + K5 * p * ir * (2.0 * q.dp - p * ir * q.dr);
-  acc[4] += 0.5 * v4;
+  acc[4] = fma(0.5, v4, acc[4]);
 }
 
 // ---------------------------------------------------------------------------
@@ -499,18 +500,18 @@ HD bool interface_terms(const T* x1, T pL, T pR, T dt, T idt, const FluxConst& f
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       if (!TONLY) {
-        acc[i] += al[3] * v3[i] + al[4] * v4[i] + al[5] * v5[i];
-        acc[10 + i] += al[4] * q4[i] + al[5] * q5[i];
+        acc[i] = fma(al[3], v3[i], fma(al[4], v4[i], fma(al[5], v5[i], acc[i])));
+        acc[10 + i] = fma(al[4], q4[i], fma(al[5], q5[i], acc[10 + i]));
       }
-      acc[5 + i] += be[3] * v3[i] + be[4] * v4[i] + be[5] * v5[i];
-      acc[15 + i] += be[4] * q4[i] + be[5] * q5[i];
+      acc[5 + i] = fma(be[3], v3[i], fma(be[4], v4[i], fma(be[5], v5[i], acc[5 + i])));
+      acc[15 + i] = fma(be[4], q4[i], fma(be[5], q5[i], acc[15 + i]));
     }
-    if (!TONLY) a20 += al[3] * s3 + al[4] * s4 + al[5] * s5;
-    a21 += be[3] * s3 + be[4] * s4 + be[5] * s5;
+    if (!TONLY) a20 = fma(al[3], s3, fma(al[4], s4, fma(al[5], s5, a20)));
+    a21 = fma(be[3], s3, fma(be[4], s4, fma(be[5], s5, a21)));
   }
   if (fc.Pr != 1.0) {  // Prandtl fix (R20)
-    if (!TONLY) acc[4] += fc.pfix * a20;
-    acc[9] += fc.pfix * a21;
+    if (!TONLY) acc[4] = fma(fc.pfix, a20, acc[4]);
+    acc[9] = fma(fc.pfix, a21, acc[9]);
   }
   return good;
 }

@@ -122,6 +122,21 @@ __device__ __forceinline__ long long eidx(int NF, int f, int i, int j, int k) {
   return (((long long)kk * c_geo.en[1] + jj) * NF + f) * c_geo.en[0] + ii;
 }
 
+// CGKS-5th reconstruction coefficients (5 NB per cell): layout [z][y][pair][x][2] with pair p = (kk / 2) * 5 + v,
+// i.e. the coefficients kk and kk + 1 (kk even) of component v of one cell side by side: one 16-byte store in
+// the reconstruction, one 16-byte shared-memory load in the flux evaluation, and TMA rows of 2 x the tile
+// width (half as many rows as one field per row)
+__device__ __forceinline__ long long cidx(int NCO, int kk, int v, int i, int j, int k) {
+  int ii = c_geo.bounded[0] ? i : wrapi(i, c_geo.n[0]);
+  int jj = c_geo.bounded[1] ? j : wrapi(j, c_geo.n[1]);
+  int kz = c_geo.bounded[2] ? k : wrapi(k, c_geo.n[2]);
+  ii -= c_geo.elo[0];
+  jj -= c_geo.elo[1];
+  kz -= c_geo.elo[2];
+  return ((long long)kz * c_geo.en[1] + jj) * NCO * c_geo.en[0] + (long long)((kk >> 1) * 5 + v) * 2 * c_geo.en[0] +
+         2 * ii + (kk & 1);
+}
+
 // stretched meshes (R37): width / inverse width of cell index c along a (c in -2 .. n+1)
 __device__ __forceinline__ double cw(int a, int c) { return __ldg(c_geo.hw[a] + c + 2); }
 __device__ __forceinline__ double icw(int a, int c) { return __ldg(c_geo.ihw[a] + c + 2); }
@@ -133,6 +148,9 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_s
 }
 __device__ __forceinline__ void cp_async8s(unsigned smem_addr, const double* gmem_src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async16s(unsigned smem_addr, const double* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -368,8 +386,8 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
     map.init(x0, y0, z0);
     __syncthreads();
   }
-  // coefficient q of component v at cb[(q * 5 + v) * eplane]
-  double* cb = coef + (valid ? eidx(NCO, 0, i, j, k) : 0);
+  // coefficients (q, q + 1) (q even) of component v at cb[((q / 2) * 5 + v) * 2 * en0 + {0, 1}] (cidx)
+  double* cb = coef + (valid ? cidx(NCO, 0, 0, i, j, k) : 0);
   if (valid) {  // the extended range of this launch (zb .. ze planes of the buffer)
     CGKS_BOUND(i - c_geo.elo[0], c_geo.en[0], "recon i");
     CGKS_BOUND(j - c_geo.elo[1], c_geo.en[1], "recon j");
@@ -488,13 +506,14 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
       for (int a = 0; a < DIM; ++a) acc[a] = fma(1.0 - chi, lin[a], acc[a]);
     }
     if (valid) {
-      double* cv = cb + v * ep;
+      double2* cv = reinterpret_cast<double2*>(cb + v * 2 * ep);
+      static_assert(S::NB % 2 == 0, "coefficient pairs");
 #pragma unroll
-      for (int q = 0; q < S::NB; ++q) {
-        // streaming store (evict-first: the coefficients are read back from HBM by the sweeps anyway):
-        // 0.624 vs 0.637 ms per launch; running pointer, no per-coefficient index arithmetic
-        __stcs(cv, acc[q]);
-        cv += 5 * ep;
+      for (int q = 0; q < S::NB; q += 2) {
+        // streaming 16-byte store (evict-first: the coefficients are read back from HBM by the sweeps anyway);
+        // running pointer, no per-coefficient index arithmetic
+        __stcs(cv, make_double2(acc[q], acc[q + 1]));
+        cv += 5 * ep;  // next pair of this component: 5 pairs of 2 x en0 doubles on
       }
     }
     CGKS_JIT(2);
@@ -929,14 +948,14 @@ __global__ void __launch_bounds__(256) k_diag(const double* __restrict__ U, cons
     const double w = gw[pi] * (DIM >= 2 ? gw[pj] : 1.0) * (DIM >= 3 ? gw[pk] : 1.0) * hc[0] * hc[1] * hc[2];
     double W[5], dW[3][5];
     if (COMPACT) {
-      const double* cb = rec + eidx(NB * 5, 0, i, j, k);
-      const long long ep = c_geo.en[0];  // field stride
+      const double* cb = rec + cidx(NB * 5, 0, 0, i, j, k);
+      const long long ep = c_geo.en[0];  // pair stride / 2
       const double* wv = wt + p * 4 * NB;
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         double val = __ldg(U + sidx(NV, v, i, j, k)), d0 = 0.0, d1 = 0.0, d2 = 0.0;
         for (int kk = 0; kk < NB; ++kk) {
-          const double c = __ldg(cb + (long long)(kk * 5 + v) * ep);
+          const double c = __ldg(cb + (long long)((kk >> 1) * 5 + v) * 2 * ep + (kk & 1));
           val = fma(c, wv[kk], val);
           d0 = fma(c, wv[NB + kk], d0);
           d1 = fma(c, wv[2 * NB + kk], d1);
@@ -1026,11 +1045,11 @@ __global__ void __launch_bounds__(256) k_qcrit(const double* __restrict__ U, con
 #pragma unroll
     for (int a = 0; a < 3; ++a) dW[a][v] = 0.0;
     if (COMPACT) {
-      for (int kk = 0; kk < NB; ++kk) W[v] = fma(__ldg(rec + eidx(NB * 5, kk * 5 + v, i, j, k)), wc[kk], W[v]);
+      for (int kk = 0; kk < NB; ++kk) W[v] = fma(__ldg(rec + cidx(NB * 5, kk, v, i, j, k)), wc[kk], W[v]);
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
         static_assert(ReconGen<DIM>::expo(0, 0) == 1, "linear basis functions first");
-        dW[a][v] = __ldg(rec + eidx(NB * 5, a * 5 + v, i, j, k)) * ihc[a];
+        dW[a][v] = __ldg(rec + cidx(NB * 5, a, v, i, j, k)) * ihc[a];
       }
     } else {
 #pragma unroll
