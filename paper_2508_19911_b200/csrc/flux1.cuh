@@ -108,6 +108,8 @@ template <int DIM, int AX, bool COMPACT, bool BOX, bool LINES = false, bool STR 
 __global__ void
 #ifdef CGKS_FLUX_MAXNREG
 __maxnreg__(CGKS_FLUX_MAXNREG)
+#elif defined(CGKS_FLUX_MAXNREG_X)
+__maxnreg__(AX == 0 ? CGKS_FLUX_MAXNREG_X : CGKS_FLUX_MAXNREG_YZ)
 #else
 __launch_bounds__(FluxTile1<DIM, AX, COMPACT>::NTHR, FluxTile1<DIM, AX, COMPACT>::MINB)
 #endif
