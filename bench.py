@@ -53,6 +53,18 @@ def slab512(ws, rank):
     return c
 
 
+def pencil_block(nb, py, pz, rank):
+    """Rank ry + py rz's block of the global nb^3 TGV split into py x pz pencils (cgks_decompose_pencil's layout):
+    rows [ry nb/py, (ry+1) nb/py) of the planes [rz nb/pz, (rz+1) nb/pz); case.n stays the global grid."""
+    from cgks_inputs import tgv
+    ry, rz = rank % py, rank // py
+    case = tgv(nb, z0=rz * (nb // pz), nzb=nb // pz)  # the rank's z-slab, then its rows
+    ysl = slice(ry * (nb // py), (ry + 1) * (nb // py))
+    case.Q = np.ascontiguousarray(case.Q[:, :, ysl])
+    case.G = np.ascontiguousarray(case.G[:, :, :, ysl])
+    return case
+
+
 def make_case(name):
     """tgv<N> (TGV, BASELINE configs[1]), tgv_ss<N> (high-speed TGV with Sutherland viscosity, nonlinear,
     P:455-474, NEXT-2: the paper's meshes are 116^3 and 384^3), hit<N>, shock_vortex, vortex40."""
@@ -261,8 +273,20 @@ def run_ours(args, rank, ws, lr):
 
         from cgks_inputs import tgv
         from paper_2508_19911_b200 import nccl_unique_id
+        nproc = (1, 1, ws)
+        if args.pencil:
+            py, pz = (int(x) for x in args.pencil.lower().split("x"))
+            if py * pz != ws or not args.strong:
+                raise SystemExit("--pencil PyxPz needs Py * Pz = N ranks and --strong --workload tgv<n>")
+            nproc = (1, py, pz)
         if args.workload == "tgv512slab":
             case = slab512(ws, rank)
+        elif args.strong and args.pencil:  # strong scaling over Py x Pz pencils (rank = ry + Py rz)
+            nb = int(args.workload[3:])
+            py, pz = nproc[1], nproc[2]
+            if nb % py or nb % pz or nb // py < 4 or nb // pz < 4:
+                raise SystemExit(f"pencils need n divisible by Py and Pz with >= 4 rows / planes per rank ({nb}, {py}x{pz})")
+            case = pencil_block(nb, py, pz, rank)
         elif args.strong:  # strong scaling: the global n^3 TGV split into N z-slabs
             nb = int(args.workload[3:])
             if nb % ws or nb // ws < 4:
@@ -275,7 +299,7 @@ def run_ours(args, rank, ws, lr):
             case.nonlinear = args.nonlinear
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, nproc=(1, 1, ws), rank=rank,
+        S = Solver.from_case(case, scheme=scheme_id, stream=stream.cuda_stream, nproc=nproc, rank=rank,
                              nccl_id=obj[0])
         cr, cn, cb = S.comm_info()
         print(json.dumps({"bench_rank": rank, "world_size": ws, "comm_rank": cr, "comm_nranks": cn,
@@ -433,7 +457,8 @@ def run_ours(args, rank, ws, lr):
                        "scheme": args.scheme + ("-geno" if case.nonlinear else "-linear")
                        + ("-lines" if args.lines else "") + (f"-stretched{args.stretch:g}" if args.stretch else ""),
                        "time_scheme": "S2O4" if scheme_id == 1 else "S1O2", "global_cells": cells,
-                       "parallelism": f"zslab{ws} (NCCL halo + allreduce-min)" if ws > 1 else (
+                       "parallelism": (f"pencil{args.pencil} (NCCL y + z halos, allreduce-min)" if args.pencil else
+                                       f"zslab{ws} (NCCL halo + allreduce-min)") if ws > 1 else (
                            "zslab1 (NCCL self halo, overlapped)" if args.nccl_self else "1gpu"),
                        "l2": "state larger than L2 (no flush)",
                        "hbm_used_gb": round(hbm_used_gb, 1),
@@ -486,6 +511,8 @@ def main():
     ap.add_argument("--stretch", type=float, default=0.0,
                     help="sine-stretched tensor-product mesh with this amplitude (NEXT-4; timing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pencil", default=None,
+                    help="N > 1 with --strong: Py x Pz pencils (e.g. 2x4) instead of N z-slabs")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1: split the global tgv<n> grid over the ranks (strong scaling) instead of n^3 per GPU")
     ap.add_argument("--nccl-self", action="store_true",

@@ -59,7 +59,8 @@ typedef struct {
   double lo[3], hi[3];       /* box; uniform spacing h[a] = (hi[a]-lo[a])/n[a]                      */
   int bc[3][2];              /* CGKS_BC_* per axis (low, high side)                                */
   double bc_state[3][2][5];  /* conservative state for CGKS_BC_INFLOW sides                        */
-  int nproc[3];              /* ranks per axis; (1,1,P) = z-slabs.  {1,1,1} or zeros = one rank     */
+  int nproc[3];              /* ranks per axis (1,Py,Pz), rank = ry + Py rz: (1,1,P) = z-slabs, Py > 1 =
+                                pencils (3-D) or y-slabs (2-D; Pz = 1).  {1,1,1} or zeros = one rank  */
   int rank;                  /* this process' rank in [0, nproc product)                           */
   const void* nccl_id;       /* 128-byte ncclUniqueId, or NULL when there is one rank              */
   void* stream;              /* cudaStream_t to run on, or NULL for a library-owned stream         */
@@ -114,12 +115,27 @@ int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]);
  * CGKS_ERR_CONFIG for unsupported layouts (nproc[0|1] > 1, P not dividing n[2], bad rank). */
 int cgks_decompose(const int64_t n[3], const int nproc[3], int rank, int64_t off[3], int64_t nloc[3], int nbr[2]);
 
+/* Pure host function (no CUDA): the pencil / y-slab decomposition used by cgks_create (north_star: "slab/pencil
+ * decomposition"; pencils (1,Py,Pz), 2-D grids split along y).  nproc = (1,Py,Pz), rank =
+ * ry + Py rz owns rows [off[1], off[1] + n[1]/Py) and planes [off[2], off[2] + n[2]/Pz); nbr = (y lower, y upper,
+ * z lower, z upper) neighbour ranks (periodic).  CGKS_ERR_CONFIG for nproc[0] > 1, indivisible extents, bad rank. */
+int cgks_decompose_pencil(const int64_t n[3], const int nproc[3], int rank, int64_t off[3], int64_t nloc[3],
+                          int nbr[4]);
+
 /* Writes a fresh 128-byte ncclUniqueId into out128 (rank 0 creates it and broadcasts it to
  * the other ranks, e.g. with torch.distributed, before cgks_create).  Loads libnccl.so.2 at
  * run time (CGKS_NCCL_LIB overrides the name).  CGKS_ERR_COMM if NCCL is unavailable. */
 int cgks_nccl_unique_id(void* out128);
 
-/* Multi-rank contexts (grid.nproc = (1,1,P), P > 1):
+/* Pencils and y-slabs (grid.nproc = (1,Py,Pz), Py > 1; y periodic, >= 4 rows and planes per rank): the state
+ * also stores 2 ghost rows per side along y.  Every stage first exchanges the y halos of the rank's own planes
+ * (2-row strips of every field, packed into dense staging by pitched device copies, ncclSend/ncclRecv with the
+ * two y neighbours), then the z halos as for slabs -- whole planes including the fresh y ghost rows, so the
+ * edge-neighbour (corner) ghosts of the compact stencil arrive without a third exchange.  The in-process
+ * group copies the strips directly between the members' buffers.  A 2-D grid with grid.nccl_id and one rank
+ * runs the y path with the rank as its own neighbour (as the z path on a 3-D grid).
+ *
+ * Multi-rank contexts (grid.nproc = (1,1,P), P > 1):
  *   - with grid.nccl_id set, each process owns one rank; cgks_step exchanges a 2-plane halo
  *     of all fields (and line DOFs) with the z neighbours (ncclSend/ncclRecv, one group per
  *     stage, on a second stream overlapped with the interior reconstruction; CGKS_NO_OVERLAP=1

@@ -4,7 +4,7 @@ The compute path is libcgks.so (csrc/, C ABI in include/cgks.h); this package on
 builds it and marshals arguments.  See DESIGN.md.
 """
 from .binding import (CGKS_CGKS5, CGKS_GKS2, CGKS_TIME_DEFAULT, CGKS_TIME_S1O2, CGKS_TIME_S2O4, CgksError, Solver,
-                      decompose, load, nccl_unique_id, scheme_defaults, step_group)
+                      decompose, decompose_pencil, load, nccl_unique_id, scheme_defaults, step_group)
 
-__all__ = ["Solver", "CgksError", "load", "scheme_defaults", "decompose", "nccl_unique_id", "step_group", "CGKS_CGKS5", "CGKS_GKS2", "CGKS_TIME_DEFAULT",
+__all__ = ["Solver", "CgksError", "load", "scheme_defaults", "decompose", "decompose_pencil", "nccl_unique_id", "step_group", "CGKS_CGKS5", "CGKS_GKS2", "CGKS_TIME_DEFAULT",
            "CGKS_TIME_S1O2", "CGKS_TIME_S2O4"]

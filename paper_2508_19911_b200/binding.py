@@ -62,7 +62,7 @@ _lib = None
 
 EXPORTS = ["cgks_scheme_defaults", "cgks_create", "cgks_local_extent", "cgks_set_state", "cgks_step",
            "cgks_get_state", "cgks_get_time", "cgks_last_error", "cgks_launches_per_step", "cgks_profile",
-           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_nccl_unique_id", "cgks_step_group", "cgks_comm_info",
+           "cgks_algorithmic_flops", "cgks_fp64_peak", "cgks_decompose", "cgks_decompose_pencil", "cgks_nccl_unique_id", "cgks_step_group", "cgks_comm_info",
            "cgks_z_chunk",
            "cgks_set_state_async", "cgks_step_async", "cgks_get_state_async", "cgks_sync", "cgks_destroy"]
 
@@ -103,6 +103,8 @@ def load(path: str = LIB_PATH):
     i64p = ctypes.POINTER(ctypes.c_int64)
     L.cgks_decompose.argtypes = [i64p, ctypes.POINTER(ctypes.c_int), ctypes.c_int, i64p, i64p,
                                  ctypes.POINTER(ctypes.c_int)]
+    L.cgks_decompose_pencil.argtypes = [i64p, ctypes.POINTER(ctypes.c_int), ctypes.c_int, i64p, i64p,
+                                        ctypes.POINTER(ctypes.c_int)]
     L.cgks_nccl_unique_id.argtypes = [ctypes.c_void_p]
     L.cgks_step_group.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int]
     ip = ctypes.POINTER(ctypes.c_int)
@@ -135,6 +137,20 @@ def decompose(n, nproc, rank):
     if rc:
         raise CgksError(rc, "unsupported decomposition")
     return tuple(off), tuple(nl), (nb[0], nb[1])
+
+
+def decompose_pencil(n, nproc, rank):
+    """Host-only pencil / y-slab decomposition nproc = (1, Py, Pz), rank = ry + Py rz:
+    (offset, local size, (y lower, y upper, z lower, z upper) neighbours)."""
+    nn = (ctypes.c_int64 * 3)(*[int(x) for x in n])
+    npr = (ctypes.c_int * 3)(*[int(x) for x in nproc])
+    off = (ctypes.c_int64 * 3)()
+    nl = (ctypes.c_int64 * 3)()
+    nb = (ctypes.c_int * 4)()
+    rc = load().cgks_decompose_pencil(nn, npr, int(rank), off, nl, nb)
+    if rc:
+        raise CgksError(rc, "unsupported decomposition")
+    return tuple(off), tuple(nl), tuple(nb)
 
 
 def nccl_unique_id() -> bytes:

@@ -90,6 +90,11 @@ struct cgks_ctx {
   // z-slab decomposition (nproc = (1,1,P)): rank, size, z offset of this slab
   int rank = 0, nranks = 1;
   long long zoff_global = 0;
+  // pencils / y-slabs (nproc = (1,Py,Pz), rank = ry + Py rz): ranks along y and z, this rank's coordinates, its y
+  // offset, the dense staging of the 2-row y halos for NCCL (send low / high, receive low / high)
+  int py = 1, pz = 1, ry = 0, rz = 0;
+  long long yoff_global = 0;
+  double* ybuf = nullptr;
   nccl::Comm comm = nullptr;
   int comm_mode = 0;  // 0 single, 1 NCCL, 2 in-process group (cgks_step_group)
   cudaStream_t stream = nullptr;
@@ -318,7 +323,7 @@ static int run_stage_half(cgks_ctx* ctx, const double* Uin, double* Uout, int mo
 // The line DOFs (NEXT-1) have the same [z][field][y][x] layout with 5 * nl fields, so their halo is
 // one more contiguous block per side, exchanged with the state it is paired with.
 static long long plane_block(const cgks_ctx* c, bool lines = false) {
-  return (long long)(lines ? 5 * c->nl : c->NV) * c->geo.plane;
+  return (long long)(lines ? 5 * c->nl : c->NV) * c->geo.splane;
 }
 static double* low_send(const cgks_ctx* c, double* X, bool l = false) {
   return X + (long long)c->geo.zoff * plane_block(c, l);
@@ -342,11 +347,82 @@ static int nccl_check(cgks_ctx* ctx, int r, const char* what) {
   return CGKS_ERR_COMM;
 }
 
+// ---------------------------------------------------------------------------
+// y halo (pencils, y-slabs of 2-D grids): 2 ghost rows per side of every field of the rank's own z-planes.
+// A halo is n[2] * NF segments of 2 rows (2 n0 contiguous doubles) at stride splane: a pitched 2-D block,
+// moved by cudaMemcpy2DAsync (a memcpy node under graph capture) -- directly between the buffers of an
+// in-process group, through dense staging buffers for NCCL.  The y exchange covers the own z-planes only
+// and runs BEFORE the z exchange, whose whole-plane blocks then carry the edge (corner) ghosts along.
+// ---------------------------------------------------------------------------
+static long long yrows(const cgks_ctx* c, bool l) { return (long long)c->geo.n[2] * (l ? 5 * c->nl : c->NV); }
+static double* yrow_ptr(const cgks_ctx* c, double* X, bool l, int jrow) {  // storage row jrow of the first own plane
+  return X + (long long)c->geo.zoff * plane_block(c, l) + (long long)jrow * c->geo.n[0];
+}
+static double* ylow_send(const cgks_ctx* c, double* X, bool l) { return yrow_ptr(c, X, l, c->geo.yoff); }
+static double* yhigh_send(const cgks_ctx* c, double* X, bool l) {
+  return yrow_ptr(c, X, l, c->geo.yoff + c->geo.n[1] - 2);
+}
+static double* ylow_ghost(const cgks_ctx* c, double* X, bool l) { return yrow_ptr(c, X, l, 0); }
+static double* yhigh_ghost(const cgks_ctx* c, double* X, bool l) {
+  return yrow_ptr(c, X, l, c->geo.yoff + c->geo.n[1]);
+}
+// pitched copy of one y halo: dense (pitch 0) or in-buffer (pitch splane) on either side
+static cudaError_t ycopy(const cgks_ctx* c, double* dst, bool dst_dense, const double* src, bool src_dense, bool l,
+                         cudaStream_t st) {
+  const size_t w = sizeof(double) * 2 * (size_t)c->geo.n[0], pitch = sizeof(double) * (size_t)c->geo.splane;
+  return cudaMemcpy2DAsync(dst, dst_dense ? w : pitch, src, src_dense ? w : pitch, w, (size_t)yrows(c, l),
+                           cudaMemcpyDeviceToDevice, st);
+}
+
+// y halo exchange of buffer X (and its line DOFs) with the two y neighbours through NCCL: pack, one group
+// of sends / receives, unpack
+static int exchange_y_nccl(cgks_ctx* ctx, double* X, cudaStream_t st) {
+  const int Py = ctx->py, base = ctx->rz * Py;
+  const int lo = base + (ctx->ry + Py - 1) % Py, hi = base + (ctx->ry + 1) % Py;
+  auto& A = nccl::g_api;
+  double* Xl = lines_of(ctx, X);
+  // staging: [part][send low, send high, recv low, recv high], each 2 n0 yrows doubles
+  double* slot[2][4];
+  {
+    double* q = ctx->ybuf;
+    for (int part = 0; part < 2; ++part)
+      for (int b = 0; b < 4; ++b) {
+        slot[part][b] = q;
+        q += 2 * (long long)ctx->geo.n[0] * yrows(ctx, part == 1);
+      }
+  }
+  for (int part = 0; part < (Xl ? 2 : 1); ++part) {
+    const bool l = part == 1;
+    double* B = l ? Xl : X;
+    if (ycopy(ctx, slot[part][0], true, ylow_send(ctx, B, l), false, l, st) != cudaSuccess ||
+        ycopy(ctx, slot[part][1], true, yhigh_send(ctx, B, l), false, l, st) != cudaSuccess)
+      return CGKS_ERR_CUDA;
+  }
+  int e = A.GroupStart();
+  for (int part = 0; part < (Xl ? 2 : 1) && !e; ++part) {
+    const size_t cnt = (size_t)(2 * (long long)ctx->geo.n[0] * yrows(ctx, part == 1));
+    if (!e) e = A.Send(slot[part][0], cnt, nccl::Float64, lo, ctx->comm, st);
+    if (!e) e = A.Send(slot[part][1], cnt, nccl::Float64, hi, ctx->comm, st);
+    if (!e) e = A.Recv(slot[part][3], cnt, nccl::Float64, hi, ctx->comm, st);
+    if (!e) e = A.Recv(slot[part][2], cnt, nccl::Float64, lo, ctx->comm, st);
+  }
+  int e2 = A.GroupEnd();
+  if (int rc = nccl_check(ctx, e ? e : e2, "y halo exchange")) return rc;
+  for (int part = 0; part < (Xl ? 2 : 1); ++part) {
+    const bool l = part == 1;
+    double* B = l ? Xl : X;
+    if (ycopy(ctx, ylow_ghost(ctx, B, l), false, slot[part][2], true, l, st) != cudaSuccess ||
+        ycopy(ctx, yhigh_ghost(ctx, B, l), false, slot[part][3], true, l, st) != cudaSuccess)
+      return CGKS_ERR_CUDA;
+  }
+  return CGKS_OK;
+}
+
 // halo exchange of buffer X (and its line DOFs) with the two z neighbours through NCCL (one group
 // per stage)
 static int exchange_nccl(cgks_ctx* ctx, double* X, cudaStream_t st) {
-  const int P = ctx->nranks, r = ctx->rank;
-  const int lo = (r + P - 1) % P, hi = (r + 1) % P;
+  const int P = ctx->pz, Py = ctx->py;
+  const int lo = ctx->ry + Py * ((ctx->rz + P - 1) % P), hi = ctx->ry + Py * ((ctx->rz + 1) % P);
   auto& A = nccl::g_api;
   double* Xl = lines_of(ctx, X);
   int e = A.GroupStart();
@@ -398,6 +474,9 @@ static int run_chunk(cgks_ctx* ctx, const double* Uin, double* Uout, int mode, i
 // one stage of a rank: halo exchange of Uin, then the stage; NCCL ranks overlap the exchange (on
 // halo_stream) with the interior reconstruction
 static int halo_stage(cgks_ctx* ctx, double* Uin, double* Uout, int mode, int stage) {
+  if (ctx->geo.halo[1] && ctx->comm_mode == 1) {  // y halos first (the z blocks carry the edge ghosts along)
+    if (int rc = exchange_y_nccl(ctx, Uin, ctx->capturing ? ctx->cap_stream : ctx->stream)) return rc;
+  }
   if (ctx->chunk) {
     const int nch = (ctx->geo.n[2] + ctx->chunk - 1) / ctx->chunk;
     int rc = CGKS_OK;
@@ -544,35 +623,54 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
     set_msg(ctx, "unknown scheme id %d", scheme->id);
     return fail(CGKS_ERR_CONFIG);
   }
-  // z-slab decomposition: nproc = (1, 1, P)
+  // decomposition: nproc = (1, Py, Pz): z-slabs (Py = 1), pencils, y-slabs (Pz = 1; the only split of a 2-D
+  // grid); rank = ry + Py rz
   const int P = grid->nproc[2] > 0 ? grid->nproc[2] : 1;
-  if ((grid->nproc[0] > 1) || (grid->nproc[1] > 1)) {
-    set_msg(ctx, "only z-slab decompositions nproc = (1,1,P) are supported");
+  const int Py = grid->nproc[1] > 0 ? grid->nproc[1] : 1;
+  if (grid->nproc[0] > 1) {
+    set_msg(ctx, "decompositions split y and z only: nproc = (1,Py,Pz)");
     return fail(CGKS_ERR_CONFIG);
   }
-  // one rank with an NCCL id: the slab machinery with the rank as its own z neighbour (the exchange
-  // is the periodic wrap through NCCL); exercises the multi-rank path on one GPU
-  const bool slab = P > 1 || grid->nccl_id != nullptr;
+  // one rank with an NCCL id: the slab machinery with the rank as its own neighbour (the exchange
+  // is the periodic wrap through NCCL); exercises the multi-rank path on one GPU: along z on a 3-D grid,
+  // along y on a 2-D grid (or, test hook CGKS_TEST_SELF_Y=1, along y as well on a 3-D grid)
+  const bool self = grid->nccl_id != nullptr && P * Py == 1;
+  const bool slab = P > 1 || (self && grid->n[2] > 1);
+  const bool yslab = Py > 1 || (self && (grid->n[2] <= 1 || std::getenv("CGKS_TEST_SELF_Y") != nullptr));
+  if (yslab) {
+    const bool yper = grid->bc[1][0] == CGKS_BC_PERIODIC && grid->bc[1][1] == CGKS_BC_PERIODIC;
+    if (grid->n[1] <= 1 || !yper || grid->n[1] % Py != 0 || grid->n[1] / Py < 4 || grid->rank < 0 ||
+        grid->rank >= P * Py || (P > 1 && grid->n[2] <= 1)) {
+      set_msg(ctx, "y decomposition needs a 2-D or 3-D grid, periodic y, ny divisible by Py, >= 4 rows per rank "
+                   "and 0 <= rank < Py Pz (ny=%lld Py=%d Pz=%d rank=%d)",
+              (long long)grid->n[1], Py, P, grid->rank);
+      return fail(CGKS_ERR_CONFIG);
+    }
+  }
   if (slab) {
     const bool zper = grid->bc[2][0] == CGKS_BC_PERIODIC && grid->bc[2][1] == CGKS_BC_PERIODIC;
     if (grid->n[2] <= 1 || !zper || grid->n[2] % P != 0 || grid->n[2] / P < 4 || grid->rank < 0 ||
-        grid->rank >= P) {
+        grid->rank >= P * Py) {
       set_msg(ctx, "z-slab decomposition needs a 3-D grid, periodic z, nz divisible by P, >= 4 planes per "
                    "rank and 0 <= rank < P (nz=%lld P=%d rank=%d)",
               (long long)grid->n[2], P, grid->rank);
       return fail(CGKS_ERR_CONFIG);
     }
   }
-  ctx->nranks = P;
-  ctx->rank = P > 1 ? grid->rank : 0;
+  ctx->nranks = P * Py;
+  ctx->rank = P * Py > 1 ? grid->rank : 0;
+  ctx->py = Py;
+  ctx->pz = P;
+  ctx->ry = ctx->rank % Py;
+  ctx->rz = ctx->rank / Py;
   // ---- z-chunking: stages pass over z-chunks of `chunk` planes when the whole-slab reconstruction
   // coefficients and face records do not fit next to the state (or CGKS_CHUNK=C forces C planes)
   {
     const bool zper = grid->bc[2][0] == CGKS_BC_PERIODIC && grid->bc[2][1] == CGKS_BC_PERIODIC;
     const long long nzl = grid->n[2] / P;
-    const bool can = grid->n[2] > 1 && zper && nzl >= 4 && (P == 1 || grid->nccl_id != nullptr);
+    const bool can = grid->n[2] > 1 && zper && nzl >= 4 && (P * Py == 1 || grid->nccl_id != nullptr);
     if (can) {
-      const long long nx = grid->n[0], ny = grid->n[1];
+      const long long nx = grid->n[0], ny = grid->n[1] / Py;
       const int NVc = scheme->id == CGKS_CGKS5 ? 20 : 5;
       const int nrec = scheme->id == CGKS_CGKS5 ? 170 : 15;
       const int ngl = 4;
@@ -635,7 +733,13 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       g.n[2] = (int)(grid->n[2] / P);        // (or, chunked periodic z, by a local copy)
       g.halo[2] = 1;
       g.zoff = 2;
-      ctx->zoff_global = (long long)ctx->rank * g.n[2];
+      ctx->zoff_global = (long long)ctx->rz * g.n[2];
+    }
+    if (a == 1 && yslab) {  // this rank's rows; 2 ghost rows per side filled by the y halo exchange
+      g.n[1] = (int)(grid->n[1] / Py);
+      g.halo[1] = 1;
+      g.yoff = 2;
+      ctx->yoff_global = (long long)ctx->ry * g.n[1];
     }
     bool per = grid->bc[a][0] == CGKS_BC_PERIODIC && grid->bc[a][1] == CGKS_BC_PERIODIC;
     if (!per && (grid->bc[a][0] == CGKS_BC_PERIODIC || grid->bc[a][1] == CGKS_BC_PERIODIC)) {
@@ -654,6 +758,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) g.fn[a][b] = g.n[b] + ((a == b && g.bounded[a]) ? 1 : 0);
   g.plane = (long long)g.n[0] * g.n[1];
+  g.splane = (long long)g.n[0] * (g.n[1] + 2 * g.yoff);
   g.eplane = (long long)g.en[0] * g.en[1];
   g.cfl = scheme->cfl;
   g.fixed_dt = scheme->fixed_dt;
@@ -750,7 +855,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   int NV = ctx->NV;
   int nrec = ctx->scheme_id == CGKS_CGKS5 ? ctx->cls.nb * 5 : 15;
   int nff = g.nfr;
-  const long long nstore = (long long)g.plane * (g.n[2] + 2 * g.zoff) * NV;  // incl. z ghost planes
+  const long long nstore = (long long)g.splane * (g.n[2] + 2 * g.zoff) * NV;  // incl. y / z ghost rows / planes
   if ((double)nstore >= 4294967296.0) {  // the reconstruction's staging map holds 32-bit element offsets
     set_msg(ctx, "state of %lld doubles per buffer exceeds the 2^32-element limit: decompose the grid", nstore);
     return fail(CGKS_ERR_CONFIG);
@@ -763,7 +868,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
             alloc(&ctx->staging, ctx->ncell * (ctx->chunk ? 1 : (g.lines ? 60 : 15)));
   if (ok && g.lines) {
     ctx->nl = dim * g.ngl;
-    const long long nls = (long long)g.plane * (g.n[2] + 2 * g.zoff) * 5 * ctx->nl;
+    const long long nls = (long long)g.splane * (g.n[2] + 2 * g.zoff) * 5 * ctx->nl;
     ok = alloc(&ctx->Lb[0], nls) && alloc(&ctx->Lb[1], nls) && alloc(&ctx->Ls, nls) && alloc(&ctx->Lc, nls);
   }
   for (int a = 0; a < dim && ok; ++a)
@@ -807,9 +912,9 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
         }
         double* bufs[3] = {ctx->U[0], ctx->U[1], ctx->Us};
         for (int b = 0; b < 3 && good; ++b) {
-          const cuuint64_t dims[4] = {(cuuint64_t)g.n[0], (cuuint64_t)g.n[1], (cuuint64_t)NV,
+          const cuuint64_t dims[4] = {(cuuint64_t)g.n[0], (cuuint64_t)(g.n[1] + 2 * g.yoff), (cuuint64_t)NV,
                                       (cuuint64_t)(g.n[2] + 2 * g.zoff)};
-          const cuuint64_t str[3] = {(cuuint64_t)g.n[0] * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.plane * NV * 8};
+          const cuuint64_t str[3] = {(cuuint64_t)g.n[0] * 8, (cuuint64_t)g.splane * 8, (cuuint64_t)g.splane * NV * 8};
           const cuuint32_t box[4] = {(cuuint32_t)tx, by, 5, bz};
           good = encode(&ctx->tm_U[b][a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, bufs[b], dims, str, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -906,7 +1011,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
               return fail(CGKS_ERR_CONFIG);
             }
         const bool per = grid->bc[a][0] == CGKS_BC_PERIODIC && grid->bc[a][1] == CGKS_BC_PERIODIC;
-        const long long off = a == 2 ? ctx->zoff_global : 0;
+        const long long off = a == 2 ? ctx->zoff_global : (a == 1 ? ctx->yoff_global : 0);
         std::vector<double> w((size_t)g.n[a] + 4), iw((size_t)g.n[a] + 4);
         for (int c = -2; c < g.n[a] + 2; ++c) {
           long long gi = c + off;
@@ -929,7 +1034,7 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
   cudaMemset(ctx->U[0], 0, sizeof(double) * nstore);
   // multi-rank: NCCL communicator when an id is given; otherwise the context joins an in-process
   // group stepped by cgks_step_group (halo copies on one device)
-  if (slab) {
+  if (slab || yslab) {
     if (grid->nccl_id) {
       if (!nccl::load()) {
         set_msg(ctx, "cannot load libnccl.so.2 (set CGKS_NCCL_LIB)");
@@ -937,12 +1042,19 @@ int cgks_create(const cgks_grid* grid, double gamma, double mu, double Pr, const
       }
       nccl::UniqueId id;
       std::memcpy(id.internal, grid->nccl_id, sizeof(id.internal));
-      int e = nccl::g_api.CommInitRank(&ctx->comm, P, id, ctx->rank);
+      int e = nccl::g_api.CommInitRank(&ctx->comm, P * Py, id, ctx->rank);
       if (e) {
         set_msg(ctx, "ncclCommInitRank failed (%d)", e);
         return fail(CGKS_ERR_COMM);
       }
       ctx->comm_mode = 1;
+      if (g.halo[1]) {  // dense staging of the y halos: [state, lines] x [send low, send high, recv low, recv high]
+        const long long ny = 8LL * g.n[0] * g.n[2] * (ctx->NV + 5 * ctx->nl);
+        if (!alloc(&ctx->ybuf, ny)) {
+          set_msg(ctx, "out of device memory for the y-halo staging (%lld doubles)", ny);
+          return fail(CGKS_ERR_CUDA);
+        }
+      }
       ctx->overlap = std::getenv("CGKS_NO_OVERLAP") == nullptr;
       if (const char* tp = std::getenv("CGKS_TEST_PEER_FAIL_STEP")) ctx->test_peer_fail = std::atoll(tp);
       if (cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -978,6 +1090,7 @@ int cgks_local_extent(const cgks_ctx* ctx, int64_t off[3], int64_t n[3]) {
     off[a] = 0;
     n[a] = ctx->geo.n[a];
   }
+  off[1] = ctx->yoff_global;
   off[2] = ctx->zoff_global;
   return CGKS_OK;
 }
@@ -993,6 +1106,26 @@ int cgks_decompose(const int64_t n[3], const int nproc[3], int rank, int64_t off
   off[2] = (int64_t)rank * nloc[2];
   nbr[0] = (rank + P - 1) % P;
   nbr[1] = (rank + 1) % P;
+  return CGKS_OK;
+}
+
+int cgks_decompose_pencil(const int64_t n[3], const int nproc[3], int rank, int64_t off[3], int64_t nloc[3],
+                          int nbr[4]) {
+  const int Py = nproc[1] > 0 ? nproc[1] : 1, Pz = nproc[2] > 0 ? nproc[2] : 1;
+  if (nproc[0] > 1 || rank < 0 || rank >= Py * Pz || n[1] % Py != 0 || n[2] % Pz != 0) return CGKS_ERR_CONFIG;
+  const int ry = rank % Py, rz = rank / Py;
+  for (int a = 0; a < 3; ++a) {
+    off[a] = 0;
+    nloc[a] = n[a];
+  }
+  nloc[1] = n[1] / Py;
+  nloc[2] = n[2] / Pz;
+  off[1] = (int64_t)ry * nloc[1];
+  off[2] = (int64_t)rz * nloc[2];
+  nbr[0] = rz * Py + (ry + Py - 1) % Py;
+  nbr[1] = rz * Py + (ry + 1) % Py;
+  nbr[2] = ry + Py * ((rz + Pz - 1) % Pz);
+  nbr[3] = ry + Py * ((rz + 1) % Pz);
   return CGKS_OK;
 }
 
@@ -1067,15 +1200,40 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
   CK(cudaMemcpyAsync(&t, c0->ts, sizeof(t), cudaMemcpyDeviceToHost, c0->stream));
   CK(cudaStreamSynchronize(c0->stream));
   const int cur0 = c0->cur;
+  const int Py = c0->py, Pz = c0->pz;  // rank r = ry + Py rz
+  const bool zh = c0->geo.halo[2] != 0, yh = c0->geo.halo[1] != 0;
+  // y halos (pencils, y-slabs): pitched copies between the members' buffers, own z-planes only; before the z
+  // exchange, whose whole-plane blocks carry the edge ghosts along
+  auto ychg = [&](int which) -> int {
+    if (n == 1 || !yh) return CGKS_OK;
+    for (int part = 0; part < (c0->lines ? 2 : 1); ++part) {
+      const bool l = part == 1;
+      for (int r = 0; r < n; ++r) {
+        cgks_ctx* me = ctxs[r];
+        const int ry = r % Py, rz = r / Py;
+        cgks_ctx* lo = ctxs[rz * Py + (ry + Py - 1) % Py];
+        cgks_ctx* hi = ctxs[rz * Py + (ry + 1) % Py];
+        auto buf = [&](cgks_ctx* c) -> double* {
+          double* X = which ? c->Us : c->U[c->cur];
+          return l ? lines_of(c, X) : X;
+        };
+        if (ycopy(me, ylow_ghost(me, buf(me), l), false, yhigh_send(lo, buf(lo), l), false, l, c0->stream) ||
+            ycopy(me, yhigh_ghost(me, buf(me), l), false, ylow_send(hi, buf(hi), l), false, l, c0->stream))
+          return CGKS_ERR_CUDA;
+      }
+    }
+    return CGKS_OK;
+  };
   auto xchg = [&](int which) -> int {  // which: 0 = U[cur], 1 = Us
-    if (n == 1) return CGKS_OK;
+    if (n == 1 || !zh) return CGKS_OK;
     for (int part = 0; part < (c0->lines ? 2 : 1); ++part) {
       const bool l = part == 1;
       const size_t bytes = sizeof(double) * (size_t)(2 * plane_block(c0, l));
       for (int r = 0; r < n; ++r) {
         cgks_ctx* me = ctxs[r];
-        cgks_ctx* lo = ctxs[(r + n - 1) % n];
-        cgks_ctx* hi = ctxs[(r + 1) % n];
+        const int ry = r % Py, rz = r / Py;
+        cgks_ctx* lo = ctxs[ry + Py * ((rz + Pz - 1) % Pz)];
+        cgks_ctx* hi = ctxs[ry + Py * ((rz + 1) % Pz)];
         auto buf = [&](cgks_ctx* c) -> double* {
           double* X = which ? c->Us : c->U[c->cur];
           return l ? lines_of(c, X) : X;
@@ -1102,13 +1260,15 @@ int cgks_step_group(cgks_ctx** ctxs, int n, int nsteps) {
     // exchange, the rest), so the split stage is covered on one device
     auto stage_all = [&](int which, int mode, int stg) -> int {
       int r2 = CGKS_OK;
+      r2 = ychg(which);
       for (int half = 0; half < 2 && !r2; ++half) {
         if (half == 1 && n > 1) r2 = xchg(which);
         for (int r = 0; r < n && !r2; ++r) {
           cgks_ctx* c = ctxs[r];
           double* in = which ? c->Us : c->U[c->cur];
           double* out = (mode == 0) ? c->Us : c->U[1 - c->cur];
-          r2 = n > 1 ? run_stage_half(c, in, out, mode, stg, half) : (half ? CGKS_OK : run_stage(c, in, out, mode, stg));
+          r2 = (n > 1 && zh) ? run_stage_half(c, in, out, mode, stg, half)
+                             : (half ? CGKS_OK : run_stage(c, in, out, mode, stg));
         }
       }
       return r2;
@@ -1558,7 +1718,7 @@ int cgks_diagnostics(cgks_ctx* ctx, double out[4]) {
   DevGuard dg_(ctx);
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
-  if (ctx->geo.halo[2]) {
+  if (ctx->geo.halo[2] || ctx->geo.halo[1]) {
     set_msg(ctx, "cgks_diagnostics: decomposed or z-chunked contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
@@ -1600,7 +1760,7 @@ int cgks_qcriterion(cgks_ctx* ctx, double* out) {
   DevGuard dg_(ctx);
   if (!ctx || !out) return CGKS_ERR_CONFIG;
   if (int r = drain_async(ctx)) return r;
-  if (ctx->geo.halo[2]) {
+  if (ctx->geo.halo[2] || ctx->geo.halo[1]) {
     set_msg(ctx, "cgks_qcriterion: decomposed or z-chunked contexts are not supported (gather the state first)");
     return CGKS_ERR_CONFIG;
   }
@@ -1868,7 +2028,7 @@ void cgks_destroy(cgks_ctx* ctx) {
   double* bufs[] = {ctx->U[0], ctx->U[1], ctx->Us,      ctx->carry,   ctx->rec,     ctx->staging, ctx->face[0],
                     ctx->face[1], ctx->face[2], ctx->gtab[0], ctx->gtab[1], ctx->gtab[2], ctx->dtab,  ctx->dpart,
                     ctx->ctab, ctx->Lb[0], ctx->Lb[1], ctx->Ls, ctx->Lc,
-                    ctx->hwd[0], ctx->hwd[1], ctx->hwd[2], ctx->ihwd[0], ctx->ihwd[1], ctx->ihwd[2]};
+                    ctx->hwd[0], ctx->hwd[1], ctx->hwd[2], ctx->ihwd[0], ctx->ihwd[1], ctx->ihwd[2], ctx->ybuf};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (ctx->ts) cudaFree(ctx->ts);

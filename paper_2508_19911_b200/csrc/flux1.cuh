@@ -152,7 +152,7 @@ k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
       for (int p = 0; p < FT::NSPL; ++p)
         tma_load_4d(tile + p * FT::PSTR, &tm_rec, bar + p, COMPACT ? 2 * (x0 - c_geo.elo[0]) : x0 - c_geo.elo[0],
                     COMPACT ? 0 : p * FT::NRH, y0 - c_geo.elo[1], z0 - c_geo.elo[2] - kofs);
-      tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0, 0, z0 + c_geo.zoff);
+      tma_load_4d(tile + FT::STILE, &tm_U, bar, x0, y0 + c_geo.yoff, 0, z0 + c_geo.zoff);
       if (COMPACT) bulk_load(tab, gtab, (unsigned)(sizeof(double) * FT::TAB), bar);
     }
   } else {
@@ -203,7 +203,7 @@ k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
         for (int v = fsub; v < 5; v += TPC) sdst[v * FT::FSU] = ld_state<BOX>(U, NV, v, ci, cj, ck);
       } else {
         const double* ub = U + sidx(NV, 0, wrap_ax(0, ci), wrap_ax(1, cj), wrap_ax(2, ck));
-        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FSU, ub + v * c_geo.plane);
+        for (int v = fsub; v < 5; v += TPC) cp_async8(sdst + v * FT::FSU, ub + v * c_geo.splane);
       }
     }
   }

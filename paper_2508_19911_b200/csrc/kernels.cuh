@@ -74,11 +74,16 @@ __host__ __device__ constexpr int nbr_off(int n, int ax) {
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
 __device__ __forceinline__ long long sidx(int NV, int f, int i, int j, int k) {
-  return ((long long)(k + c_geo.zoff) * NV + f) * c_geo.plane + (long long)j * c_geo.n[0] + i;
+  return ((long long)(k + c_geo.zoff) * NV + f) * c_geo.splane + (long long)(j + c_geo.yoff) * c_geo.n[0] + i;
 }
 
 // periodic wrap, except on decomposed axes whose ghost cells are stored
 __device__ __forceinline__ int wrap_ax(int a, int i) { return c_geo.halo[a] ? i : wrapi(i, c_geo.n[a]); }
+// the same with the passed index clamped to the 2 stored ghost layers: the ragged tail of a reconstruction tile
+// reaches further (its values feed no cell, but the read must stay inside the buffer)
+__device__ __forceinline__ int wrap_ax_c(int a, int i) {
+  return c_geo.halo[a] ? min(max(i, -2), c_geo.n[a] + 1) : wrapi(i, c_geo.n[a]);
+}
 
 // value of field f (0-4 Q, 5-19 gradient [axis][var]) of cell (i,j,k), any integer index
 template <bool BOX>
@@ -94,7 +99,10 @@ __device__ __forceinline__ double ld_state(const double* __restrict__ U, int NV,
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (c_geo.halo[a]) continue;
+      if (c_geo.halo[a]) {  // stored ghosts (the ragged tail of a reconstruction tile stays inside the buffer)
+        idx[a] = min(max(idx[a], -2), c_geo.n[a] + 1);
+        continue;
+      }
       if (c_geo.bounded[a]) {
         idx[a] = idx[a] < 0 ? 0 : (idx[a] >= c_geo.n[a] ? c_geo.n[a] - 1 : idx[a]);
       } else {
@@ -324,7 +332,7 @@ struct ReconStageMap {
     for (int h = threadIdx.x; h < RT::HALO; h += RT::NTH) {
       const int hx = h % RT::HX, hy = (h / RT::HX) % RT::HY, hz = h / (RT::HX * RT::HY);
       const int i = x0 - 1 + hx, j = DIM >= 2 ? y0 - 1 + hy : 0, kk = DIM == 3 ? z0 - 1 + hz : 0;
-      off[h] = (unsigned)sidx(20, 0, wrap_ax(0, i), wrap_ax(1, j), wrap_ax(2, kk));
+      off[h] = (unsigned)sidx(20, 0, wrap_ax_c(0, i), wrap_ax_c(1, j), wrap_ax_c(2, kk));
     }
   }
 };
@@ -343,14 +351,14 @@ __device__ __forceinline__ void recon_stage(const double* __restrict__ U, double
       buf[idx] = ld_state<true>(U, 20, fld, i, j, kk);
     }
   } else {
-    const double* Uv = U + (long long)v * c_geo.plane;
+    const double* Uv = U + (long long)v * c_geo.splane;
 #pragma unroll 1
     for (int h = threadIdx.x; h < RT::HALO; h += RT::NTH) {
       {
         const double* src = Uv + map.off[h];
 #pragma unroll
         for (int f = 0; f < RT::NFS; ++f)
-          cp_async8(buf + f * RT::HALO + h, src + (f == 0 ? 0 : 5 + (f - 1) * 5) * c_geo.plane);
+          cp_async8(buf + f * RT::HALO + h, src + (f == 0 ? 0 : 5 + (f - 1) * 5) * c_geo.splane);
       }
     }
   }
@@ -435,7 +443,7 @@ __global__ void __launch_bounds__(ReconTile<DIM>::NTH, CGKS_RECON_MINB) k_recon5
         for (int a = 0; a < 3; ++a) li[a] = wrap_ax(a, li[a]);
       }
       L.lv = Lin + (valid ? sidx(NLF, v, li[0], li[1], li[2]) : 0);
-      L.lstride = 5 * c_geo.plane;
+      L.lstride = 5 * c_geo.splane;
     }
     double acc[S::NB];
 #pragma unroll
@@ -882,8 +890,8 @@ static __global__ void k_pack(const double* __restrict__ src, double* __restrict
   const int f = (int)(t / nc);
   const long long c = t % nc;
   const int k = (int)(c / c_geo.plane);
-  const long long r = c % c_geo.plane;
-  dst[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.plane + r] = src ? src[t] : 0.0;
+  const long long r = c % c_geo.plane + (long long)c_geo.yoff * c_geo.n[0];  // rows are contiguous behind the y ghosts
+  dst[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.splane + r] = src ? src[t] : 0.0;
 }
 
 static __global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int NV, int f0, int nf) {
@@ -893,8 +901,8 @@ static __global__ void k_unpack(const double* __restrict__ src, double* __restri
   const int f = (int)(t / nc);
   const long long c = t % nc;
   const int k = (int)(c / c_geo.plane);
-  const long long r = c % c_geo.plane;
-  dst[t] = src[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.plane + r];
+  const long long r = c % c_geo.plane + (long long)c_geo.yoff * c_geo.n[0];
+  dst[t] = src[((long long)(k + c_geo.zoff) * NV + f0 + f) * c_geo.splane + r];
 }
 
 // ---------------------------------------------------------------------------

@@ -97,7 +97,6 @@ int flux_launch(LaunchEnv& env, const char* name, const StageArgs& a, int stage)
   const size_t smem = FT::smem_bytes();
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 5;
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     attr = true;
   }
   // face planes [kb, ke) along z: all of them, or those of the z-chunk a.ck0 .. a.ck0 + a.cn (chunked

@@ -15,10 +15,12 @@ struct Geo {
   int bounded[3];    // axis has non-periodic boundaries, or is a decomposed axis (ghost storage)
   int halo[3];       // axis is decomposed: ghost cells are stored (filled by the halo exchange)
   int zoff;          // storage offset of z-plane 0 (2 ghost planes when z is decomposed)
+  int yoff;          // storage offset of y-row 0 (2 ghost rows when y is decomposed: pencils, 2-D y-slabs)
   int elo[3];        // extended (reconstruction) range start: -1 on bounded axes
   int en[3];         // extended counts
   int fn[3][3];      // face-grid dims for faces normal to axis a: fn[a][b]
-  long long plane;   // n0*n1
+  long long plane;   // n0*n1 (cells of a z-plane)
+  long long splane;  // n0*(n1 + 2 yoff): storage stride of one field of a z-plane
   long long eplane;  // en0*en1
   double h[3], ih[3];
   int bc[3][2];

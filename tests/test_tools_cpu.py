@@ -69,6 +69,24 @@ def test_slab_inputs_tile_the_global_grid():
     assert b1.n == (512, 512, 64) and b1.hi[2] - b1.lo[2] == pytest.approx(2 * np.pi / 8)
 
 
+def test_pencil_inputs_tile_the_global_grid():
+    # bench.py --strong --pencil PyxPz: the per-rank blocks (rank = ry + Py rz) tile tgv(n)
+    from cgks_inputs import tgv
+    from paper_2508_19911_b200.binding import decompose_pencil
+    sys.path.insert(0, ROOT)
+    import bench
+    full = tgv(16)
+    Q = np.zeros_like(full.Q)
+    G = np.zeros_like(full.G)
+    for r in range(8):
+        b = bench.pencil_block(16, 2, 4, r)
+        off, nl, _ = decompose_pencil((16, 16, 16), (1, 2, 4), r)
+        assert b.n == (16, 16, 16) and b.Q.shape == (5, nl[2], nl[1], nl[0])
+        Q[:, off[2]:off[2] + nl[2], off[1]:off[1] + nl[1]] = b.Q
+        G[:, :, off[2]:off[2] + nl[2], off[1]:off[1] + nl[1]] = b.G
+    assert np.array_equal(Q, full.Q) and np.array_equal(G, full.G)
+
+
 def test_bench_reference_arm_line():
     # the reference arm (CPU oracle on a bounded sample) prints one JSON line with our arm's config
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
