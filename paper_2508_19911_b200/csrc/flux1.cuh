@@ -22,9 +22,16 @@ namespace cgks {
 #ifndef CGKS_EVAL_SQ
 #define CGKS_EVAL_SQ 1
 #endif
+#ifndef CGKS_EVAL_REMAP
+#define CGKS_EVAL_REMAP 1
+#endif
 #ifndef CGKS_FY1
-#define CGKS_FY1 2  // faces of a y- / z-face patch along the normal axis (x extent = faces per block / FY1):
-                        // 16 x 2 patches (128-byte TMA rows), measured 1.611 / 1.609 ms vs 8 x 4: 1.622 / 1.617, 4 x 8: 1.66
+#define CGKS_FY1 4  // faces of a y- / z-face patch along the normal axis (x extent = faces per block / FY1).
+                    // 64-thread blocks: 4 x 4 patches (tile of 4 x 5 cells, 64-byte TMA rows; the two sides of a face
+                    // sit 64 bytes apart modulo 128, so the evaluation's 16-byte loads are conflict-free, and the
+                    // block's 31 KB leave the SM 60 KB of L1): y / z 1.380 / 1.385 ms, stage 2 1.363 / 1.360, against
+                    // 8 x 2 patches (8 x 3 cells, 128-byte rows, 2-way conflicts between the sides): 1.431 / 1.424,
+                    // 1.379 / 1.396.  (128-thread blocks, round 2 earlier: 16 x 2 1.611, 8 x 4 1.622, 4 x 8 1.66)
 #endif
 
 template <int DIM, int AX, bool COMPACT>
@@ -282,8 +289,20 @@ k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
     // quantities qa = gp >> 1 (value or d/dn) and qa + 2 (d/dtA or d/dtB) at all 4 Gauss points, so every
     // coefficient it loads feeds two FMAs (170 shared-memory loads per lane instead of 340 for both sides);
     // the results wait in registers for the block barrier (tile dead), then go to their lanes' columns.
-    const int sd = gp & 1, qa = gp >> 1;
-    const int cs = sd ? cR : cL;
+    // x-faces: the lane works for its own face (sides cL, cL + 1 are adjacent 16-byte pairs).  y- / z-faces: the
+    // two sides are tile rows a multiple of 128 bytes apart, so lanes of one quarter-warp reading both sides of a
+    // face hit the same banks (ncu: 49 M LDS bank conflicts per launch against 3 M for x-faces); there lane Lw of
+    // a warp (one row of 8 faces) takes face Lw & 7, side (Lw >> 3) & 1, quantity pair Lw >> 4: every quarter-warp
+    // reads 8 consecutive pairs of one tile row (conflict-free) and shares its table entries.  Results bitwise
+    // equal.  Measured per launch with 8 x 2 patches (y / z, ms): stage-2 kernels 1.403 / 1.412 -> 1.378 / 1.396,
+    // full-record kernels 1.431 / 1.424 -> 1.450 / 1.446 (ptxas then spills 48 instead of 32 bytes), so only the
+    // former used it; the default 4 x 4 patches are conflict-free as they are (FX = 4: not remapped)
+    constexpr bool REMAP = AX != 0 && FX == 8 && (CGKS_EVAL_REMAP == 2 || (CGKS_EVAL_REMAP == 1 && TONLY));
+    const int lw = lane & 31;
+    const int sd = REMAP ? (lw >> 3) & 1 : gp & 1, qa = REMAP ? lw >> 4 : gp >> 1;
+    const int ef = REMAP ? (lane >> 5) * 8 + (lw & 7) : fl;  // the face (of the block) this lane evaluates
+    const int ecol = ef * NG;                                // its lanes' columns
+    const int cs = REMAP ? ((ef / FX) + sd) * FX + ef % FX : (sd ? cR : cL);
     const double* tc = tile + FT::pbase(cs);
     const double* sc = tile + FT::STILE + FT::cbaseU(cs);
     const double* Ta = tab + (sd * NQ + qa) * FT::TS;
@@ -338,8 +357,8 @@ k_flux1(const double* __restrict__ U, const double* __restrict__ rec,
       for (int v = 0; v < 5; ++v)
 #pragma unroll
         for (int g2 = 0; g2 < 4; ++g2) {
-          CGKS_BOUND(((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2), FT::TILE, "flux eval scatter");
-          tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (lane - gp + g2)] = R[w][v][g2];
+          CGKS_BOUND(((sd * NQ + qa + 2 * w) * 5 + v) * RS + (ecol + g2), FT::TILE, "flux eval scatter");
+          tile[((sd * NQ + qa + 2 * w) * 5 + v) * RS + (ecol + g2)] = R[w][v][g2];
         }
     CGKS_JIT(4);
     __syncwarp();
