@@ -131,7 +131,7 @@ def test_positivity_error_keeps_last_state():
     S.close()
 
 
-def _sampled_one_step(case, scheme, samples, seed=0, nonlinear=None):
+def _sampled_one_step(case, scheme, samples, seed=0, nonlinear=None, **solver_kw):
     """Full-size parity in the bench launch configuration: one GPU step on the whole grid; the oracle
     steps a 9^dim periodic box around each sampled cell (the one-step dependency radius is 4 cells,
     2 per stage) with the global dt computed by the oracle from the full field."""
@@ -141,7 +141,7 @@ def _sampled_one_step(case, scheme, samples, seed=0, nonlinear=None):
     prob = oracle.Problem(**d, scheme=scheme, time_scheme=2 if scheme == 1 else 1)
     dt = oracle.dt(prob, case.Q)
     Solver = _gpu()
-    S = Solver.from_case(case, scheme=scheme, nonlinear=d["nonlinear"])
+    S = Solver.from_case(case, scheme=scheme, nonlinear=d["nonlinear"], **solver_kw)
     S.set_state(case.Q, case.G)
     S.step(1)
     Qg, Gg = S.get_state()
@@ -192,6 +192,19 @@ def test_full_size_tgv128_cgks5_sampled():
 
 def test_full_size_tgv128_gks2_sampled():
     e = _sampled_one_step(tgv(128), 0, samples=12)
+    assert e <= 1e-10, e
+
+
+@pytest.mark.slow
+def test_full_size_slab512_nccl_self_sampled():
+    # the per-GPU block of bench.py --gpus N (BASELINE configs[4]: 512 x 512 x 64 planes of the 512^3 TGV) in the
+    # launch configuration the bench times on one GPU: the NCCL slab path with the periodic self halo, one step on
+    # the whole block, sampled cells against the oracle
+    import torch  # noqa: F401  (loads the libnccl.so.2 the library binds at run time)
+    import bench
+    from paper_2508_19911_b200 import nccl_unique_id
+    case = bench.slab512(1, 0)
+    e = _sampled_one_step(case, 1, samples=6, nccl_id=nccl_unique_id())
     assert e <= 1e-10, e
 
 

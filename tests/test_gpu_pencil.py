@@ -178,3 +178,15 @@ def test_nccl_self_y_chunked_bitwise():
     Q1, G1, t1, _ = _single(case, 1, 0, 4, **kw)
     Qn, Gn, tn, _ = _nccl_self(case, 1, 0, 4, {"CGKS_TEST_SELF_Y": "1", "CGKS_CHUNK": "5"}, **kw)
     assert t1 == tn and np.array_equal(Q1, Qn) and np.array_equal(G1, Gn)
+
+
+def test_nccl_self_y_stretched_bitwise():
+    # stretched tensor-product mesh (NEXT-4) through the y + z self halos: the ghost rows / planes take the
+    # periodic images' widths, as the plain context's wrap does
+    from cgks_inputs import stretched_nodes
+    case = random_smooth((16, 12, 16), seed=3)
+    nodes = tuple(stretched_nodes(case.n[a], case.lo[a], case.hi[a], 0.2) for a in range(3))
+    kw = dict(mu=1e-3, Pr=0.72, nodes=nodes)
+    Q1, G1, t1, _ = _single(case, 1, 0, 4, **kw)
+    Qn, Gn, tn, _ = _nccl_self(case, 1, 0, 4, {"CGKS_TEST_SELF_Y": "1"}, **kw)
+    assert t1 == tn and np.array_equal(Q1, Qn) and np.array_equal(G1, Gn)
