@@ -591,8 +591,9 @@ __global__ void __launch_bounds__(256) k_recon2(const double* __restrict__ U, do
 // Face record (per face, normal axis AX): Fn[5] Ft[5] (+ QLn QLt QRn QRt for CGKS-5th).
 // The face between cells (idx - e_AX) and idx carries the index idx (0..n, n+1 faces if bounded).
 // ---------------------------------------------------------------------------
-// threads per flux block (= Gauss points per block) per normal axis: 64 (16 faces: an x-run of 16, or an
-// 8 x 2 y-/z-face patch), 6 blocks = 12 warps per SM (168 registers).  Measured per launch (ms, x / y / z):
+// threads per flux block (= Gauss points per block) per normal axis: 64 (16 faces: an x-run of 16, or a
+// 4 x 4 y-/z-face patch, CGKS_FY1 in flux1.cuh), 6 blocks = 12 warps per SM (168 registers).  Measured per
+// launch before the 4 x 4 patches (ms, x / y / z):
 // x-faces 64 threads 1.535 vs 128: 1.71, 32: 1.92; y/z-faces 64 threads (8 x 2) 1.539 / 1.530 vs 128 (16 x 2)
 // 1.542 / 1.545, 128 (8 x 4) 1.62 / 1.62 (round-2 kernel); 16 warps per SM (128 registers) spill and lose
 // ~35 %
