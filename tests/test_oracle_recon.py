@@ -170,6 +170,34 @@ def test_venkat_extremum_and_constant():
     assert phi[0] >= 0.0
 
 
+def test_venkat_closed_form_value():
+    """Venkatakrishnan's limiter function (R11) on data that fix every term: along x the averages are
+    0.5, 1, 3 (h = 1), so the LS slope is 1.25 per cell; at the + face D2 = 0.625, D1 = qmax - q0 = 2 gives
+    phi > 1 (clipped), at the - face D2 = -0.625, D1 = qmin - q0 = -0.5 gives
+    phi = (D1^2 + e2 + 2 D1 D2) / (D1^2 + 2 D2^2 + D1 D2 + e2), e2 = (K h)^3 = 0.027 (K = 0.3): the textbook form
+    (Venkatakrishnan 1995).  The cell takes the minimum over its faces."""
+    n = 5
+    Q = np.ones((5, n, n, n))
+    Q[4] = 2.5
+    Q[0][:, :, 1] = 0.5
+    Q[0][:, :, 2] = 1.0
+    Q[0][:, :, 3] = 3.0
+    G = np.zeros((3, 5, n, n, n))
+    prob = oracle.Problem(n=(n, n, n), lo=(0, 0, 0), hi=(n, n, n), scheme=0, nonlinear=1)
+    W, dW, phi = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[0.5, 0, 0], [-0.5, 0, 0]]))
+    d1, d2, e2 = -0.5, -0.625, 0.3 ** 3
+    want = (d1 * d1 + e2 + 2 * d1 * d2) / (d1 * d1 + 2 * d2 * d2 + d1 * d2 + e2)
+    assert want == pytest.approx(0.902 / 1.37075, rel=1e-14)
+    assert phi[0] == pytest.approx(want, rel=1e-14)
+    assert np.all(phi[1:] == 1.0)
+    assert W[0, 0] == pytest.approx(1.0 + want * 0.625, rel=1e-14) and W[1, 0] == pytest.approx(1.0 - want * 0.625, rel=1e-14)
+    assert dW[0, 0, 0] == pytest.approx(want * 1.25, rel=1e-14)
+    # a smaller K sharpens the limiter: e2 -> 0 gives (D1^2 + 2 D1 D2) / (D1^2 + 2 D2^2 + D1 D2)
+    prob.k_venkat = 1e-6
+    _, _, phi0 = oracle.recon_eval(prob, Q, G, (2, 2, 2), np.array([[0.5, 0, 0]]))
+    assert phi0[0] == pytest.approx((0.25 + 0.625) / (0.25 + 0.78125 + 0.3125), rel=1e-12)
+
+
 def test_geno_chi_scale_closed_form():
     # chi_scale C divides zeta (R8): chi_C = 1 / (1 + (zeta_1 / C)^4), zeta_1 = (1/chi_1 - 1)^(1/4),
     # checked on a curved field where the sub-stencil contrast gives an intermediate chi
@@ -265,11 +293,19 @@ def test_geno_weights_known_ratios(r):
     # minus-x slope b with b^2 + 2 s^2 = 3 s^2 r  =>  b = s sqrt(3 r - 2)
     b = s * np.sqrt(3.0 * r - 2.0)
     prob, Q, G, c = _geno_block([b, s, s], [s, s, s], [s, s, s])
-    IS, om, _, _ = oracle.geno_cell(prob, Q, G, c)
+    IS, om, _, chi = oracle.geno_cell(prob, Q, G, c)
     assert np.allclose(IS[0] / IS[1], r, rtol=1e-13)
+    # R7: IS_m = sum of the squared reference slopes of sub-stencil m (component v scaled by scale[v])
+    scale = np.array([1.0, 0.5, 0.25, 0.125, 2.0])
+    assert np.allclose(IS[1], 3.0 * s * s * scale ** 2, rtol=1e-13)
     w0 = r ** -5 / (r ** -5 + 5.0)
     assert np.allclose(om[0], w0, rtol=1e-13), (om[0], w0)
     assert np.allclose(om[1:], 1.0 / (r ** -5 + 5.0), rtol=1e-13)
+    # R8 (the reading DESIGN.md adopts; the paper defers chi to its references): chi = 1 / (1 + zeta^4),
+    # zeta = (IS_max - IS_min) / (IS_min + eps + 0.01 IS_max) -- with IS_max = r IS_min a function of r alone
+    # (r = 2 gives chi = 0.52: the blend is half ENO already at a factor 2 between the indicators)
+    zeta = (r - 1.0) / (1.0 + 0.01 * r)
+    assert np.allclose(chi, 1.0 / (1.0 + zeta ** 4), rtol=1e-10), chi
 
 
 def test_geno_blend_value_1d_known_ratio():

@@ -189,3 +189,49 @@ def test_supersonic_tgv_runs_nonlinear():
         ek0 = (0.5 * (c.Q[1] ** 2 + c.Q[2] ** 2 + c.Q[3] ** 2) / c.Q[0]).sum()
         ek1 = (0.5 * (Q[1] ** 2 + Q[2] ** 2 + Q[3] ** 2) / Q[0]).sum()
         assert ek1 < ek0
+
+
+# ---- box boundary rules (R29: the paper runs its jets with boundary treatments it does not spell out; DESIGN.md
+# adopts x-low inflow = Dirichlet state with zero gradient, x-high = zero-order extrapolation, y periodic) ------
+def _box_problem(scheme, state_in, n=(8, 6, 1)):
+    bcs = np.zeros((3, 2, 5))
+    bcs[0, 0] = state_in
+    return oracle.Problem(n=n, lo=(0, 0, 0), hi=(float(n[0]), float(n[1]), 1.0), scheme=scheme, nonlinear=0,
+                          bc=((1, 2), (0, 0), (0, 0)), bc_state=bcs, mu=1e-3, Pr=0.72)
+
+
+@pytest.mark.parametrize("scheme", [1, 0])
+def test_box_uniform_flow_is_preserved(scheme):
+    # a uniform state equal to the inflow state passes through the box unchanged (Dirichlet ghost = interior
+    # state, extrapolated ghost = interior state): every ghost rule reproduces the uniform field
+    state = np.array([1.2, 1.2 * 0.8, 1.2 * 0.1, 0.0, 3.0])
+    prob = _box_problem(scheme, state)
+    n = prob.n
+    Q = np.tile(state[:, None, None, None], (1, n[2], n[1], n[0]))
+    G = np.zeros((3, 5, n[2], n[1], n[0]))
+    Q1, G1, t, _, rc = oracle.run(prob, Q, G, 5)
+    assert rc == 0 and t > 0
+    assert np.abs(Q1 - Q).max() <= 1e-14 * np.abs(Q).max()
+    assert np.abs(G1).max() <= 1e-13
+
+
+def test_box_ghost_rules_fix_the_boundary_slopes():
+    # GKS-2nd least-squares slope of the two boundary cells on data linear in x, q = 2 + 0.1 i:
+    # outflow ghost = the boundary cell itself (zero-order extrapolation), so the last cell's x slope is HALF the
+    # field's (a linear extrapolation would give all of it); inflow ghost = the Dirichlet state q_in, so the first
+    # cell's slope is (q_1 - q_in) / 2
+    state_in = np.array([1.7, 0.0, 0.0, 0.0, 5.0])
+    prob = _box_problem(0, state_in)
+    n = prob.n
+    Q = np.zeros((5, n[2], n[1], n[0]))
+    Q[0] = 2.0 + 0.1 * np.arange(n[0])[None, None, :]
+    Q[4] = 5.0
+    G = np.zeros((3, 5, n[2], n[1], n[0]))
+    x = np.array([[0.0, 0.0, 0.0]])
+    _, dW_hi, _ = oracle.recon_eval(prob, Q, G, (n[0] - 1, 2, 0), x)
+    _, dW_mid, _ = oracle.recon_eval(prob, Q, G, (3, 2, 0), x)
+    _, dW_lo, _ = oracle.recon_eval(prob, Q, G, (0, 2, 0), x)
+    assert dW_mid[0, 0, 0] == pytest.approx(0.1, rel=1e-13)
+    assert dW_hi[0, 0, 0] == pytest.approx(0.05, rel=1e-13)
+    assert dW_lo[0, 0, 0] == pytest.approx((2.1 - 1.7) / 2.0, rel=1e-13)
+    assert np.abs(dW_hi[0, 1]).max() <= 1e-15  # no y slope
