@@ -18,8 +18,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # (time-derivative-only) sweeps 2.4 / 4.5 / 5.3 % faster (x / y / z: 1.357 / 1.362 / 1.360 -> 1.325 / 1.300 /
 # 1.288 ms, 8 instead of 32-48 bytes of spills), the full sweeps unchanged, k_recon5 +1 %: TGV 128^3 10.47 ->
 # 10.29 ms/step (A/B on one box, levels 0-3 alike, 4 and 8 like the default); results bitwise equal
+# Only the 3-D translation unit takes it: the 2-D kernels lose 1-3 % (flux) and 10 % (recon2) with it; within the
+# 3-D unit GKS-2nd's recon2 is 15 % slower and its update 4 % faster (+0.7 % per GKS-2nd step)
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-Xptxas", "--register-usage-level=3"]
+         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+FLAGS_PER_SOURCE = {"stage_d3.cu": ["-Xptxas", "--register-usage-level=3"]}
 # experiment knobs (defaults are the tuned values): extra -D flags, alternate output name
 EXTRA = os.environ.get("CGKS_NVCC_DEFS", "").split()
 BUILD = os.path.join(HERE, "build")
@@ -45,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
     procs, objs = [], []
     for s in SOURCES:  # one process per translation unit, in parallel
         obj = os.path.join(BUILD, s + ".o")
-        cmd = [NVCC] + FLAGS + EXTRA + ["-c", os.path.join(CSRC, s), "-o", obj]
+        cmd = [NVCC] + FLAGS + FLAGS_PER_SOURCE.get(s, []) + EXTRA + ["-c", os.path.join(CSRC, s), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     text, failed = "", False
