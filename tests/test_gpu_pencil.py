@@ -190,3 +190,17 @@ def test_nccl_self_y_stretched_bitwise():
     Q1, G1, t1, _ = _single(case, 1, 0, 4, **kw)
     Qn, Gn, tn, _ = _nccl_self(case, 1, 0, 4, {"CGKS_TEST_SELF_Y": "1"}, **kw)
     assert t1 == tn and np.array_equal(Q1, Qn) and np.array_equal(G1, Gn)
+
+
+def test_pencil_config_errors():
+    # cgks_create refuses: a split x axis, rows not divisible by Py, fewer than 4 rows per rank, a bounded y axis
+    from paper_2508_19911_b200 import CgksError, Solver
+    case = random_smooth((16, 12, 16), seed=1)
+    for nproc in [(2, 1, 1), (1, 5, 1), (1, 4, 1), (1, 2, 3)]:  # 12 rows: 5 does not divide, 4 leaves 3 rows; 16 planes / 3
+        with pytest.raises(CgksError) as e:
+            Solver.from_case(case, scheme=1, nproc=nproc, rank=0)
+        assert e.value.code == 2  # CGKS_ERR_CONFIG
+    sv = cases.shock_vortex(64, 32)  # x is bounded: only y can be split, and y must be periodic
+    bc = ((0, 0), (1, 2), (0, 0))
+    with pytest.raises(CgksError):
+        Solver(sv.n, sv.lo, sv.hi, scheme=1, bc=bc, bc_state=sv.bc_state, nproc=(1, 2, 1), rank=0)
