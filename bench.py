@@ -104,10 +104,46 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.rows = []
+        self.source = "nvml"
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        """NVML handle of this rank's GPU (by the CUDA device's UUID; by index when the UUID is unavailable)."""
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _run_nvml(self):
+        """In-process NVML sampling every 10 ms (a 20-step region of 0.2 s yields ~20 samples; an nvidia-smi
+        process per sample yields one or two).  Rows in the nvidia-smi column order."""
+        nv, h = self._nvml_handle()
+        bits = [(0x8, 3), (0x40, 4), (0x20, 5), (0x4, 6)]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+            except Exception:
+                pw = float("nan")
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            row = [str(sm), str(mx), f"{pw:.1f}", "", "", "", ""]
+            for bit, col in bits:
+                row[col] = "Active" if (r & bit) else "Not Active"
+            self.rows.append(row)
+            self._stop.wait(0.01)
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -135,8 +171,10 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source,
+                "sm_mhz_min": min(sm) if sm else None, "power_w_max": max(pw) if pw else None}
 
 
 def dist_init():
